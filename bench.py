@@ -1,0 +1,395 @@
+#!/usr/bin/env python3
+"""Benchmark: THb/SO2 frames per second at 1080p, 2-level Haar (BASELINE.json
+config 3, "1920x1080 RGB frame, 2-level Haar, single B200 throughput sweep").
+
+One "step" = the hybrid hot path over one batch of `--batch` synthetic frames
+(frames already in HBM): low-pass chain -> fp64 EM -> fused per-pixel
+reconstruction + Beer-Lambert fit + THb/SO2.  Frames are independent, so
+multi-GPU runs (torchrun) shard frames with no data-path collective
+("scaling": "weak"): every rank processes its own batch; the step time is the
+max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`--impl reference` times the reference CPU implementation of the path (the
+pinned NumPy oracle port, oracle/oximap_oracle.py: the reference is pure
+Python and cannot travel to the GPU box) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "THb/SO2 frames/sec at 1080p, 2-level Haar"
+UNIT = "frames/s"
+WORKLOAD = "1920x1080 RGB, 2-level Haar, hybrid (Tikhonov detail + iterative Bayes LL), THb+SO2 maps"
+CPU_SAMPLE_FRAMES = 3
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--batch", type=int, default=32, help="frames per step per GPU")
+    p.add_argument("--height", type=int, default=1080)
+    p.add_argument("--width", type=int, default=1920)
+    p.add_argument("--levels", type=int, default=2)
+    p.add_argument("--texture", type=float, default=0.3, help="phantom texture_density")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def operators():
+    from paper_1706_07263_b200 import fixtures
+
+    return fixtures.default_sensitivity(), fixtures.default_basis()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        try:
+            for line in open(self.path):
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except OSError:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+# ---------------------------------------------------------------- inputs
+def make_frames(batch, H, W, texture, rank, device):
+    """(batch, H, W, 3) float32 phantom frames on `device`: 4 distinct truth
+    maps per rank (seeded), forward model + per-frame noise on the GPU."""
+    import torch
+
+    from paper_1706_07263_b200 import synth
+
+    sens, basis = operators()
+    out = torch.empty((batch, H, W, 3), dtype=torch.float32, device=device)
+    n_truth = min(4, batch)
+    per = -(-batch // n_truth)
+    for t in range(n_truth):
+        spec = synth.tissue_phantom_spec(H, W, seed=100 * rank + t, noise_sigma=0.0, texture_density=texture)
+        truth = synth.truth_map(spec)
+        lo, hi = t * per, min(batch, (t + 1) * per)
+        if lo < hi:
+            out[lo:hi] = synth.device_frames(truth, sens, basis, hi - lo, noise_sigma=0.01, seed=1000 * rank + t,
+                                             device=device)
+    return out
+
+
+# ---------------------------------------------------------------- cpu baseline
+def cpu_baseline(frames_host: np.ndarray, levels: int) -> dict:
+    """Oracle port on the host cores: threads = all cores, BLAS pinned to 1
+    thread each (the reference's fastest setting)."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import oximap_oracle as O
+
+    sens, basis = operators()
+    threads = O.default_threads()
+    with threadpool_limits(limits=1):
+        O.estimate_frame(frames_host[0].astype(np.float64)[:64, :64], sens.c, basis.xi, n_levels=levels)
+        t0 = time.perf_counter()
+        for f in frames_host:
+            O.estimate_frame(f.astype(np.float64), sens.c, basis.xi, n_levels=levels, threads=threads,
+                             want_cube=False)
+        dt = time.perf_counter() - t0
+    return {"value": len(frames_host) / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{len(frames_host)} x {frames_host.shape[1]}x{frames_host.shape[2]} frames, n={levels}, "
+                      f"hybrid via oracle/oximap_oracle.py (bit-identical to the reference), "
+                      f"threads={threads}, BLAS 1 thread", "seconds": dt}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1706_07263_b200 import synth
+
+    sens, basis = operators()
+    frames = [synth.phantom_rgb_f32(args.height, args.width, s, sens, basis, texture_density=args.texture)
+              .astype(np.float32) for s in range(2)]
+    from threadpoolctl import threadpool_limits
+
+    from oracle import oximap_oracle as O
+
+    threads = O.default_threads()
+    times = []
+    with threadpool_limits(limits=1):
+        for i in range(args.warmup + args.steps):
+            f = frames[i % 2].astype(np.float64)
+            t0 = time.perf_counter()
+            O.estimate_frame(f, sens.c, basis.xi, n_levels=args.levels, threads=threads, want_cube=False)
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+    total = sum(times)
+    value = len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "height": args.height, "width": args.width, "levels": args.levels,
+                   "frames_per_step": 1, "texture_density": args.texture},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"1 frame per step ({args.height}x{args.width}, n={args.levels}) through the "
+                                   "oracle port of the reference (bit-identical outputs), threads=all cores, BLAS 1"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- ours
+def probe_peaks(lib, torch, dev):
+    """Measured fp64-FMA and MUFU-lg2 pipe peaks on this GPU (probe.cu)."""
+    import ctypes
+
+    sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    sink64 = torch.zeros(256, dtype=torch.float64, device=dev)
+    sink32 = torch.zeros(256, dtype=torch.float32, device=dev)
+    out = {}
+    for name, fn, sink, iters in (("fp64_fma", lib.oxm_probe_fp64_fma, sink64, 400),
+                                  ("mufu_lg2", lib.oxm_probe_mufu_lg2, sink32, 400)):
+        ops = ctypes.c_double()
+        s = torch.cuda.current_stream()
+        best = float("inf")
+        for rep in range(4):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn(sm * 8, iters, sink.data_ptr(), ctypes.byref(ops), s.cuda_stream)
+            b.record()
+            b.synchronize()
+            if rep:
+                best = min(best, a.elapsed_time(b) * 1e-3)
+        out[name] = ops.value / best
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
+    torch.cuda.set_device(dev)
+
+    import paper_1706_07263_b200 as ox
+    from paper_1706_07263_b200 import _native
+
+    lib = _native.load()
+    sens, basis = operators()
+    H, W, n, B = args.height, args.width, args.levels, args.batch
+    eng = ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev)
+    frames = make_frames(B, H, W, args.texture, rank, dev)
+    out = eng.allocate(B, H, W, fits=True)
+    nll = B * (-(-H // 2**n)) * (-(-W // 2**n))
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        eng.launch(frames, out)
+    eng.check_flags(out)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        start.record(stream)
+        for k in range(args.steps):
+            eng.launch(frames, out, stage_events=ev[k])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed = start.elapsed_time(stop) * 1e-3
+    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_max = float(t.item())
+    stage_s = [statistics.mean(e[i].elapsed_time(e[i + 1]) * 1e-3 for e in ev) for i in range(3)]
+    fits_total = int(out.fits.sum().item())
+    eng.check_flags(out)
+    clocks = clk.summary()
+
+    # ---- end to end: pinned host frames -> maps in pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        host_in = frames.cpu().pin_memory()
+        thb_h = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
+        so2_h = torch.empty((B, H, W), dtype=torch.float32).pin_memory()
+        state = {}
+        chunk = 4
+        eng.maps_from_host(host_in, thb_h, so2_h, chunk=chunk, _state=state)  # warm
+        e2e_steps = max(2, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eng.maps_from_host(host_in, thb_h, so2_h, chunk=chunk, _state=state)
+        e2e_dt = time.perf_counter() - t0
+        te = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": UNIT,
+               "h2d_bytes_per_step": B * H * W * 3 * 4, "d2h_bytes_per_step": B * H * W * 2 * 4,
+               "steps": e2e_steps, "chunk_frames": chunk, "api": "HybridMapEngine.maps_from_host -> oxm_hybrid_maps_f32"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = probe_peaks(lib, torch, dev)
+    hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs") if (ROOT / "MEASURED_PEAKS.json").exists() else None
+    # per-stage algorithmic work
+    px = B * H * W
+    bytes_ll = px * 12 + nll * 3 * 8
+    bytes_px = px * 12 + px * 8 + nll * (26 + 3) * 8
+    flops_per_fit = 2 * DFMA_PER_FIT
+    em_flops = fits_total * flops_per_fit
+    stages = {
+        "ll_kernel": {"ms": stage_s[0] * 1e3, "GB/s": bytes_ll / stage_s[0] / 1e9},
+        "em_soa_kernel": {"ms": stage_s[1] * 1e3, "fits_per_coeff": fits_total / nll,
+                          "fp64_TFLOP/s": em_flops / stage_s[1] / 1e12},
+        "px_f32_kernel": {"ms": stage_s[2] * 1e3, "GB/s": bytes_px / stage_s[2] / 1e9,
+                          "lg2_T/s": px * 26 / stage_s[2] / 1e12},
+    }
+    dominant = max(range(3), key=lambda i: stage_s[i])
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(["ll_kernel", "em_soa_kernel", "px_f32_kernel"][dominant])
+    if dominant == 1:
+        peak = 2 * peaks["fp64_fma"] / 1e12
+        ach = em_flops / stage_s[1] / 1e12
+        roof = {"bound": "fp64", "kernel": "em_soa_kernel", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "traffic": traffic,
+                "peak_source": "measured in this run by oxm_probe_fp64_fma (MEASURED_PEAKS.json has no fp64 figure)",
+                "work": f"{DFMA_PER_FIT} fp64 FMA-equivalents per EM fit x {fits_total} fits"}
+    elif dominant == 2:
+        ach = bytes_px / stage_s[2] / 1e9
+        roof = {"bound": "hbm", "kernel": "px_f32_kernel", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm if hbm else None, "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        ach = bytes_ll / stage_s[0] / 1e9
+        roof = {"bound": "hbm", "kernel": "ll_kernel", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm if hbm else None, "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        sample = frames[:CPU_SAMPLE_FRAMES].cpu().numpy()
+        cpu = cpu_baseline(sample, n)
+
+    value = world * B * args.steps / elapsed_max
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64 EM + f32 per-pixel (f64 fallback)",
+        "data": "synthetic (tissue phantoms, seeded; forward model + noise on GPU)",
+        "config": {"workload": WORKLOAD, "height": H, "width": W, "levels": n, "frames_per_step_per_gpu": B,
+                   "global_batch": world * B, "texture_density": args.texture,
+                   "l2": f"inputs {B * H * W * 12 / 1e6:.0f} MB per step > 126 MB L2 (no flush needed)",
+                   "parallelism": f"frame-sharded x{world}, no data-path collective"},
+        "roofline": roof,
+        "stages": stages,
+        "probes": {"fp64_fma_T/s": peaks["fp64_fma"] / 1e12, "mufu_lg2_T/s": peaks["mufu_lg2"] / 1e12},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": HybridMapLaunches * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# fp64 FMA-equivalent operations per EM fit, counted from the em_soa_kernel
+# SASS loop body (tools/count_em_sass.py)
+DFMA_PER_FIT = 780
+HybridMapLaunches = 3
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * oximap_b200.h -- C ABI of the B200-native haemoglobin-map path.
+ *
+ * The reference (`oximap`, /root/reference/pkg/src/oximap) is pure Python and
+ * has no FFI layer: its boundary is the public Python API re-exported by
+ * pkg/src/oximap/__init__.py:10-80.  Every entry point below replaces the body
+ * of one of those Python functions (cited per function); a ctypes binding of
+ * this header is what `oximap` would call.
+ *
+ * Conventions
+ *  - Plain C types only: device pointers, element counts, a cudaStream_t passed
+ *    as `void*` (NULL = legacy default stream).  No torch types.
+ *  - All arrays are C-order.  Images/planes are HWC interleaved (H, W, C) like
+ *    the reference's NumPy arrays; per-coefficient vectors are (n, 3) / (n, L).
+ *  - Every function returns an `int` status (OXM_OK or a negative OXM_ERR_*).
+ *    Shape/config errors are returned before any launch.  Data-dependent
+ *    errors (non-finite input, negative low-pass) are detected on the device and
+ *    reported as bits in a caller-owned `uint32_t* flags` word that the caller
+ *    reads after synchronising the stream (the reference raises them eagerly,
+ *    haar.py:133-134, bayes.py:77-78).
+ *  - Launches are asynchronous on `stream`; the library holds no global
+ *    mutable state besides immutable operator contexts.
+ */
+#ifndef OXIMAP_B200_H
+#define OXIMAP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define OXM_API __attribute__((visibility("default")))
+#else
+#define OXM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OXM_ABI_VERSION 1
+#define OXM_MAX_BANDS 64 /* spectral bands L supported by the kernels */
+
+/* Status codes; the Python host maps them onto the reference exception
+ * classes of errors.py:1-30. */
+enum {
+  OXM_OK = 0,
+  OXM_ERR_ARGUMENT = -1,        /* ArgumentError                         */
+  OXM_ERR_DATA = -2,            /* DataError                             */
+  OXM_ERR_NUMERICAL = -3,       /* NumericalError                        */
+  OXM_ERR_SINGULAR = -4,        /* SingularOperatorError                 */
+  OXM_ERR_ILL_CONDITIONED = -5, /* IllConditionedPriorError              */
+  OXM_ERR_CUDA = -10,           /* CUDA runtime error (launch / device)  */
+  OXM_ERR_WORKSPACE = -11       /* workspace too small                   */
+};
+
+/* Device-side flag bits (OR-ed into *flags by the kernels). */
+#define OXM_FLAG_NONFINITE 1u   /* input sample not finite: haar.py:133-134, core.py:18-22 */
+#define OXM_FLAG_NEGATIVE_LL 2u /* low-pass coefficient < 0: bayes.py:77-78               */
+
+/* Host-side operator set (all float64, C-order).  Built by the Python host
+ * exactly as the reference builds them:
+ *   solve     L x 3  Tikhonov ridge inverse (C^T C + g I)^-1 C^T   unmix.py:53-74
+ *   fit_mat   3 x L  (xi^T xi)^-1 xi^T                             bayes.py:99-104
+ *   xi        L x 3  chromophore basis (hbo, hb, 1)                core.py:134-158
+ *   sens      3 x L  camera sensitivity C                          core.py:112-131
+ *   gain      L x 3  N^-1 C^T, N = C^T C + beta D2^T D2            bayes.py:117-129
+ * The shape-prior update N^-1 (C^T y + P e) of bayes.py:131-135 is evaluated
+ * as e + gain (y - C e), an exact identity because N^-1 P = I - N^-1 C^T C. */
+typedef struct oxm_operators {
+  int32_t n_bands;   /* L, 3 <= L <= OXM_MAX_BANDS   */
+  int32_t max_iters; /* BayesConfig.max_iters >= 1   */
+  double epsilon;    /* BayesConfig.epsilon in (0,1) */
+  double rel_tol;    /* BayesConfig.rel_tol > 0      */
+  double fallback_below; /* fp32 map path: recompute a pixel in fp64 when its
+                            smallest reconstructed band is below this       */
+  const double* solve;
+  const double* fit_mat;
+  const double* xi;
+  const double* sens;
+  const double* gain;
+} oxm_operators;
+
+typedef struct oxm_ctx oxm_ctx;
+
+/* ---- library ------------------------------------------------------------ */
+OXM_API int oxm_abi_version(void);
+OXM_API const char* oxm_status_string(int status);
+/* Last CUDA error string recorded by this thread (for OXM_ERR_CUDA). */
+OXM_API const char* oxm_last_error(void);
+
+/* Immutable per-device operator context.
+ * Replaces the per-call operator construction of pipeline.py:182 /
+ * bayes.py:239-240 (done once per (sensitivity, basis, config)). */
+OXM_API int oxm_ctx_create(int device, const oxm_operators* ops, oxm_ctx** out);
+OXM_API int oxm_ctx_destroy(oxm_ctx* ctx);
+
+/* ---- K1: multi-level Haar forward ---------------------------------------
+ * Replaces haar.forward (haar.py:120-142) incl. per-level edge replication
+ * (haar.py:80-85).  `planes` receives, for level k = 1..n (finest first), the
+ * four planes lp, dh, dv, dd of shape (h_k, w_k, C) back to back, where
+ * h_k = ceil(h_{k-1} / 2).  oxm_haar_layout gives h_k, w_k and the total
+ * element count.  Non-finite input sets OXM_FLAG_NONFINITE. */
+OXM_API int oxm_haar_layout(int64_t height, int64_t width, int n_levels,
+                    int64_t* level_hw /* n_levels x 2, may be NULL */,
+                    int64_t* total_elems_per_channel);
+OXM_API int oxm_haar_forward_f32(const float* image, int64_t height, int64_t width, int64_t channels,
+                         int n_levels, float* planes, uint32_t* flags, void* stream);
+OXM_API int oxm_haar_forward_f64(const double* image, int64_t height, int64_t width, int64_t channels,
+                         int n_levels, double* planes, uint32_t* flags, void* stream);
+
+/* ---- K2: multi-level Haar inverse ---------------------------------------
+ * Replaces haar.inverse (haar.py:104-117, 145-150).  `level_shapes` holds for
+ * each level k = 1..n (finest first) four int64: plane rows h_k, plane cols
+ * w_k, and the crop (orig rows, orig cols) of that level.  `dirs` packs dh, dv,
+ * dd of every level (finest first), each (h_k, w_k, C); `coarse_lp` is the
+ * residual low-pass (h_n, w_n, C).  Output (orig rows_1, orig cols_1, C).
+ * Inconsistent shapes return OXM_ERR_DATA (haar.py:105-109). */
+OXM_API int oxm_haar_inverse_f32(const float* coarse_lp, const float* dirs, const int64_t* level_shapes,
+                         int n_levels, int64_t channels, float* out, void* stream);
+OXM_API int oxm_haar_inverse_f64(const double* coarse_lp, const double* dirs, const int64_t* level_shapes,
+                         int n_levels, int64_t channels, double* out, void* stream);
+
+/* ---- K3: per-coefficient 3 -> L linear unmix ----------------------------
+ * Replaces tikhonov_unmix (unmix.py:77-82) and, with the min-norm matrix,
+ * lsq_unmix (unmix.py:21-37): out[i, :] = matrix (L x 3, host) @ rgb[i, :]. */
+OXM_API int oxm_unmix_f32(int n_bands, const double* matrix, const float* rgb, int64_t n, float* out,
+                  void* stream);
+OXM_API int oxm_unmix_f64(int n_bands, const double* matrix, const double* rgb, int64_t n, double* out,
+                  void* stream);
+
+/* ---- K4: iterative low-pass (shape-prior EM) estimator ------------------
+ * Replaces estimate_lowpass / _iterate_block (bayes.py:185-272).  `y` is the
+ * unit-scale low-pass data (n, 3) (rgb_lp / scale, bayes.py:237).  `init`
+ * (n, L) replaces the Tikhonov start when non-NULL (bayes.py:243-249).
+ * Outputs: spectra (n, L), x (n, 3) = (hbo, hb, offset) fit of spectra, and
+ * fits (n) = number of Beer-Lambert fits run for that coefficient (the
+ * discrete stopping decision of bayes.py:199-205), each may be NULL. */
+OXM_API int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double* init, int64_t n,
+                   double* spectra, double* x, int32_t* fits, void* stream);
+
+/* Shape-prior update for arbitrary (y, e) pairs: expectation_step
+ * (bayes.py:162-182), out (n, L) = N^-1 (C^T y + P e) (no clamp). */
+OXM_API int oxm_expectation_step(const oxm_ctx* ctx, const double* y, const double* e, int64_t n,
+                         double* out, void* stream);
+
+/* ---- K5: per-pixel Beer-Lambert fit -------------------------------------
+ * Replaces fit_cube (pipeline.py:66-94) / fit_concentration (bayes.py:138-151):
+ * x = -fit_mat log(max(s, eps)) then x * (cal, cal, 1).  Outputs planar
+ * hbo, hb, offset (n each); any may be NULL. */
+OXM_API int oxm_fit_f32(const oxm_ctx* ctx, const float* cube, int64_t n, double calibration,
+                float* hbo, float* hb, float* offset, void* stream);
+OXM_API int oxm_fit_f64(const oxm_ctx* ctx, const double* cube, int64_t n, double calibration,
+                double* hbo, double* hb, double* offset, void* stream);
+/* Beer-Lambert forward model exp(-xi x): expected_spectrum (bayes.py:154-159). */
+OXM_API int oxm_expected_spectrum_f64(const oxm_ctx* ctx, const double* x, int64_t n, double* out,
+                              void* stream);
+
+/* ---- K6: fused hybrid estimator (estimate_frame mode="hybrid") ----------
+ * Replaces pipeline.py:176-217 + fit_cube + ConcentrationMap.thb/sat_o2
+ * (core.py:197-209) for a batch of `batch` frames (batch, H, W, 3).
+ * Uses the exact collapse of the hybrid path: for pixel p in low-pass block
+ * b = (py >> n, px >> n),  cube(p) = S[b] + solve (rgb(p) - LL_n[b] / 2^n),
+ * with LL_n the recursively edge-replicated low-pass (haar.py:80-101) and
+ * S = the EM spectra of LL_n / 2^n (bayes.py:185-207).
+ * Workspace: oxm_hybrid_workspace_bytes(); any output pointer may be NULL.
+ * f32 variant: fp64 low-pass chain + fp64 EM, fp32 per-pixel stage with an
+ * fp64 recompute of pixels whose smallest band < ops.fallback_below.
+ * Outputs are planar (batch, H, W); fits is (batch, ceil(H/2^n), ceil(W/2^n)).
+ * stage_events: NULL, or 4 cudaEvent_t recorded on `stream` before the
+ * low-pass kernel, before the EM kernel, before the per-pixel kernel and after
+ * it (live per-kernel timing for the roofline report). */
+OXM_API size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, int64_t height,
+                                  int64_t width, int n_levels);
+OXM_API int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,
+                        int64_t width, int n_levels, double calibration, void* workspace,
+                        size_t workspace_bytes, float* thb, float* so2, float* hbo, float* hb,
+                        float* offset, int32_t* fits, uint32_t* flags, void* stream,
+                        void* const* stage_events);
+/* f64 variant used by the drop-in estimate_frame: everything in fp64, and the
+ * (H, W, L) spectral cube (pipeline.py:207-208) is produced when cube != NULL. */
+OXM_API int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, int64_t batch, int64_t height,
+                         int64_t width, int n_levels, double calibration, void* workspace,
+                         size_t workspace_bytes, double* cube, double* hbo, double* hb,
+                         double* offset, int32_t* fits, uint32_t* flags, void* stream,
+                         void* const* stage_events);
+
+/* ---- roofline probes ------------------------------------------------------
+ * Measure the pipe peaks the non-GEMM kernels are bound by, on this device:
+ * fp64 FMA throughput (EM) and fp32 MUFU lg2 throughput (per-pixel fit).
+ * Each launches `blocks` x 256 threads doing `iters` rounds of 8 independent
+ * chains; *ops_per_launch receives the operation count (FMA or lg2). */
+OXM_API int oxm_probe_fp64_fma(int blocks, int iters, double* sink, double* ops_per_launch, void* stream);
+OXM_API int oxm_probe_mufu_lg2(int blocks, int iters, float* sink, double* ops_per_launch, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* OXIMAP_B200_H */

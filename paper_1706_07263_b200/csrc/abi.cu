@@ -1,0 +1,94 @@
+// C-ABI plumbing: status strings, per-thread CUDA error text and the
+// immutable per-device operator context (include/oximap_b200.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "oxm_common.cuh"
+
+namespace oxm {
+
+static thread_local char g_last_error[256] = "";
+
+void set_last_error(const char* where, cudaError_t err) {
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s (%s)", where, cudaGetErrorString(err),
+                cudaGetErrorName(err));
+}
+
+}  // namespace oxm
+
+using namespace oxm;
+
+extern "C" int oxm_abi_version(void) { return OXM_ABI_VERSION; }
+
+extern "C" const char* oxm_last_error(void) { return g_last_error; }
+
+extern "C" const char* oxm_status_string(int status) {
+  switch (status) {
+    case OXM_OK: return "ok";
+    case OXM_ERR_ARGUMENT: return "argument error";
+    case OXM_ERR_DATA: return "data error";
+    case OXM_ERR_NUMERICAL: return "numerical error";
+    case OXM_ERR_SINGULAR: return "singular operator";
+    case OXM_ERR_ILL_CONDITIONED: return "ill-conditioned prior";
+    case OXM_ERR_CUDA: return "cuda error";
+    case OXM_ERR_WORKSPACE: return "workspace too small";
+    default: return "unknown status";
+  }
+}
+
+extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out) {
+  if (!o || !out) return OXM_ERR_ARGUMENT;
+  *out = nullptr;
+  const int L = o->n_bands;
+  // BayesConfig.__post_init__ domain (bayes.py:50-58)
+  if (L < 3 || L > kMaxBands) return OXM_ERR_ARGUMENT;
+  if (o->max_iters < 1) return OXM_ERR_ARGUMENT;
+  if (!(o->epsilon > 0.0 && o->epsilon < 1.0)) return OXM_ERR_ARGUMENT;
+  if (!(o->rel_tol > 0.0)) return OXM_ERR_ARGUMENT;
+  if (!o->solve || !o->fit_mat || !o->xi || !o->sens || !o->gain) return OXM_ERR_ARGUMENT;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    set_last_error("oxm_ctx_create", cudaErrorInvalidDevice);
+    cudaGetLastError();
+    return OXM_ERR_CUDA;
+  }
+  oxm_ctx* c = new (std::nothrow) oxm_ctx();
+  if (!c) return OXM_ERR_CUDA;
+  std::memset(static_cast<void*>(&c->ops), 0, sizeof(c->ops));
+  c->device = device;
+  DevOps& d = c->ops;
+  d.L = L;
+  d.max_iters = o->max_iters;
+  d.eps = o->epsilon;
+  d.rel_tol = o->rel_tol;
+  d.fallback_below = o->fallback_below;
+  d.eps_f = static_cast<float>(o->epsilon);
+  const double ln2 = 0.69314718055994530942;
+  for (int l = 0; l < L; ++l) {
+    for (int k = 0; k < 3; ++k) {
+      d.solve[l][k] = o->solve[3 * l + k];
+      d.xi[l][k] = o->xi[3 * l + k];
+      d.gain[l][k] = o->gain[3 * l + k];
+      d.fitm[k][l] = o->fit_mat[k * L + l];
+      d.sens[k][l] = o->sens[k * L + l];
+      d.solve_f[l][k] = static_cast<float>(d.solve[l][k]);
+      d.fitl2_f[k][l] = static_cast<float>(-ln2 * d.fitm[k][l]);
+    }
+  }
+  for (int l = 0; l < L; ++l)
+    for (int k = 0; k < 3; ++k)
+      if (!std::isfinite(d.solve[l][k]) || !std::isfinite(d.xi[l][k]) || !std::isfinite(d.gain[l][k]) ||
+          !std::isfinite(d.fitm[k][l]) || !std::isfinite(d.sens[k][l])) {
+        delete c;
+        return OXM_ERR_NUMERICAL;
+      }
+  *out = c;
+  return OXM_OK;
+}
+
+extern "C" int oxm_ctx_destroy(oxm_ctx* ctx) {
+  delete ctx;
+  return OXM_OK;
+}

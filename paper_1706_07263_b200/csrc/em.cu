@@ -1,0 +1,115 @@
+// K4: standalone low-pass estimator (estimate_lowpass, bayes.py:210-272) and
+// the shape-prior update for arbitrary (y, e) (expectation_step, bayes.py:162-182).
+//
+// One thread per coefficient; operators in constant bank 0.  Spectra are
+// written row-major (n, L) like the reference's return value; each thread's
+// row is staged through shared memory so the global stores are coalesced.
+#include "oxm_em.cuh"
+
+namespace oxm {
+namespace {
+
+constexpr int kEmThreads = 128;
+
+template <int KL>
+__global__ void __launch_bounds__(kEmThreads) em_lowpass_kernel(const __grid_constant__ DevOps ops,
+                                                                const double* __restrict__ y,
+                                                                const double* __restrict__ init, int64_t n,
+                                                                double* __restrict__ spectra,
+                                                                double* __restrict__ xout,
+                                                                int32_t* __restrict__ fits) {
+  constexpr int LM = BandCount<KL>::kMax;
+  const int L = BandCount<KL>::get(ops);
+  extern __shared__ double stage[];  // [kEmThreads][L]
+  const int64_t base = (int64_t)blockIdx.x * kEmThreads;
+  const int64_t i = base + threadIdx.x;
+  const bool live = i < n;
+  double* row = stage + (int64_t)threadIdx.x * L;
+  if (live) {
+    const double y0 = y[3 * i + 0], y1 = y[3 * i + 1], y2 = y[3 * i + 2];
+    double x0, x1, x2;
+    int nf;
+    em_coefficient<KL>(ops, y0, y1, y2, init ? init + i * L : nullptr, x0, x1, x2, nf,
+                       [&](int l, double v) { row[l] = v; });
+    if (xout) {
+      xout[3 * i + 0] = x0;
+      xout[3 * i + 1] = x1;
+      xout[3 * i + 2] = x2;
+    }
+    if (fits) fits[i] = nf;
+  }
+  (void)LM;
+  if (spectra) {
+    __syncthreads();
+    const int64_t cnt = min64(kEmThreads, n - base);
+    const int64_t tot = cnt * L;
+    double* dst = spectra + base * L;
+    for (int64_t k = threadIdx.x; k < tot; k += kEmThreads) dst[k] = stage[k];
+  }
+}
+
+template <int KL>
+__global__ void __launch_bounds__(kEmThreads) expectation_kernel(const __grid_constant__ DevOps ops,
+                                                                 const double* __restrict__ y,
+                                                                 const double* __restrict__ e, int64_t n,
+                                                                 double* __restrict__ out) {
+  constexpr int LM = BandCount<KL>::kMax;
+  const int L = BandCount<KL>::get(ops);
+  const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
+  if (i >= n) return;
+  const double* ei = e + i * L;
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll(KL > 0 ? LM : 1)
+  for (int l = 0; l < LM; ++l) {
+    if (KL == 0 && l >= L) break;
+    const double el = ei[l];
+    c0 = fma(ops.sens[0][l], el, c0);
+    c1 = fma(ops.sens[1][l], el, c1);
+    c2 = fma(ops.sens[2][l], el, c2);
+  }
+  const double r0 = y[3 * i] - c0, r1 = y[3 * i + 1] - c1, r2 = y[3 * i + 2] - c2;
+#pragma unroll(KL > 0 ? LM : 1)
+  for (int l = 0; l < LM; ++l) {
+    if (KL == 0 && l >= L) break;
+    out[i * L + l] = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, ei[l])));
+  }
+}
+
+}  // namespace
+}  // namespace oxm
+
+using namespace oxm;
+
+extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double* init, int64_t n, double* spectra,
+                              double* x, int32_t* fits, void* stream) {
+  if (!ctx || n < 0 || (n > 0 && !y)) return OXM_ERR_ARGUMENT;
+  if (n == 0) return OXM_OK;
+  DeviceGuard dg(ctx->device);
+  const int L = ctx->ops.L;
+  const size_t smem = sizeof(double) * kEmThreads * L;
+  const unsigned grid = grid_1d(n, kEmThreads);
+  cudaStream_t s = as_stream(stream);
+  if (L == 26) {
+    em_lowpass_kernel<26><<<grid, kEmThreads, smem, s>>>(ctx->ops, y, init, n, spectra, x, fits);
+  } else {
+    if (smem > 48 * 1024) {
+      cudaFuncSetAttribute(em_lowpass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    em_lowpass_kernel<0><<<grid, kEmThreads, smem, s>>>(ctx->ops, y, init, n, spectra, x, fits);
+  }
+  return check_launch("em_lowpass");
+}
+
+extern "C" int oxm_expectation_step(const oxm_ctx* ctx, const double* y, const double* e, int64_t n, double* out,
+                                    void* stream) {
+  if (!ctx || n < 0 || (n > 0 && (!y || !e || !out))) return OXM_ERR_ARGUMENT;
+  if (n == 0) return OXM_OK;
+  DeviceGuard dg(ctx->device);
+  const unsigned grid = grid_1d(n, kEmThreads);
+  cudaStream_t s = as_stream(stream);
+  if (ctx->ops.L == 26)
+    expectation_kernel<26><<<grid, kEmThreads, 0, s>>>(ctx->ops, y, e, n, out);
+  else
+    expectation_kernel<0><<<grid, kEmThreads, 0, s>>>(ctx->ops, y, e, n, out);
+  return check_launch("expectation_step");
+}

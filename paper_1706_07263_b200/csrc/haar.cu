@@ -1,0 +1,318 @@
+// K1 / K2: fused multi-level 2D Haar forward and inverse (fp32 and fp64).
+//
+// Reference semantics: haar.py:24-33 (orthonormal 4x4 window matrix, window
+// order TL,TR,BL,BR = a,b,c,d), haar.py:80-85 (per-level right/bottom edge
+// replication of odd planes), haar.py:88-101 (lp,dh,dv,dd), haar.py:104-117
+// (inverse butterflies + crop to orig_shape), haar.py:120-150 (recursion).
+//
+// Design: one thread owns one (coarsest-position, channel) column of the
+// pyramid for a pass of up to 3 levels, i.e. a 2^NL x 2^NL pixel block of one
+// channel, held entirely in registers.  The frame is read exactly once per
+// pass and every coefficient written once; adjacent threads own adjacent
+// channels / blocks so HWC loads and stores stay sector-contiguous per warp.
+// Deeper pyramids chain passes through the coarsest low-pass plane (which
+// the reference returns anyway).  The add order matches NumPy's left-to-right
+// evaluation of `0.5 * (a + b - c - d)` so fp64 results are bit-identical.
+#include <algorithm>
+
+#include "oxm_common.cuh"
+
+namespace oxm {
+namespace {
+
+constexpr int kMaxPass = 3;  // levels fused per pass
+
+struct FwdGeom {
+  int64_t C;
+  int64_t h[kMaxPass + 1], w[kMaxPass + 1];  // [0] = source plane dims
+  int64_t off[kMaxPass + 1][4];              // element offsets of lp,dh,dv,dd per level (1..NL)
+};
+
+template <typename T>
+__device__ __forceinline__ bool is_bad(T v) {
+  return !isfinite(v);
+}
+
+template <typename T, int NL>
+__global__ void __launch_bounds__(256) haar_fwd_kernel(const T* __restrict__ src, FwdGeom g,
+                                                       T* __restrict__ out, uint32_t* flags) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t C = g.C;
+  const int64_t total = g.h[NL] * g.w[NL] * C;
+  if (t >= total) return;
+  const int64_t c = t % C;
+  const int64_t rest = t / C;
+  const int64_t J = rest % g.w[NL];
+  const int64_t I = rest / g.w[NL];
+  constexpr int S0 = 1 << NL;
+
+  T p[S0][S0];
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < S0; ++r) {
+    const int64_t row = min(I * S0 + r, g.h[0] - 1);
+#pragma unroll
+    for (int s = 0; s < S0; ++s) {
+      const int64_t col = min(J * S0 + s, g.w[0] - 1);
+      const T v = ldg(src + (row * g.w[0] + col) * C + c);
+      bad |= is_bad(v);
+      p[r][s] = v;
+    }
+  }
+  if (bad && flags) atomicOr(flags, OXM_FLAG_NONFINITE);
+
+#pragma unroll
+  for (int k = 0; k < NL; ++k) {
+    const int Sk = S0 >> k;
+    const int Sn = Sk >> 1;
+    const int64_t br = I * Sk, bc = J * Sk;  // global position of p[0][0] at level k
+    const int64_t hn = g.h[k + 1], wn = g.w[k + 1];
+#pragma unroll
+    for (int i = 0; i < Sn; ++i) {
+#pragma unroll
+      for (int j = 0; j < Sn; ++j) {
+        // edge replication: the odd partner row/col falls back to its twin
+        const bool rowok = br + 2 * i + 1 < g.h[k];
+        const bool colok = bc + 2 * j + 1 < g.w[k];
+        const T a = p[2 * i][2 * j];
+        const T b = colok ? p[2 * i][2 * j + 1] : a;
+        const T cc = rowok ? p[2 * i + 1][2 * j] : a;
+        const T d = rowok ? (colok ? p[2 * i + 1][2 * j + 1] : cc) : b;
+        const T lp = T(0.5) * (((a + b) + cc) + d);
+        const T dh = T(0.5) * (((a + b) - cc) - d);
+        const T dv = T(0.5) * (((a - b) - cc) + d);
+        const T dd = T(0.5) * (((a - b) + cc) - d);
+        const int64_t gi = (br >> 1) + i, gj = (bc >> 1) + j;
+        if (gi < hn && gj < wn) {
+          const int64_t e = (gi * wn + gj) * C + c;
+          out[g.off[k + 1][0] + e] = lp;
+          out[g.off[k + 1][1] + e] = dh;
+          out[g.off[k + 1][2] + e] = dv;
+          out[g.off[k + 1][3] + e] = dd;
+        }
+        p[i][j] = lp;  // (i,j) <= (2i,2j): only already-consumed windows are overwritten
+      }
+    }
+  }
+}
+
+struct InvGeom {
+  int64_t C;
+  int64_t h[kMaxPass + 1], w[kMaxPass + 1];  // [l] = dims of the level-l low-pass / dir planes; [0] = output
+  int64_t off[kMaxPass + 1][3];              // dh,dv,dd element offsets at level l (1..NL)
+};
+
+template <typename T, int NL>
+__global__ void __launch_bounds__(256) haar_inv_kernel(const T* __restrict__ top, const T* __restrict__ dirs,
+                                                       InvGeom g, T* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t C = g.C;
+  const int64_t total = g.h[NL] * g.w[NL] * C;
+  if (t >= total) return;
+  const int64_t c = t % C;
+  const int64_t rest = t / C;
+  const int64_t J = rest % g.w[NL];
+  const int64_t I = rest / g.w[NL];
+  constexpr int S0 = 1 << NL;
+
+  T p[S0][S0];
+  p[0][0] = ldg(top + (I * g.w[NL] + J) * C + c);
+#pragma unroll
+  for (int l = NL; l >= 1; --l) {
+    const int Sl = 1 << (NL - l);  // positions per side owned at level l
+    const int64_t br = I * Sl, bc = J * Sl;
+    const int64_t hl = g.h[l], wl = g.w[l];
+    const int64_t ho = g.h[l - 1], wo = g.w[l - 1];
+    // walk backwards so in-place expansion never overwrites an unread parent
+#pragma unroll
+    for (int i = Sl - 1; i >= 0; --i) {
+#pragma unroll
+      for (int j = Sl - 1; j >= 0; --j) {
+        const int64_t gi = br + i, gj = bc + j;
+        T lp = p[i][j], dh = T(0), dv = T(0), dd = T(0);
+        if (gi < hl && gj < wl) {
+          const int64_t e = (gi * wl + gj) * C + c;
+          dh = ldg(dirs + g.off[l][0] + e);
+          dv = ldg(dirs + g.off[l][1] + e);
+          dd = ldg(dirs + g.off[l][2] + e);
+        }
+        const T o00 = T(0.5) * (((lp + dh) + dv) + dd);
+        const T o01 = T(0.5) * (((lp + dh) - dv) - dd);
+        const T o10 = T(0.5) * (((lp - dh) - dv) + dd);
+        const T o11 = T(0.5) * (((lp - dh) + dv) - dd);
+        if (l == 1) {
+          const int64_t r0 = 2 * gi, c0 = 2 * gj;
+          if (r0 < ho) {
+            if (c0 < wo) out[(r0 * wo + c0) * C + c] = o00;
+            if (c0 + 1 < wo) out[(r0 * wo + c0 + 1) * C + c] = o01;
+          }
+          if (r0 + 1 < ho) {
+            if (c0 < wo) out[((r0 + 1) * wo + c0) * C + c] = o10;
+            if (c0 + 1 < wo) out[((r0 + 1) * wo + c0 + 1) * C + c] = o11;
+          }
+        } else {
+          p[2 * i][2 * j] = o00;
+          p[2 * i][2 * j + 1] = o01;
+          p[2 * i + 1][2 * j] = o10;
+          p[2 * i + 1][2 * j + 1] = o11;
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+int haar_forward_impl(const T* image, int64_t H, int64_t W, int64_t C, int n, T* planes, uint32_t* flags,
+                      cudaStream_t stream) {
+  if (n < 1 || H < 1 || W < 1 || C < 1) return OXM_ERR_ARGUMENT;
+  if (!image || !planes) return OXM_ERR_ARGUMENT;
+  // dims and plane offsets of every level
+  int64_t hh = H, ww = W, off = 0;
+  const T* src = image;
+  int64_t level = 0;  // levels done
+  while (level < n) {
+    const int NL = static_cast<int>(min64(kMaxPass, n - level));
+    FwdGeom g{};
+    g.C = C;
+    g.h[0] = hh;
+    g.w[0] = ww;
+    for (int k = 1; k <= NL; ++k) {
+      g.h[k] = (g.h[k - 1] + 1) / 2;
+      g.w[k] = (g.w[k - 1] + 1) / 2;
+      const int64_t sz = g.h[k] * g.w[k] * C;
+      for (int q = 0; q < 4; ++q) g.off[k][q] = off + q * sz;
+      off += 4 * sz;
+    }
+    const int64_t total = g.h[NL] * g.w[NL] * C;
+    const int threads = 128;
+    const unsigned grid = grid_1d(total, threads);
+    switch (NL) {
+      case 1: haar_fwd_kernel<T, 1><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+      case 2: haar_fwd_kernel<T, 2><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+      default: haar_fwd_kernel<T, 3><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+    }
+    int st = check_launch("haar_forward");
+    if (st) return st;
+    // next pass starts from this pass's coarsest low-pass plane
+    src = planes + g.off[NL][0];
+    hh = g.h[NL];
+    ww = g.w[NL];
+    level += NL;
+  }
+  return OXM_OK;
+}
+
+template <typename T>
+int haar_inverse_impl(const T* coarse_lp, const T* dirs, const int64_t* shp, int n, int64_t C, T* out,
+                      cudaStream_t stream) {
+  if (n < 1 || C < 1 || !coarse_lp || !dirs || !out || !shp) return OXM_ERR_ARGUMENT;
+  // validate the chain: level k planes (h_k, w_k); crop (oh_k, ow_k) <= 2*(h_k, w_k) effectively;
+  // level k-1's planes must equal level k's crop (haar.py:105-109).
+  int64_t eff_h[64], eff_w[64];
+  if (n > 60) return OXM_ERR_ARGUMENT;
+  for (int k = 0; k < n; ++k) {
+    const int64_t h = shp[4 * k + 0], w = shp[4 * k + 1], oh = shp[4 * k + 2], ow = shp[4 * k + 3];
+    if (h < 1 || w < 1 || oh < 0 || ow < 0) return OXM_ERR_DATA;
+    eff_h[k] = std::min(oh, 2 * h);  // numpy slicing clamps out[:oh, :ow]
+    eff_w[k] = std::min(ow, 2 * w);
+    if (k > 0 && (shp[4 * (k - 1) + 0] != eff_h[k] || shp[4 * (k - 1) + 1] != eff_w[k])) return OXM_ERR_DATA;
+  }
+  if (eff_h[0] < 1 || eff_w[0] < 1) return OXM_ERR_DATA;
+  // element offsets of each level's dh,dv,dd in the packed dirs buffer
+  int64_t doff[64];
+  int64_t acc = 0;
+  for (int k = 0; k < n; ++k) {
+    doff[k] = acc;
+    acc += 3 * shp[4 * k] * shp[4 * k + 1] * C;
+  }
+  // passes from the coarsest level down; intermediate low-pass planes live in
+  // stream-ordered scratch that is released right after its consumer launch
+  const T* top = coarse_lp;
+  T* prev_scratch = nullptr;
+  int hi = n;  // levels hi .. lo+1 handled by this pass (1-based)
+  int st = OXM_OK;
+  while (hi > 0) {
+    const int NLc = std::min(kMaxPass, hi);
+    const int lo = hi - NLc;
+    InvGeom g{};
+    g.C = C;
+    for (int l = 1; l <= NLc; ++l) {
+      const int k = lo + l - 1;  // 0-based pyramid level index
+      g.h[l] = shp[4 * k];
+      g.w[l] = shp[4 * k + 1];
+      for (int q = 0; q < 3; ++q) g.off[l][q] = doff[k] + q * g.h[l] * g.w[l] * C;
+    }
+    g.h[0] = eff_h[lo];
+    g.w[0] = eff_w[lo];
+    T* dst = out;
+    T* new_scratch = nullptr;
+    if (lo > 0) {
+      const size_t bytes = sizeof(T) * (size_t)(g.h[0] * g.w[0] * C);
+      cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&new_scratch), bytes, stream);
+      if (err != cudaSuccess) {
+        set_last_error("haar_inverse scratch", err);
+        st = OXM_ERR_CUDA;
+        break;
+      }
+      dst = new_scratch;
+    }
+    const int64_t total = g.h[NLc] * g.w[NLc] * C;
+    const int threads = 128;
+    const unsigned grid = grid_1d(total, threads);
+    switch (NLc) {
+      case 1: haar_inv_kernel<T, 1><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+      case 2: haar_inv_kernel<T, 2><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+      default: haar_inv_kernel<T, 3><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+    }
+    st = check_launch("haar_inverse");
+    if (prev_scratch) cudaFreeAsync(prev_scratch, stream);
+    prev_scratch = new_scratch;
+    if (st) break;
+    top = dst;
+    hi = lo;
+  }
+  if (prev_scratch) cudaFreeAsync(prev_scratch, stream);
+  return st;
+}
+
+}  // namespace
+}  // namespace oxm
+
+using namespace oxm;
+
+extern "C" int oxm_haar_layout(int64_t height, int64_t width, int n_levels, int64_t* level_hw,
+                               int64_t* total_elems_per_channel) {
+  if (n_levels < 1 || height < 1 || width < 1) return OXM_ERR_ARGUMENT;
+  int64_t h = height, w = width, tot = 0;
+  for (int k = 0; k < n_levels; ++k) {
+    h = (h + 1) / 2;
+    w = (w + 1) / 2;
+    if (level_hw) {
+      level_hw[2 * k] = h;
+      level_hw[2 * k + 1] = w;
+    }
+    tot += 4 * h * w;
+  }
+  if (total_elems_per_channel) *total_elems_per_channel = tot;
+  return OXM_OK;
+}
+
+extern "C" int oxm_haar_forward_f32(const float* image, int64_t height, int64_t width, int64_t channels,
+                                    int n_levels, float* planes, uint32_t* flags, void* stream) {
+  return haar_forward_impl<float>(image, height, width, channels, n_levels, planes, flags, as_stream(stream));
+}
+
+extern "C" int oxm_haar_forward_f64(const double* image, int64_t height, int64_t width, int64_t channels,
+                                    int n_levels, double* planes, uint32_t* flags, void* stream) {
+  return haar_forward_impl<double>(image, height, width, channels, n_levels, planes, flags, as_stream(stream));
+}
+
+extern "C" int oxm_haar_inverse_f32(const float* coarse_lp, const float* dirs, const int64_t* level_shapes,
+                                    int n_levels, int64_t channels, float* out, void* stream) {
+  return haar_inverse_impl<float>(coarse_lp, dirs, level_shapes, n_levels, channels, out, as_stream(stream));
+}
+
+extern "C" int oxm_haar_inverse_f64(const double* coarse_lp, const double* dirs, const int64_t* level_shapes,
+                                    int n_levels, int64_t channels, double* out, void* stream) {
+  return haar_inverse_impl<double>(coarse_lp, dirs, level_shapes, n_levels, channels, out, as_stream(stream));
+}

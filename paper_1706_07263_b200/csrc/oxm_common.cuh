@@ -1,0 +1,89 @@
+// Shared definitions for the sm_100a kernels behind include/oximap_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "oximap_b200.h"
+
+namespace oxm {
+
+constexpr int kMaxBands = OXM_MAX_BANDS;
+
+// Operator set passed BY VALUE as a __grid_constant__ kernel parameter, so it
+// lives in constant bank 0 and every FMA below takes its matrix entry as a
+// c[0x0][...] operand (uniform across the warp, no LDS/LDG).  ~9.3 KB, well
+// under the 32 KB kernel-parameter limit of CUDA >= 12.1.
+struct DevOps {
+  int L;
+  int max_iters;
+  double eps;
+  double rel_tol;
+  double fallback_below;
+  double solve[kMaxBands][3];  // Tikhonov ridge inverse, unmix.py:53-65
+  double fitm[3][kMaxBands];   // (xi^T xi)^-1 xi^T, bayes.py:102
+  double xi[kMaxBands][3];     // chromophore basis, core.py:134-158
+  double sens[3][kMaxBands];   // camera matrix C, core.py:112-131
+  double gain[kMaxBands][3];   // N^-1 C^T, N = C^T C + beta D2^T D2 (bayes.py:117-129)
+  float solve_f[kMaxBands][3];
+  float fitl2_f[3][kMaxBands];  // -ln(2) * fit_mat: x = sum_l fitl2 * log2(s)
+  float eps_f;
+};
+
+struct oxm_ctx_impl {
+  int device;
+  DevOps ops;
+};
+
+// Per-thread error text for OXM_ERR_CUDA.
+void set_last_error(const char* where, cudaError_t err);
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = (cudaSetDevice(dev) == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline int check_launch(const char* where) {
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) {
+    set_last_error(where, err);
+    return OXM_ERR_CUDA;
+  }
+  return OXM_OK;
+}
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+__host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+inline unsigned grid_1d(int64_t n, int threads) {
+  int64_t g = ceil_div(n, threads);
+  return static_cast<unsigned>(g < 1 ? 1 : g);
+}
+
+__device__ __forceinline__ bool finite_d(double v) { return isfinite(v); }
+
+// Quiet NaN used for the SO2 "THb == 0" sentinel (core.py:202-209).
+__device__ __forceinline__ float qnan_f() { return __int_as_float(0x7fc00000); }
+
+// ld.global.nc: read-only streaming loads for frames / cubes.
+template <typename T>
+__device__ __forceinline__ T ldg(const T* p) {
+  return __ldg(p);
+}
+
+}  // namespace oxm
+
+struct oxm_ctx : oxm::oxm_ctx_impl {};

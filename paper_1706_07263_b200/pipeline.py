@@ -1,0 +1,216 @@
+"""End-to-end frame estimators -- drop-in for oximap.pipeline (pipeline.py:1-245).
+
+``estimate_frame(mode="hybrid")`` is the north-star hot path.  Here it runs
+the fused K6 kernels (``oxm_hybrid_frame_f64``): fp64 low-pass chain, fp64
+EM, and an fp64 per-pixel reconstruction + fit that also materialises the
+(H, W, L) SpectralCube the API returns.  The throughput path for video
+batches (fp32 maps, no cube) is ``engine.HybridMapEngine``.
+
+The other modes reuse the same kernels: ``tikhonov_only`` = K3 + K5,
+``bayes_only`` = K4 at full resolution + K5, ``direct_msi`` = K5.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import Iterable, Iterator
+
+import numpy as np
+import torch
+
+from . import _native
+from .bayes import BayesConfig, LowPassBlock, em_device, em_operator_set, fit_device
+from .core import ChromophoreBasis, CameraSensitivity, ConcentrationMap, RgbImage, SpectralCube, check_grids
+from .device import download, ptr, require_cuda, stream_handle, upload
+from .errors import ArgumentError, DataError
+from .haar import level_dims
+from .operators import OperatorSet, context, make_operator_set
+from .unmix import TikhonovOperator, apply_matrix_device
+
+MODES = ("hybrid", "tikhonov_only", "bayes_only", "direct_msi")
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    """Pipeline knobs (pipeline.py:44-63); ``threads`` is accepted and ignored
+    by the GPU path."""
+
+    mode: str = "hybrid"
+    n_levels: int = 1
+    tikhonov_gamma: float = 1e-3  # relative: scaled by trace(C^T C) / L
+    bayes: BayesConfig = field(default_factory=BayesConfig)
+    threads: int = 1
+    calibration_scale: float = 1.0
+
+    def __post_init__(self):
+        if self.mode not in MODES:
+            raise ArgumentError(f"mode must be one of {MODES}, got {self.mode!r}")
+        if self.n_levels < 1:
+            raise ArgumentError(f"n_levels must be >= 1, got {self.n_levels}")
+        if not self.tikhonov_gamma > 0:
+            raise ArgumentError(f"tikhonov_gamma must be > 0, got {self.tikhonov_gamma}")
+        if self.threads < 1:
+            raise ArgumentError(f"threads must be >= 1, got {self.threads}")
+        if not self.calibration_scale > 0:
+            raise ArgumentError(f"calibration_scale must be > 0, got {self.calibration_scale}")
+
+
+def _map_from_planes(x: np.ndarray, h: int, w: int) -> ConcentrationMap:
+    return ConcentrationMap(hbo=x[:, 0].reshape(h, w), hb=x[:, 1].reshape(h, w), offset=x[:, 2].reshape(h, w))
+
+
+def fit_cube(
+    cube: SpectralCube,
+    basis: ChromophoreBasis,
+    *,
+    epsilon: float = 1e-6,
+    calibration_scale: float = 1.0,
+    threads: int = 1,
+) -> ConcentrationMap:
+    """Per-pixel Beer-Lambert fit (pipeline.py:66-94) on the GPU (K5, fp64)."""
+    del threads
+    check_grids(cube.grid, basis.grid)
+    h, w, L = cube.data.shape
+    if h * w == 0:
+        z = np.zeros((h, w))
+        return ConcentrationMap(hbo=z, hb=z, offset=z)
+    ops = make_operator_set(n_bands=L, xi=basis.xi, epsilon=epsilon)
+    x = fit_device(upload(cube.data.reshape(-1, L), torch.float64, require_cuda()), ops, calibration_scale)
+    return _map_from_planes(download(x), h, w)
+
+
+def hybrid_device(
+    frames: torch.Tensor,
+    ops: OperatorSet,
+    n_levels: int,
+    calibration: float,
+    *,
+    want_cube: bool = True,
+    stream=None,
+) -> dict:
+    """K6 (fp64) on a device batch (B, H, W, 3) float64.  Returns device
+    tensors cube (B, H, W, L) | None, x (3, B, H, W), fits (B, hL, wL).
+    Raises ArgumentError on size / negative low-pass like pipeline.py:177-193."""
+    lib = _native.load()
+    frames = frames.contiguous()
+    B, H, W, _ = frames.shape
+    if H < 2**n_levels or W < 2**n_levels:
+        raise ArgumentError(f"frame {H}x{W} is smaller than 2^{n_levels} in one dimension")
+    hL, wL = level_dims(H, W, n_levels)[-1]
+    L = ops.n_bands
+    dev = frames.device
+    ctx = context(ops, dev.index)
+    ws_bytes = int(lib.oxm_hybrid_workspace_bytes(ctx.handle, B, H, W, n_levels))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    cube = torch.empty((B, H, W, L), dtype=torch.float64, device=dev) if want_cube else None
+    x = torch.empty((3, B, H, W), dtype=torch.float64, device=dev)
+    fits = torch.empty((B, hL, wL), dtype=torch.int32, device=dev)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = lib.oxm_hybrid_frame_f64(
+        ctx.handle, ptr(frames), B, H, W, n_levels, float(calibration), ptr(ws), ws_bytes,
+        ptr(cube), ptr(x[0]), ptr(x[1]), ptr(x[2]), ptr(fits), ptr(flags), stream_handle(stream), None,
+    )
+    _native.check(st, "hybrid_frame_f64")
+    f = int(flags.item())
+    if f & _native.FLAG_NONFINITE:
+        raise ArgumentError("image contains non-finite values")
+    if f & _native.FLAG_NEGATIVE_LL:
+        raise ArgumentError("low-pass coefficients must be finite and non-negative")
+    return {"cube": cube, "x": x, "fits": fits}
+
+
+def _hybrid_operators(sensitivity, basis, cfg: PipelineConfig) -> OperatorSet:
+    op = TikhonovOperator.from_relative(sensitivity, cfg.tikhonov_gamma)
+    return em_operator_set(sensitivity, basis, cfg.bayes, op)
+
+
+def estimate_frame(
+    frame: RgbImage | SpectralCube,
+    sensitivity: CameraSensitivity,
+    basis: ChromophoreBasis,
+    cfg: PipelineConfig,
+    stats: dict | None = None,
+) -> tuple[SpectralCube, ConcentrationMap]:
+    """Surrogate spectral cube + concentration map of one frame
+    (pipeline.py:117-217)."""
+    check_grids(sensitivity.grid, basis.grid)
+    if stats is not None:
+        stats.clear()
+    grid = sensitivity.grid
+    L = grid.count
+    eps, cal = cfg.bayes.epsilon, cfg.calibration_scale
+
+    if cfg.mode == "direct_msi":
+        if not isinstance(frame, SpectralCube):
+            raise ArgumentError("direct_msi mode takes a SpectralCube frame")
+        check_grids(frame.grid, basis.grid)
+        cmap = fit_cube(frame, basis, epsilon=eps, calibration_scale=cal)
+        if stats is not None:
+            stats.update(bayes_coefficients=0, tikhonov_coefficients=0)
+        return frame, cmap
+
+    if not isinstance(frame, RgbImage):
+        raise ArgumentError(f"{cfg.mode} mode takes an RgbImage frame")
+    H, W = frame.height, frame.width
+    dev = require_cuda()
+
+    if cfg.mode == "bayes_only":
+        LowPassBlock(rgb_lp=frame.data, scale=1.0)  # same non-negativity contract (bayes.py:77-78)
+        ops = _hybrid_operators(sensitivity, basis, cfg)
+        spectra, _, _ = em_device(upload(frame.data.reshape(-1, 3), torch.float64, dev), ops)
+        x = fit_device(spectra, ops, cal)
+        cube = SpectralCube(grid=grid, data=download(spectra).reshape(H, W, L))
+        if stats is not None:
+            stats.update(bayes_coefficients=H * W, tikhonov_coefficients=0)
+        return cube, _map_from_planes(download(x), H, W)
+
+    if H < 2**cfg.n_levels or W < 2**cfg.n_levels:
+        raise ArgumentError(f"frame {H}x{W} is smaller than 2^{cfg.n_levels} in one dimension")
+    dims = level_dims(H, W, cfg.n_levels)
+    n_lp = dims[-1][0] * dims[-1][1]
+    n_dir = 3 * sum(h * w for h, w in dims)
+
+    if cfg.mode == "tikhonov_only":
+        # linear end to end: transform -> unmix -> inverse == per-pixel unmix
+        op = TikhonovOperator.from_relative(sensitivity, cfg.tikhonov_gamma)
+        ops = make_operator_set(n_bands=L, xi=basis.xi, epsilon=eps)
+        spec = apply_matrix_device(upload(frame.data.reshape(-1, 3), torch.float64, dev), op.solve)
+        x = fit_device(spec, ops, cal)
+        cube = SpectralCube(grid=grid, data=download(spec).reshape(H, W, L))
+        if stats is not None:
+            stats.update(bayes_coefficients=0, tikhonov_coefficients=n_lp + n_dir)
+        return cube, _map_from_planes(download(x), H, W)
+
+    # hybrid
+    ops = _hybrid_operators(sensitivity, basis, cfg)
+    out = hybrid_device(upload(frame.data[None], torch.float64, dev), ops, cfg.n_levels, cal)
+    cube = SpectralCube(grid=grid, data=download(out["cube"][0]))
+    xs = download(out["x"][:, 0])
+    cmap = ConcentrationMap(hbo=xs[0], hb=xs[1], offset=xs[2])
+    if stats is not None:
+        stats.update(bayes_coefficients=n_lp, tikhonov_coefficients=n_dir)
+    return cube, cmap
+
+
+def estimate_sequence(
+    frames: Iterable[RgbImage],
+    sensitivity: CameraSensitivity,
+    basis: ChromophoreBasis,
+    cfg: PipelineConfig,
+    timings: list | None = None,
+) -> Iterator[ConcentrationMap]:
+    """Stream maps for a frame sequence (pipeline.py:220-245)."""
+    shape = None
+    for frame in frames:
+        dims = (frame.height, frame.width)
+        if shape is None:
+            shape = dims
+        elif dims != shape:
+            raise DataError(f"frame dimensions changed mid-stream: {shape} -> {dims}")
+        t0 = time.perf_counter()
+        _, cmap = estimate_frame(frame, sensitivity, basis, cfg)
+        if timings is not None:
+            timings.append(time.perf_counter() - t0)
+        yield cmap

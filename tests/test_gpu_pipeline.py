@@ -1,0 +1,208 @@
+"""GPU parity of the hot path: estimate_frame (fp64 drop-in, K6 fp64) and the
+batched fp32 map engine (K6 fp32) against the reference's golden outputs and
+the pinned CPU oracle, at the BASELINE.json configurations.
+
+Tolerances (north_star): THb |d| <= 1e-4 |THb_ref|, SO2 |d| <= 1e-5 absolute,
+identical SO2 NaN pattern, and the per-low-pass-coefficient fit count (the
+EM's discrete stopping decision, bayes.py:199-205) bit-exact."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1706_07263_b200 as ox
+from oracle import oximap_oracle as O
+from paper_1706_07263_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+THB_REL = 1e-4
+SO2_ABS = 1e-5
+
+
+def assert_maps_close(thb, so2, ref_thb, ref_so2, thb_rel=THB_REL, so2_abs=SO2_ABS):
+    assert np.array_equal(np.isnan(so2), np.isnan(ref_so2)), "SO2 NaN pattern differs"
+    err = np.abs(thb - ref_thb)
+    assert np.all(err <= thb_rel * np.abs(ref_thb) + 1e-12), f"THb max rel err {np.max(err / np.maximum(np.abs(ref_thb), 1e-12)):.3e}"
+    ok = ~np.isnan(ref_so2)
+    assert np.max(np.abs(so2[ok] - ref_so2[ok]), initial=0.0) <= so2_abs
+
+
+# ---------------------------------------------------------------- fp64 drop-in
+@pytest.mark.parametrize("i", range(8))
+def test_estimate_frame_matches_reference(cuda, golden, sensitivity, basis, i):
+    g = golden("frames")
+    H, W, n, nb, nt = (int(v) for v in g[f"meta{i}"])
+    mode = str(g[f"mode{i}"])
+    stats = {}
+    cube, cmap = ox.estimate_frame(ox.RgbImage(g[f"rgb{i}"]), sensitivity, basis,
+                                   ox.PipelineConfig(mode=mode, n_levels=n), stats=stats)
+    assert stats == {"bayes_coefficients": nb, "tikhonov_coefficients": nt}
+    if f"cube{i}" in g:
+        assert np.max(np.abs(cube.data - g[f"cube{i}"])) <= 1e-9
+    assert np.max(np.abs(cmap.stacked() - g[f"x{i}"])) <= 1e-7
+    assert_maps_close(cmap.thb, cmap.sat_o2, g[f"thb{i}"], g[f"so2{i}"], thb_rel=1e-9, so2_abs=1e-10)
+
+
+def test_hybrid_fit_counts_bitexact_fp64(cuda, golden, sensitivity, basis):
+    from paper_1706_07263_b200.pipeline import _hybrid_operators, hybrid_device
+
+    g, ops = golden("frames"), golden("operators")
+    for i in range(6):
+        H, W, n = (int(v) for v in g[f"meta{i}"][:3])
+        rgb = g[f"rgb{i}"]
+        out = hybrid_device(torch.from_numpy(rgb[None]).to(cuda), _hybrid_operators(sensitivity, basis, ox.PipelineConfig(n_levels=n)), n, 1.0, want_cube=False)
+        ref = O.estimate_frame(rgb, ops["c"], ops["xi"], n_levels=n, want_cube=False)
+        assert np.array_equal(out["fits"][0].cpu().numpy(), ref["fits"]), i
+
+
+def test_modes_and_identities(cuda, sensitivity, basis, rng):
+    # constant frame: hybrid == bayes_only (test_pipeline.py:24-35)
+    y = sensitivity.c @ np.exp(-(basis.xi @ [30.0, 25.0, 0.0]))
+    frame = ox.RgbImage(np.zeros((8, 8, 3)) + y)
+    hc, hm = ox.estimate_frame(frame, sensitivity, basis, ox.PipelineConfig(mode="hybrid", n_levels=2))
+    bc, bm = ox.estimate_frame(frame, sensitivity, basis, ox.PipelineConfig(mode="bayes_only"))
+    assert np.max(np.abs(hc.data - bc.data)) <= 1e-10
+    assert np.max(np.abs(hm.stacked() - bm.stacked())) <= 1e-8
+    # tikhonov_only == image-domain unmix (test_pipeline.py:47-56)
+    fd = rng.uniform(0.1, 1.5, size=(12, 16, 3))
+    cube, cmap = ox.estimate_frame(ox.RgbImage(fd), sensitivity, basis, ox.PipelineConfig(mode="tikhonov_only"))
+    op = ox.TikhonovOperator.from_relative(sensitivity, 1e-3)
+    direct = ox.tikhonov_unmix(fd, op)
+    assert np.max(np.abs(cube.data - direct)) <= 1e-8
+    # direct_msi is the plain fit (test_pipeline.py:58-66)
+    x = rng.uniform(5, 50, size=(6, 6, 3))
+    x[..., 2] = rng.uniform(-0.3, 0.3, size=(6, 6))
+    msi = ox.forward_msi(ox.ConcentrationMap.from_stacked(x), basis)
+    oc, om = ox.estimate_frame(msi, sensitivity, basis, ox.PipelineConfig(mode="direct_msi"))
+    assert oc is msi and np.max(np.abs(om.stacked() - x)) <= 1e-9
+    # zero frame defined output (test_pipeline.py:37-45)
+    for mode in ("hybrid", "tikhonov_only", "bayes_only"):
+        c0, m0 = ox.estimate_frame(ox.RgbImage(np.zeros((4, 4, 3))), sensitivity, basis,
+                                   ox.PipelineConfig(mode=mode, n_levels=1))
+        assert np.all(np.isfinite(c0.data)) and np.all(np.isfinite(m0.stacked()))
+        assert np.all(np.isnan(m0.sat_o2) | (m0.thb > 0))
+
+
+def test_pipeline_errors_and_calibration(cuda, sensitivity, basis):
+    with pytest.raises(ox.ArgumentError, match="smaller"):
+        ox.estimate_frame(ox.RgbImage(np.ones((4, 4, 3))), sensitivity, basis, ox.PipelineConfig(n_levels=3))
+    with pytest.raises(ox.ArgumentError):
+        ox.estimate_frame(ox.RgbImage(np.ones((4, 4, 3))), sensitivity, basis, ox.PipelineConfig(mode="direct_msi"))
+    neg = -np.ones((8, 8, 3))
+    with pytest.raises(ox.ArgumentError):
+        ox.estimate_frame(ox.RgbImage(neg), sensitivity, basis, ox.PipelineConfig(n_levels=1))
+    spec = synth.tissue_phantom_spec(8, 8, seed=2, noise_sigma=0.0, texture_density=0.0)
+    _, _, rgb = synth.generate_phantom(spec, sensitivity, basis)
+    _, base = ox.estimate_frame(rgb, sensitivity, basis, ox.PipelineConfig())
+    _, scaled = ox.estimate_frame(rgb, sensitivity, basis, ox.PipelineConfig(calibration_scale=2.0))
+    assert np.allclose(scaled.hbo, 2.0 * base.hbo, atol=1e-12)
+    assert np.allclose(scaled.offset, base.offset, atol=1e-12)
+    # sequence semantics (test_pipeline.py:146-171)
+    frames = [ox.RgbImage(np.full((8, 8, 3), 0.7))] * 3
+    timings = []
+    maps = list(ox.estimate_sequence(frames, sensitivity, basis, ox.PipelineConfig(), timings=timings))
+    assert len(maps) == 3 and len(timings) == 3
+    assert all(np.array_equal(m.stacked(), maps[0].stacked()) for m in maps)
+    with pytest.raises(ox.DataError, match="mid-stream"):
+        list(ox.estimate_sequence([ox.RgbImage(np.ones((8, 8, 3))), ox.RgbImage(np.ones((8, 10, 3)))],
+                                  sensitivity, basis, ox.PipelineConfig()))
+
+
+# ---------------------------------------------------------------- fp32 engine
+def _engine_vs_oracle(cuda, sensitivity, basis, frames64, n, *, fits=True):
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=n))
+    x = torch.from_numpy(frames64.astype(np.float32)).to(cuda)
+    out = eng.run(x, fits=True)
+    torch.cuda.synchronize()
+    thb, so2 = out.thb.cpu().numpy(), out.so2.cpu().numpy()
+    gfits = out.fits.cpu().numpy()
+    c, xi = sensitivity.c, basis.xi
+    for b in range(frames64.shape[0]):
+        ref = O.estimate_frame(frames64[b], c, xi, n_levels=n, want_cube=False, threads=O.default_threads())
+        assert_maps_close(thb[b], so2[b], ref["thb"], ref["so2"])
+        if fits:
+            assert np.array_equal(gfits[b], ref["fits"]), f"fit-count flips: {np.sum(gfits[b] != ref['fits'])}"
+    return out
+
+
+def test_engine_cfg1_256(cuda, golden, sensitivity, basis):
+    g = golden("frames")
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=1))
+    out = eng.run(torch.from_numpy(g["rgb5"][None].astype(np.float32)).to(cuda))
+    assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), g["thb5"], g["so2"+"5"])
+
+
+@pytest.mark.parametrize("H,W,n,td", [(37, 23, 2, 0.3), (45, 70, 3, 0.3), (64, 64, 2, 0.0), (9, 15, 1, 0.0)])
+def test_engine_small_and_odd(cuda, sensitivity, basis, H, W, n, td):
+    frames = np.stack([synth.phantom_rgb_f32(H, W, s, sensitivity, basis, texture_density=td) for s in (1, 2)])
+    _engine_vs_oracle(cuda, sensitivity, basis, frames, n)
+
+
+def test_engine_cfg2_stereo_pair(cuda, sensitivity, basis):
+    # da Vinci SD: 720x576 per eye, two independent frames, n=1
+    frames = np.stack([synth.phantom_rgb_f32(576, 720, s, sensitivity, basis) for s in (0, 1)])
+    _engine_vs_oracle(cuda, sensitivity, basis, frames, 1)
+
+
+def test_engine_cfg3_1080p(cuda, sensitivity, basis):
+    frames = synth.phantom_rgb_f32(1080, 1920, 3, sensitivity, basis)[None]
+    _engine_vs_oracle(cuda, sensitivity, basis, frames, 2)
+
+
+def test_engine_cfg3_1080p_smooth(cuda, sensitivity, basis):
+    frames = synth.phantom_rgb_f32(1080, 1920, 4, sensitivity, basis, texture_density=0.0)[None]
+    _engine_vs_oracle(cuda, sensitivity, basis, frames, 2)
+
+
+def test_engine_cfg5_4k(cuda, sensitivity, basis):
+    frames = synth.phantom_rgb_f32(2160, 3840, 5, sensitivity, basis)[None]
+    _engine_vs_oracle(cuda, sensitivity, basis, frames, 3)
+
+
+def test_engine_batch_properties(cuda, sensitivity, basis):
+    """Config 4 properties at batch scale: frames are independent, so a
+    cycled batch must give identical maps per repeated frame, equal to the
+    single-frame result, and the host pipelined path equals the device path."""
+    distinct = np.stack([synth.phantom_rgb_f32(270, 480, s, sensitivity, basis) for s in range(4)]).astype(np.float32)
+    batch = np.concatenate([distinct] * 5)  # 20 frames
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2))
+    dev = eng.run(torch.from_numpy(batch).to(cuda))
+    thb = dev.thb.cpu().numpy()
+    for k in range(4, 20):
+        assert np.array_equal(thb[k], thb[k % 4])
+    single = eng.run(torch.from_numpy(distinct[1:2]).to(cuda))
+    assert np.array_equal(single.thb.cpu().numpy()[0], thb[1])
+    src = torch.from_numpy(batch).pin_memory()
+    hthb = torch.empty(batch.shape[:3], dtype=torch.float32).pin_memory()
+    hso2 = torch.empty(batch.shape[:3], dtype=torch.float32).pin_memory()
+    eng.maps_from_host(src, hthb, hso2, chunk=6)
+    assert np.array_equal(hthb.numpy(), thb)
+    assert np.array_equal(hso2.numpy(), dev.so2.cpu().numpy(), equal_nan=True)
+
+
+def test_engine_flags(cuda, sensitivity, basis):
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=1))
+    bad = torch.ones((1, 8, 8, 3), device=cuda)
+    bad[0, 3, 3, 1] = float("nan")
+    with pytest.raises(ox.ArgumentError):
+        eng.run(bad)
+    with pytest.raises(ox.ArgumentError):
+        eng.run(-torch.ones((1, 8, 8, 3), device=cuda))
+    with pytest.raises(ox.ArgumentError):
+        eng.run(torch.ones((1, 1, 8, 3), device=cuda))
+    z = eng.run(torch.zeros((1, 4, 4, 3), device=cuda))
+    assert torch.isfinite(z.thb).all()
+
+
+def test_engine_planes_match_fp64(cuda, golden, sensitivity, basis):
+    g = golden("frames")
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2))
+    out = eng.run(torch.from_numpy(g["rgb3"][None].astype(np.float32)).to(cuda), planes=True)
+    x = g["x3"]
+    hbo = out.hbo[0].double().cpu().numpy()
+    assert np.max(np.abs(hbo - x[..., 0])) <= 1e-4 * np.max(np.abs(x[..., 0]))
+    off = out.offset[0].double().cpu().numpy()
+    assert np.max(np.abs(off - x[..., 2])) <= 1e-4
