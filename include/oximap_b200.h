@@ -61,7 +61,7 @@ enum {
  * exactly as the reference builds them:
  *   solve     L x 3  Tikhonov ridge inverse (C^T C + g I)^-1 C^T   unmix.py:53-74
  *   fit_mat   3 x L  (xi^T xi)^-1 xi^T                             bayes.py:99-104
- *   xi        L x 3  chromophore basis (hbo, hb, 1)                core.py:134-158
+ *   xi        L x 3  chromophore basis (hbo, hb, 1); xi[:, 2] must be 1  core.py:134-158
  *   sens      3 x L  camera sensitivity C                          core.py:112-131
  *   gain      L x 3  N^-1 C^T, N = C^T C + beta D2^T D2            bayes.py:117-129
  * The shape-prior update N^-1 (C^T y + P e) of bayes.py:131-135 is evaluated

@@ -77,6 +77,12 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
       d.fitl2_f[k][l] = static_cast<float>(-ln2 * d.fitm[k][l]);
     }
   }
+  // the EM kernels use xi[:, 2] == 1 (ChromophoreBasis contract, core.py:152-153)
+  for (int l = 0; l < L; ++l)
+    if (d.xi[l][2] != 1.0) {
+      delete c;
+      return OXM_ERR_ARGUMENT;
+    }
   for (int l = 0; l < L; ++l)
     for (int k = 0; k < 3; ++k)
       if (!std::isfinite(d.solve[l][k]) || !std::isfinite(d.xi[l][k]) || !std::isfinite(d.gain[l][k]) ||

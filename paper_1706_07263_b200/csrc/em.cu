@@ -1,9 +1,10 @@
 // K4: standalone low-pass estimator (estimate_lowpass, bayes.py:210-272) and
 // the shape-prior update for arbitrary (y, e) (expectation_step, bayes.py:162-182).
 //
-// One thread per coefficient; operators in constant bank 0.  Spectra are
-// written row-major (n, L) like the reference's return value; each thread's
-// row is staged through shared memory so the global stores are coalesced.
+// One thread per coefficient; operators in constant bank 0, exp/log tables
+// and the per-thread expected spectrum in shared memory.  Spectra are
+// written row-major (n, L) like the reference's return value (this is the
+// drop-in API path; the video path is hybrid.cu's SoA em_soa_kernel).
 #include "oxm_em.cuh"
 
 namespace oxm {
@@ -18,34 +19,28 @@ __global__ void __launch_bounds__(kEmThreads) em_lowpass_kernel(const __grid_con
                                                                 double* __restrict__ spectra,
                                                                 double* __restrict__ xout,
                                                                 int32_t* __restrict__ fits) {
-  constexpr int LM = BandCount<KL>::kMax;
   const int L = BandCount<KL>::get(ops);
-  extern __shared__ double stage[];  // [kEmThreads][L]
-  const int64_t base = (int64_t)blockIdx.x * kEmThreads;
-  const int64_t i = base + threadIdx.x;
-  const bool live = i < n;
-  double* row = stage + (int64_t)threadIdx.x * L;
-  if (live) {
-    const double y0 = y[3 * i + 0], y1 = y[3 * i + 1], y2 = y[3 * i + 2];
-    double x0, x1, x2;
-    int nf;
-    em_coefficient<KL>(ops, y0, y1, y2, init ? init + i * L : nullptr, x0, x1, x2, nf,
-                       [&](int l, double v) { row[l] = v; });
-    if (xout) {
-      xout[3 * i + 0] = x0;
-      xout[3 * i + 1] = x1;
-      xout[3 * i + 2] = x2;
-    }
-    if (fits) fits[i] = nf;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
+  double* ecol = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
+  load_math_tables(mt);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
+  if (i >= n) return;
+  const double y0 = y[3 * i + 0], y1 = y[3 * i + 1], y2 = y[3 * i + 2];
+  double x0, x1, x2;
+  int nf;
+  double* row = spectra ? spectra + i * L : nullptr;
+  em_coefficient<KL>(ops, mt, ecol, kEmThreads, y0, y1, y2, init ? init + i * L : nullptr, x0, x1, x2, nf,
+                     [&](int l, double v) {
+                       if (row) row[l] = v;
+                     });
+  if (xout) {
+    xout[3 * i + 0] = x0;
+    xout[3 * i + 1] = x1;
+    xout[3 * i + 2] = x2;
   }
-  (void)LM;
-  if (spectra) {
-    __syncthreads();
-    const int64_t cnt = min64(kEmThreads, n - base);
-    const int64_t tot = cnt * L;
-    double* dst = spectra + base * L;
-    for (int64_t k = threadIdx.x; k < tot; k += kEmThreads) dst[k] = stage[k];
-  }
+  if (fits) fits[i] = nf;
 }
 
 template <int KL>
@@ -86,7 +81,7 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   if (n == 0) return OXM_OK;
   DeviceGuard dg(ctx->device);
   const int L = ctx->ops.L;
-  const size_t smem = sizeof(double) * kEmThreads * L;
+  const size_t smem = em_smem_bytes(L, kEmThreads);
   const unsigned grid = grid_1d(n, kEmThreads);
   cudaStream_t s = as_stream(stream);
   if (L == 26) {

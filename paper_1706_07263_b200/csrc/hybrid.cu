@@ -13,14 +13,20 @@
 //                     fp64 with the reference's add order (bit-exact LL),
 //                     non-finite / negative checks -> flags
 //   2. em_soa_kernel  one thread per coefficient: K4 in fp64 -> S (SoA)
-//   3. px kernel      one thread per pixel column segment: reconstruct the
-//                     26-band spectrum in registers, log, 3x26 fit, THb/SO2.
-//                     fp32 variant: MUFU lg2 with S split hi/lo in shared
-//                     memory; pixels whose smallest band < fallback_below
-//                     are recomputed in fp64 (cancellation guard).
-//                     fp64 variant: everything fp64, optional (H,W,L) cube.
+//   3. px kernel      one thread per (column, 2^n-row block segment): rebuild
+//                     the 26-band spectrum in registers, log, 3x26 fit,
+//                     THb/SO2.  fp32 variant: S as an fp32 (hi, lo) pair per
+//                     band, MUFU lg2, R rows per thread interleaved for ILP;
+//                     pixels whose smallest band < fallback_below are
+//                     appended (warp-aggregated) to a list and
+//   4. fallback       recomputed in fp64 by a small grid-stride kernel
+//                     (cancellation guard; ~0.6 % of textured pixels), so
+//                     the hot kernel has no divergent fp64 code at all.
+//                     fp64 variant (drop-in API): everything fp64, optional
+//                     (H, W, L) cube, no fallback needed.
 // Neither the directional planes nor the 26-channel cube touch HBM on the
-// fp32 path: HBM traffic is the frame read twice + the maps written once.
+// fp32 path: HBM traffic is the frame read twice, the per-block spectra
+// (8 B/band/coefficient) once, and the maps written once.
 #include <algorithm>
 
 #include "oxm_em.cuh"
@@ -31,7 +37,8 @@ namespace {
 constexpr int kMaxLevels = 24;
 constexpr int kLlThreads = 128;
 constexpr int kEmThreads = 128;
-constexpr int kPxCols = 256;  // pixel columns per CTA in the map kernels
+constexpr int kPxCols = 128;  // pixel columns per CTA in the fp32 map kernel
+constexpr int kFbThreads = 128;
 
 struct LevelDims {
   int n;
@@ -113,34 +120,48 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const TIn* __restrict__ 
   if (flags && (bad || neg)) atomicOr(flags, (bad ? OXM_FLAG_NONFINITE : 0u) | (neg ? OXM_FLAG_NEGATIVE_LL : 0u));
 }
 
-// S[l][idx] = EM spectra of ybar[:, idx]  (SoA, coalesced per band).
-template <int KL>
+// EM spectra of ybar[:, idx], SoA per band (coalesced): fp64 S[l][idx] for
+// the fp64 path, or an fp32 (hi, lo) pair Shi/Slo[l][idx] for the fp32 path
+// (hi + lo carries 48 significant bits: plenty for the fp64 fallback).
+template <int KL, bool F32OUT>
 __global__ void __launch_bounds__(kEmThreads) em_soa_kernel(const __grid_constant__ DevOps ops,
                                                             const double* __restrict__ ybar, int64_t nll,
-                                                            double* __restrict__ S, int32_t* __restrict__ fits) {
+                                                            double* __restrict__ S, float* __restrict__ Shi,
+                                                            float* __restrict__ Slo, int32_t* __restrict__ fits) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
+  double* ecol = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
+  load_math_tables(mt);
+  __syncthreads();
   const int64_t idx = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
   if (idx >= nll) return;
   const double y0 = ybar[idx], y1 = ybar[nll + idx], y2 = ybar[2 * nll + idx];
   double x0, x1, x2;
   int nf;
-  em_coefficient<KL>(ops, y0, y1, y2, nullptr, x0, x1, x2, nf,
-                     [&](int l, double v) { S[(int64_t)l * nll + idx] = v; });
+  em_coefficient<KL>(ops, mt, ecol, kEmThreads, y0, y1, y2, nullptr, x0, x1, x2, nf, [&](int l, double v) {
+    if constexpr (F32OUT) {
+      const float h = __double2float_rn(v);
+      Shi[(int64_t)l * nll + idx] = h;
+      Slo[(int64_t)l * nll + idx] = __double2float_rn(v - (double)h);
+    } else {
+      S[(int64_t)l * nll + idx] = v;
+    }
+  });
   if (fits) fits[idx] = nf;
 }
 
 // Per-pixel fp64 spectrum + fit (used by the fp64 kernel and as the fp32
 // kernel's cancellation fallback).  Returns x = (hbo, hb, offset) unscaled.
-template <int KL, typename CubeStore>
-__device__ __forceinline__ void pixel_fit_f64(const DevOps& ops, const double* __restrict__ S, int64_t nll,
-                                              int64_t bidx, double d0, double d1, double d2, double& x0,
-                                              double& x1, double& x2, CubeStore cube_store) {
+template <int KL, typename SpecLoad, typename CubeStore>
+__device__ __forceinline__ void pixel_fit_f64(const DevOps& ops, SpecLoad spec, double d0, double d1, double d2,
+                                              double& x0, double& x1, double& x2, CubeStore cube_store) {
   constexpr int LM = BandCount<KL>::kMax;
   const int L = BandCount<KL>::get(ops);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll(KL > 0 ? LM : 1)
   for (int l = 0; l < LM; ++l) {
     if (KL == 0 && l >= L) break;
-    const double s = fma(ops.solve[l][2], d2, fma(ops.solve[l][1], d1, fma(ops.solve[l][0], d0, S[(int64_t)l * nll + bidx])));
+    const double s = fma(ops.solve[l][2], d2, fma(ops.solve[l][1], d1, fma(ops.solve[l][0], d0, spec(l))));
     cube_store(l, s);
     const double lg = log(fmax(s, ops.eps));
     a0 = fma(ops.fitm[0][l], lg, a0);
@@ -158,94 +179,141 @@ struct PxGeom {
   double cal;
 };
 
-// fp32 map kernel.  CTA = kPxCols columns x one low-pass block row (2^n pixel
-// rows) of one frame; each thread walks the 2^n rows of its column.
-template <int KL>
+__device__ __forceinline__ float lg2_approx(float v) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
+// fp32 map kernel.  CTA = kPxCols columns x R rows of one low-pass block row
+// of one frame; each thread owns one column and R rows and walks the bands
+// once, updating its R pixels per band (R independent MUFU/FMA chains).
+// The block spectrum (hi, lo) is read straight from L1/L2: the 2^n threads of
+// a block column share each line.
+template <int KL, int R>
 __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__ DevOps ops,
                                                          const float* __restrict__ frames, PxGeom g,
-                                                         const double* __restrict__ S,
+                                                         const float* __restrict__ Shi,
+                                                         const float* __restrict__ Slo,
                                                          const double* __restrict__ ybar, float* __restrict__ thb,
                                                          float* __restrict__ so2, float* __restrict__ hbo,
-                                                         float* __restrict__ hb, float* __restrict__ off) {
+                                                         float* __restrict__ hb, float* __restrict__ off,
+                                                         uint32_t* __restrict__ fb_count, uint32_t* __restrict__ fb_list) {
   constexpr int LM = BandCount<KL>::kMax;
   const int L = BandCount<KL>::get(ops);
-  const int LS = L | 1;
-  extern __shared__ float sm[];
-  const int nbmax = (kPxCols >> g.n) + 1;
-  float* shi = sm;                  // [nbmax][LS]
-  float* slo = shi + nbmax * LS;    // [nbmax][LS]
-  float* yhi = slo + nbmax * LS;    // [nbmax][3]
-  float* ylo = yhi + nbmax * 3;     // [nbmax][3]
-
-  const int64_t f = blockIdx.z, by = blockIdx.y;
-  const int64_t c0 = (int64_t)blockIdx.x * kPxCols;
-  const int64_t clast = min(c0 + kPxCols, g.W) - 1;
-  const int64_t bx0 = c0 >> g.n;
-  const int nb = (int)((clast >> g.n) - bx0 + 1);
-  const int64_t brow = (f * g.hL + by) * g.wL;  // coefficient index of (f, by, 0)
-
-  // stage this tile's block spectra as (hi, lo) fp32 pairs
-  for (int q = threadIdx.x; q < nb * L; q += kPxCols) {
-    const int l = q / nb, j = q - l * nb;
-    const double v = S[(int64_t)l * g.nll + brow + bx0 + j];
-    const float h = __double2float_rn(v);
-    shi[j * LS + l] = h;
-    slo[j * LS + l] = __double2float_rn(v - (double)h);
-  }
-  for (int q = threadIdx.x; q < nb * 3; q += kPxCols) {
-    const int k = q / nb, j = q - k * nb;
-    const double v = ybar[(int64_t)k * g.nll + brow + bx0 + j];
-    const float h = __double2float_rn(v);
-    yhi[j * 3 + k] = h;
-    ylo[j * 3 + k] = __double2float_rn(v - (double)h);
-  }
-  __syncthreads();
-
-  const int64_t col = c0 + threadIdx.x;
+  const int64_t f = blockIdx.z;
+  const int64_t col = (int64_t)blockIdx.x * kPxCols + threadIdx.x;
+  const int bs = 1 << g.n;                    // rows per low-pass block
+  const int cpb = bs > R ? bs / R : 1;        // row chunks per block row
+  const int64_t by = blockIdx.y / cpb;
+  const int64_t row0 = by * bs + (int64_t)(blockIdx.y - by * cpb) * R;
   if (col >= g.W) return;
-  const int j = (int)((col >> g.n) - bx0);
-  const float* sh = shi + j * LS;
-  const float* sl = slo + j * LS;
-  const float yh0 = yhi[3 * j], yh1 = yhi[3 * j + 1], yh2 = yhi[3 * j + 2];
-  const float yl0 = ylo[3 * j], yl1 = ylo[3 * j + 1], yl2 = ylo[3 * j + 2];
-  const int64_t bidx = brow + bx0 + j;
-  const float cal = (float)g.cal;
-  const int64_t r0 = by << g.n;
-  const int64_t r1 = min(r0 + ((int64_t)1 << g.n), g.H);
-  for (int64_t row = r0; row < r1; ++row) {
-    const int64_t p = (f * g.H + row) * g.W + col;
-    const float v0 = ldg(frames + 3 * p), v1 = ldg(frames + 3 * p + 1), v2 = ldg(frames + 3 * p + 2);
-    const float d0 = (v0 - yh0) - yl0, d1 = (v1 - yh1) - yl1, d2 = (v2 - yh2) - yl2;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, vmin = 3.0e38f;
+  const int nrow = (int)min64(min64(R, g.H - row0), (int64_t)bs);
+  const int64_t bidx = (f * g.hL + by) * g.wL + (col >> g.n);
+
+  float yh[3], yl[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double v = ybar[(int64_t)k * g.nll + bidx];
+    yh[k] = __double2float_rn(v);
+    yl[k] = __double2float_rn(v - (double)yh[k]);
+  }
+  float d[R][3], acc[R][3], vmin[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = (f * g.H + row0 + min(r, nrow - 1)) * g.W + col;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      d[r][k] = (ldg(frames + 3 * p + k) - yh[k]) - yl[k];
+      acc[r][k] = 0.f;
+    }
+    vmin[r] = 3.0e38f;
+  }
 #pragma unroll(KL > 0 ? LM : 1)
-    for (int l = 0; l < LM; ++l) {
-      if (KL == 0 && l >= L) break;
-      const float s = fmaf(ops.solve_f[l][2], d2, fmaf(ops.solve_f[l][1], d1, fmaf(ops.solve_f[l][0], d0, sl[l]))) + sh[l];
-      vmin = fminf(vmin, s);
-      const float lg = __log2f(fmaxf(s, ops.eps_f));
-      a0 = fmaf(ops.fitl2_f[0][l], lg, a0);
-      a1 = fmaf(ops.fitl2_f[1][l], lg, a1);
-      a2 = fmaf(ops.fitl2_f[2][l], lg, a2);
+  for (int l = 0; l < LM; ++l) {
+    if (KL == 0 && l >= L) break;
+    const float sh = ldg(Shi + (int64_t)l * g.nll + bidx);
+    const float sl = ldg(Slo + (int64_t)l * g.nll + bidx);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const float s = fmaf(ops.solve_f[l][2], d[r][2], fmaf(ops.solve_f[l][1], d[r][1], fmaf(ops.solve_f[l][0], d[r][0], sl))) + sh;
+      vmin[r] = fminf(vmin[r], s);
+      const float lg = lg2_approx(fmaxf(s, ops.eps_f));
+      acc[r][0] = fmaf(ops.fitl2_f[0][l], lg, acc[r][0]);
+      acc[r][1] = fmaf(ops.fitl2_f[1][l], lg, acc[r][1]);
+      acc[r][2] = fmaf(ops.fitl2_f[2][l], lg, acc[r][2]);
     }
-    if (vmin < (float)ops.fallback_below) {
-      // cancellation guard: redo this pixel in fp64 from the fp64 spectra
-      double x0, x1, x2;
-      const double D0 = (double)v0 - ybar[bidx];
-      const double D1 = (double)v1 - ybar[g.nll + bidx];
-      const double D2 = (double)v2 - ybar[2 * g.nll + bidx];
-      pixel_fit_f64<KL>(ops, S, g.nll, bidx, D0, D1, D2, x0, x1, x2, [](int, double) {});
-      a0 = (float)(x0);
-      a1 = (float)(x1);
-      a2 = (float)(x2);
+  }
+  const float cal = (float)g.cal;
+  const float thr = (float)ops.fallback_below;
+  const unsigned active = __activemask();
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const bool ok = r < nrow;
+    const int64_t p = (f * g.H + row0 + r) * g.W + col;
+    if (ok) {
+      const float xo = acc[r][0] * cal, xd = acc[r][1] * cal;
+      const float co = fmaxf(xo, 0.f);
+      const float t = co + fmaxf(xd, 0.f);
+      if (thb) thb[p] = t;
+      if (so2) so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
+      if (hbo) hbo[p] = xo;
+      if (hb) hb[p] = xd;
+      if (off) off[p] = acc[r][2];
     }
-    const float xo = a0 * cal, xd = a1 * cal;
+    // cancellation guard: queue the pixel for the fp64 fixup kernel
+    const bool need = ok && vmin[r] < thr;
+    const unsigned m = __ballot_sync(active, need);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
+      base = __shfl_sync(active, base, leader);
+      if (need) fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)p;
+    }
+  }
+}
+
+// fp64 recompute of the queued pixels (grid-stride over the list).
+template <int KL>
+__global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
+                                                                 const float* __restrict__ frames, PxGeom g,
+                                                                 const float* __restrict__ Shi,
+                                                                 const float* __restrict__ Slo,
+                                                                 const double* __restrict__ ybar,
+                                                                 const uint32_t* __restrict__ fb_count,
+                                                                 const uint32_t* __restrict__ fb_list,
+                                                                 float* __restrict__ thb, float* __restrict__ so2,
+                                                                 float* __restrict__ hbo, float* __restrict__ hb,
+                                                                 float* __restrict__ off) {
+  const uint32_t cnt = *fb_count;
+  const int64_t plane = g.H * g.W;
+  for (uint32_t i = blockIdx.x * kFbThreads + threadIdx.x; i < cnt; i += gridDim.x * kFbThreads) {
+    const int64_t p = fb_list[i];
+    const int64_t f = p / plane;
+    const int64_t rem = p - f * plane;
+    const int64_t row = rem / g.W, col = rem - row * g.W;
+    const int64_t bidx = (f * g.hL + (row >> g.n)) * g.wL + (col >> g.n);
+    const double D0 = (double)frames[3 * p] - ybar[bidx];
+    const double D1 = (double)frames[3 * p + 1] - ybar[g.nll + bidx];
+    const double D2 = (double)frames[3 * p + 2] - ybar[2 * g.nll + bidx];
+    double x0, x1, x2;
+    pixel_fit_f64<KL>(
+        ops,
+        [&](int l) {
+          const int64_t q = (int64_t)l * g.nll + bidx;
+          return (double)Shi[q] + (double)Slo[q];
+        },
+        D0, D1, D2, x0, x1, x2, [](int, double) {});
+    const float xo = (float)(x0 * g.cal), xd = (float)(x1 * g.cal);
     const float co = fmaxf(xo, 0.f);
     const float t = co + fmaxf(xd, 0.f);
     if (thb) thb[p] = t;
-    if (so2) so2[p] = t > 0.f ? __fdiv_rn(co, t) : qnan_f();
+    if (so2) so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
     if (hbo) hbo[p] = xo;
     if (hb) hb[p] = xd;
-    if (off) off[p] = a2;
+    if (off) off[p] = (float)x2;
   }
 }
 
@@ -270,9 +338,11 @@ __global__ void __launch_bounds__(128) px_f64_kernel(const __grid_constant__ Dev
   const double D2 = ldg(frames + 3 * p + 2) - ybar[2 * g.nll + bidx];
   double x0, x1, x2;
   double* crow = cube ? cube + p * L : nullptr;
-  pixel_fit_f64<KL>(ops, S, g.nll, bidx, D0, D1, D2, x0, x1, x2, [&](int l, double s) {
-    if (crow) crow[l] = s;
-  });
+  pixel_fit_f64<KL>(
+      ops, [&](int l) { return S[(int64_t)l * g.nll + bidx]; }, D0, D1, D2, x0, x1, x2,
+      [&](int l, double s) {
+        if (crow) crow[l] = s;
+      });
   if (hbo) hbo[p] = x0 * g.cal;
   if (hb) hb[p] = x1 * g.cal;
   if (off) off[p] = x2;
@@ -290,12 +360,41 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
   return OXM_OK;
 }
 
-inline void mark(void* const* ev, int i, cudaStream_t s) {
-  if (ev && ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
+// Workspace (256-B aligned sections):
+//   ybar  3 x nll  double
+//   spectra  L x nll x 8 B   (fp64 S, or fp32 Shi followed by fp32 Slo)
+//   fallback counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
+struct Workspace {
+  double* ybar;
+  double* S;
+  float* Shi;
+  float* Slo;
+  uint32_t* fb_count;
+  uint32_t* fb_list;
+};
+
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+size_t workspace_bytes(int L, int64_t nll, int64_t npx) {
+  return 256 + align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(double) * (size_t)L * (size_t)nll) +
+         256 + align256(sizeof(uint32_t) * (size_t)npx);
 }
 
-size_t workspace_bytes(int L, int64_t nll) { return sizeof(double) * (size_t)nll * (size_t)(L + 3) + 256; }
+Workspace carve(void* ws, int L, int64_t nll) {
+  uintptr_t p = (reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255);
+  Workspace w;
+  w.ybar = reinterpret_cast<double*>(p);
+  p += align256(sizeof(double) * 3 * (size_t)nll);
+  w.S = reinterpret_cast<double*>(p);
+  w.Shi = reinterpret_cast<float*>(p);
+  w.Slo = w.Shi + (size_t)L * (size_t)nll;
+  p += align256(sizeof(double) * (size_t)L * (size_t)nll);
+  w.fb_count = reinterpret_cast<uint32_t*>(p);
+  w.fb_list = reinterpret_cast<uint32_t*>(p + 256);
+  return w;
+}
 
+// zeroes the fallback counter as part of the low-pass launch (no memset node)
 template <typename TIn>
 int launch_ll(const TIn* frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll, uint32_t* flags,
               cudaStream_t s) {
@@ -309,18 +408,48 @@ int launch_ll(const TIn* frames, int64_t batch, const LevelDims& d, double* ybar
   return check_launch("hybrid_ll");
 }
 
-int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, double* S, int32_t* fits, cudaStream_t s) {
+template <bool F32OUT>
+int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Workspace& w, int32_t* fits,
+                  cudaStream_t s) {
   const unsigned grid = grid_1d(nll, kEmThreads);
-  if (ops.L == 26)
-    em_soa_kernel<26><<<grid, kEmThreads, 0, s>>>(ops, ybar, nll, S, fits);
-  else
-    em_soa_kernel<0><<<grid, kEmThreads, 0, s>>>(ops, ybar, nll, S, fits);
+  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
+  if (ops.L == 26) {
+    em_soa_kernel<26, F32OUT><<<grid, kEmThreads, smem, s>>>(ops, ybar, nll, w.S, w.Shi, w.Slo, fits);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(em_soa_kernel<0, F32OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    em_soa_kernel<0, F32OUT><<<grid, kEmThreads, smem, s>>>(ops, ybar, nll, w.S, w.Shi, w.Slo, fits);
+  }
   return check_launch("hybrid_em");
+}
+
+template <int KL>
+int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64_t batch, const Workspace& w,
+                  float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
+  const int bs = 1 << g.n;
+  const int R = bs >= 8 ? 8 : bs;
+  const int64_t cpb = bs > R ? bs / R : 1;
+  dim3 grid((unsigned)ceil_div(g.W, kPxCols), (unsigned)(g.hL * cpb), (unsigned)batch);
+  if (g.hL * cpb > 65535 || batch > 65535) return OXM_ERR_ARGUMENT;
+  switch (R) {
+    case 2: px_f32_kernel<KL, 2><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    case 4: px_f32_kernel<KL, 4><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    default: px_f32_kernel<KL, 8><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+  }
+  int st = check_launch("hybrid_px_f32");
+  if (st) return st;
+  px_fallback_kernel<KL><<<148 * 2, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, w.fb_count, w.fb_list,
+                                                         thb, so2, hbo, hb, off);
+  return check_launch("hybrid_fallback");
+}
+
+inline void mark(void* const* ev, int i, cudaStream_t s) {
+  if (ev && ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
 }
 
 template <typename TIn>
 int hybrid_prologue(const oxm_ctx* ctx, const TIn* frames, int64_t batch, int64_t H, int64_t W, int n,
-                    void* ws, size_t ws_bytes, LevelDims& d, int64_t& nll, double*& S, double*& ybar) {
+                    void* ws, size_t ws_bytes, LevelDims& d, int64_t& nll, Workspace& w) {
   if (!ctx || batch < 0 || !frames) return OXM_ERR_ARGUMENT;
   if (n < 1 || n > kMaxLevels) return OXM_ERR_ARGUMENT;
   // pipeline.py:177-181: frame must be at least 2^n in both dimensions
@@ -329,12 +458,13 @@ int hybrid_prologue(const oxm_ctx* ctx, const TIn* frames, int64_t batch, int64_
   if (st) return st;
   nll = batch * d.h[n] * d.w[n];
   const int L = ctx->ops.L;
-  if (!ws || ws_bytes < workspace_bytes(L, nll)) return OXM_ERR_WORKSPACE;
-  uintptr_t p = (reinterpret_cast<uintptr_t>(ws) + 255) & ~uintptr_t(255);
-  ybar = reinterpret_cast<double*>(p);
-  S = ybar + 3 * nll;
+  if (!ws || ws_bytes < workspace_bytes(L, nll, batch * H * W)) return OXM_ERR_WORKSPACE;
+  w = carve(ws, L, nll);
   return OXM_OK;
 }
+
+// fallback counter reset, ordered before the per-pixel kernel
+__global__ void zero_u32(uint32_t* p) { *p = 0u; }
 
 }  // namespace
 }  // namespace oxm
@@ -345,7 +475,7 @@ extern "C" size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, 
                                              int n_levels) {
   LevelDims d;
   if (!ctx || level_dims(height, width, n_levels, d) != OXM_OK || batch < 0) return 0;
-  return workspace_bytes(ctx->ops.L, batch * d.h[n_levels] * d.w[n_levels]);
+  return workspace_bytes(ctx->ops.L, batch * d.h[n_levels] * d.w[n_levels], batch * height * width);
 }
 
 extern "C" int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,
@@ -355,32 +485,25 @@ extern "C" int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int6
                                    void* const* ev) {
   LevelDims d;
   int64_t nll;
-  double *S, *ybar;
-  int st = hybrid_prologue<float>(ctx, frames, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll,
-                                  S, ybar);
+  Workspace w;
+  int st = hybrid_prologue<float>(ctx, frames, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
   if (st) return st;
   if (batch == 0) return OXM_OK;
+  // the fallback list stores 32-bit pixel indices
+  if (batch * height * width >= (int64_t)1 << 32) return OXM_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  if ((st = launch_ll<float>(frames, batch, d, ybar, nll, flags, s))) return st;
+  zero_u32<<<1, 1, 0, s>>>(w.fb_count);
+  if ((st = launch_ll<float>(frames, batch, d, w.ybar, nll, flags, s))) return st;
   mark(ev, 1, s);
-  if ((st = launch_em_soa(ctx->ops, ybar, nll, S, fits, s))) return st;
+  if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
   mark(ev, 2, s);
   PxGeom g{height, width, d.h[n_levels], d.w[n_levels], nll, n_levels, calibration};
-  const int L = ctx->ops.L;
-  const int nbmax = (kPxCols >> n_levels) + 1;
-  const size_t smem = sizeof(float) * (size_t)nbmax * (2 * (L | 1) + 6);
-  dim3 grid((unsigned)ceil_div(width, kPxCols), (unsigned)d.h[n_levels], (unsigned)batch);
-  if (grid.y > 65535 || grid.z > 65535) return OXM_ERR_ARGUMENT;
-  if (L == 26)
-    px_f32_kernel<26><<<grid, kPxCols, smem, s>>>(ctx->ops, frames, g, S, ybar, thb, so2, hbo, hb, offset);
-  else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(px_f32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    px_f32_kernel<0><<<grid, kPxCols, smem, s>>>(ctx->ops, frames, g, S, ybar, thb, so2, hbo, hb, offset);
-  }
-  st = check_launch("hybrid_px_f32");
+  if (ctx->ops.L == 26)
+    st = launch_px_f32<26>(ctx->ops, frames, g, batch, w, thb, so2, hbo, hb, offset, s);
+  else
+    st = launch_px_f32<0>(ctx->ops, frames, g, batch, w, thb, so2, hbo, hb, offset, s);
   mark(ev, 3, s);
   return st;
 }
@@ -391,24 +514,24 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
                                     int32_t* fits, uint32_t* flags, void* stream, void* const* ev) {
   LevelDims d;
   int64_t nll;
-  double *S, *ybar;
-  int st = hybrid_prologue<double>(ctx, frames, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll,
-                                   S, ybar);
+  Workspace w;
+  int st = hybrid_prologue<double>(ctx, frames, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
   if (st) return st;
   if (batch == 0) return OXM_OK;
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  if ((st = launch_ll<double>(frames, batch, d, ybar, nll, flags, s))) return st;
+  if ((st = launch_ll<double>(frames, batch, d, w.ybar, nll, flags, s))) return st;
   mark(ev, 1, s);
-  if ((st = launch_em_soa(ctx->ops, ybar, nll, S, fits, s))) return st;
+  if ((st = launch_em_soa<false>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
   mark(ev, 2, s);
   PxGeom g{height, width, d.h[n_levels], d.w[n_levels], nll, n_levels, calibration};
   const int64_t npx = batch * height * width;
+  const double* S = w.S;
   if (ctx->ops.L == 26)
-    px_f64_kernel<26><<<grid_1d(npx, 128), 128, 0, s>>>(ctx->ops, frames, g, batch, S, ybar, cube, hbo, hb, offset);
+    px_f64_kernel<26><<<grid_1d(npx, 128), 128, 0, s>>>(ctx->ops, frames, g, batch, S, w.ybar, cube, hbo, hb, offset);
   else
-    px_f64_kernel<0><<<grid_1d(npx, 128), 128, 0, s>>>(ctx->ops, frames, g, batch, S, ybar, cube, hbo, hb, offset);
+    px_f64_kernel<0><<<grid_1d(npx, 128), 128, 0, s>>>(ctx->ops, frames, g, batch, S, w.ybar, cube, hbo, hb, offset);
   st = check_launch("hybrid_px_f64");
   mark(ev, 3, s);
   return st;

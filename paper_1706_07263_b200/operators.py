@@ -111,7 +111,8 @@ def make_operator_set(
     if not 3 <= L <= _native.MAX_BANDS:
         raise ArgumentError(f"the CUDA kernels support 3..{_native.MAX_BANDS} bands, got {L}")
     z3 = np.zeros((L, 3))
-    xi_ = z3 if xi is None else np.asarray(xi, dtype=np.float64)
+    unit = np.column_stack([np.zeros((L, 2)), np.ones(L)])  # placeholder basis: (0, 0, 1) rows
+    xi_ = unit if xi is None else np.asarray(xi, dtype=np.float64)
     fit = np.zeros((3, L)) if xi is None else fit_matrix(xi_)
     return OperatorSet(
         n_bands=L,
