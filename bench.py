@@ -72,24 +72,44 @@ def operators():
 class ClockSampler:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    FIELD_SETS = [
+        ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"),
+        ("index,clocks.sm,clocks.max.sm,power.draw,clocks_throttle_reasons.active,"
+         "clocks_throttle_reasons.hw_slowdown,clocks_throttle_reasons.hw_thermal_slowdown,"
+         "clocks_throttle_reasons.sw_thermal_slowdown,clocks_throttle_reasons.sw_power_cap"),
+    ]
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = None
 
+    def _fields(self):
+        for f in self.FIELD_SETS:
+            try:
+                r = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={f}", "--format=csv,noheader,nounits"],
+                                   capture_output=True, text=True, timeout=20)
+            except (OSError, subprocess.TimeoutExpired):
+                return None
+            if r.returncode == 0 and r.stdout.strip():
+                return f
+        return None
+
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+        fields = self._fields()
+        self.proc = None
+        if fields:
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={fields}", "--format=csv,noheader,nounits",
+                     "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                time.sleep(0.3)
+            except OSError:
+                self.proc = None
         return self
 
     def __exit__(self, *a):
