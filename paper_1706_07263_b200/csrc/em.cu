@@ -1,47 +1,14 @@
 // K4: standalone low-pass estimator (estimate_lowpass, bayes.py:210-272) and
 // the shape-prior update for arbitrary (y, e) (expectation_step, bayes.py:162-182).
 //
-// One thread per coefficient; operators in constant bank 0, exp/log tables
-// and the per-thread expected spectrum in shared memory.  Spectra are
-// written row-major (n, L) like the reference's return value (this is the
-// drop-in API path; the video path is hybrid.cu's SoA em_soa_kernel).
+// The estimator is em_persistent_kernel (oxm_em.cuh); here it writes spectra
+// row-major (n, L) like the reference's return value (the drop-in API path;
+// the video path in hybrid.cu writes them SoA).
 #include "oxm_em.cuh"
 
 namespace oxm {
 namespace {
 
-constexpr int kEmThreads = 128;
-
-template <int KL>
-__global__ void __launch_bounds__(kEmThreads) em_lowpass_kernel(const __grid_constant__ DevOps ops,
-                                                                const double* __restrict__ y,
-                                                                const double* __restrict__ init, int64_t n,
-                                                                double* __restrict__ spectra,
-                                                                double* __restrict__ xout,
-                                                                int32_t* __restrict__ fits) {
-  const int L = BandCount<KL>::get(ops);
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
-  double* ecol = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
-  load_math_tables(mt);
-  __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
-  if (i >= n) return;
-  const double y0 = y[3 * i + 0], y1 = y[3 * i + 1], y2 = y[3 * i + 2];
-  double x0, x1, x2;
-  int nf;
-  double* row = spectra ? spectra + i * L : nullptr;
-  em_coefficient<KL>(ops, mt, ecol, kEmThreads, y0, y1, y2, init ? init + i * L : nullptr, x0, x1, x2, nf,
-                     [&](int l, double v) {
-                       if (row) row[l] = v;
-                     });
-  if (xout) {
-    xout[3 * i + 0] = x0;
-    xout[3 * i + 1] = x1;
-    xout[3 * i + 2] = x2;
-  }
-  if (fits) fits[i] = nf;
-}
 
 template <int KL>
 __global__ void __launch_bounds__(kEmThreads) expectation_kernel(const __grid_constant__ DevOps ops,
@@ -80,19 +47,18 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   if (!ctx || n < 0 || (n > 0 && !y)) return OXM_ERR_ARGUMENT;
   if (n == 0) return OXM_OK;
   DeviceGuard dg(ctx->device);
-  const int L = ctx->ops.L;
-  const size_t smem = em_smem_bytes(L, kEmThreads);
-  const unsigned grid = grid_1d(n, kEmThreads);
+  EmIO io{};
+  io.y = y;
+  io.y_soa = 0;
+  io.init = init;
+  io.n = n;
+  io.S = spectra;
+  io.x = x;
+  io.fits = fits;
   cudaStream_t s = as_stream(stream);
-  if (L == 26) {
-    em_lowpass_kernel<26><<<grid, kEmThreads, smem, s>>>(ctx->ops, y, init, n, spectra, x, fits);
-  } else {
-    if (smem > 48 * 1024) {
-      cudaFuncSetAttribute(em_lowpass_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    }
-    em_lowpass_kernel<0><<<grid, kEmThreads, smem, s>>>(ctx->ops, y, init, n, spectra, x, fits);
-  }
-  return check_launch("em_lowpass");
+  if (!spectra) return OXM_ERR_ARGUMENT;
+  if (ctx->ops.L == 26) return launch_em_persistent<26, SpecOut::kAosF64>(ctx->ops, io, s);
+  return launch_em_persistent<0, SpecOut::kAosF64>(ctx->ops, io, s);
 }
 
 extern "C" int oxm_expectation_step(const oxm_ctx* ctx, const double* y, const double* e, int64_t n, double* out,

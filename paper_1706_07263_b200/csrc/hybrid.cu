@@ -36,7 +36,6 @@ namespace {
 
 constexpr int kMaxLevels = 24;
 constexpr int kLlThreads = 128;
-constexpr int kEmThreads = 128;
 constexpr int kPxCols = 128;  // pixel columns per CTA in the fp32 map kernel
 constexpr int kFbThreads = 128;
 
@@ -118,36 +117,6 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const TIn* __restrict__ 
     ybar[c * nll + idx] = v;
   }
   if (flags && (bad || neg)) atomicOr(flags, (bad ? OXM_FLAG_NONFINITE : 0u) | (neg ? OXM_FLAG_NEGATIVE_LL : 0u));
-}
-
-// EM spectra of ybar[:, idx], SoA per band (coalesced): fp64 S[l][idx] for
-// the fp64 path, or an fp32 (hi, lo) pair Shi/Slo[l][idx] for the fp32 path
-// (hi + lo carries 48 significant bits: plenty for the fp64 fallback).
-template <int KL, bool F32OUT>
-__global__ void __launch_bounds__(kEmThreads) em_soa_kernel(const __grid_constant__ DevOps ops,
-                                                            const double* __restrict__ ybar, int64_t nll,
-                                                            double* __restrict__ S, float* __restrict__ Shi,
-                                                            float* __restrict__ Slo, int32_t* __restrict__ fits) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
-  double* ecol = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
-  load_math_tables(mt);
-  __syncthreads();
-  const int64_t idx = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
-  if (idx >= nll) return;
-  const double y0 = ybar[idx], y1 = ybar[nll + idx], y2 = ybar[2 * nll + idx];
-  double x0, x1, x2;
-  int nf;
-  em_coefficient<KL>(ops, mt, ecol, kEmThreads, y0, y1, y2, nullptr, x0, x1, x2, nf, [&](int l, double v) {
-    if constexpr (F32OUT) {
-      const float h = __double2float_rn(v);
-      Shi[(int64_t)l * nll + idx] = h;
-      Slo[(int64_t)l * nll + idx] = __double2float_rn(v - (double)h);
-    } else {
-      S[(int64_t)l * nll + idx] = v;
-    }
-  });
-  if (fits) fits[idx] = nf;
 }
 
 // Per-pixel fp64 spectrum + fit (used by the fp64 kernel and as the fp32
@@ -275,8 +244,10 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   }
 }
 
-// fp64 recompute of the queued pixels (grid-stride over the list).
-template <int KL>
+// fp64 recompute of the queued pixels: one warp per pixel, one band per lane
+// (the 26 band loads and logs of a pixel proceed in parallel), operators
+// staged in shared memory so the per-lane band index does not serialise
+// constant-bank reads; the three fit sums are warp-reduced.
 __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
                                                                  const float* __restrict__ frames, PxGeom g,
                                                                  const float* __restrict__ Shi,
@@ -287,9 +258,18 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
                                                                  float* __restrict__ thb, float* __restrict__ so2,
                                                                  float* __restrict__ hbo, float* __restrict__ hb,
                                                                  float* __restrict__ off) {
+  __shared__ double T[kMaxBands][3], F[3][kMaxBands];
+  const int L = ops.L;
+  for (int q = threadIdx.x; q < 3 * L; q += kFbThreads) {
+    T[q / 3][q % 3] = ops.solve[q / 3][q % 3];
+    F[q / L][q % L] = ops.fitm[q / L][q % L];
+  }
+  __syncthreads();
   const uint32_t cnt = *fb_count;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * kFbThreads) >> 5;
   const int64_t plane = g.H * g.W;
-  for (uint32_t i = blockIdx.x * kFbThreads + threadIdx.x; i < cnt; i += gridDim.x * kFbThreads) {
+  for (int64_t i = ((int64_t)blockIdx.x * kFbThreads + threadIdx.x) >> 5; i < cnt; i += warps) {
     const int64_t p = fb_list[i];
     const int64_t f = p / plane;
     const int64_t rem = p - f * plane;
@@ -298,22 +278,32 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
     const double D0 = (double)frames[3 * p] - ybar[bidx];
     const double D1 = (double)frames[3 * p + 1] - ybar[g.nll + bidx];
     const double D2 = (double)frames[3 * p + 2] - ybar[2 * g.nll + bidx];
-    double x0, x1, x2;
-    pixel_fit_f64<KL>(
-        ops,
-        [&](int l) {
-          const int64_t q = (int64_t)l * g.nll + bidx;
-          return (double)Shi[q] + (double)Slo[q];
-        },
-        D0, D1, D2, x0, x1, x2, [](int, double) {});
-    const float xo = (float)(x0 * g.cal), xd = (float)(x1 * g.cal);
-    const float co = fmaxf(xo, 0.f);
-    const float t = co + fmaxf(xd, 0.f);
-    if (thb) thb[p] = t;
-    if (so2) so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
-    if (hbo) hbo[p] = xo;
-    if (hb) hb[p] = xd;
-    if (off) off[p] = (float)x2;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int l = lane; l < L; l += 32) {
+      const int64_t q = (int64_t)l * g.nll + bidx;
+      const double S = (double)Shi[q] + (double)Slo[q];
+      const double sp = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
+      const double lg = log(fmax(sp, ops.eps));
+      a0 = fma(F[0][l], lg, a0);
+      a1 = fma(F[1][l], lg, a1);
+      a2 = fma(F[2][l], lg, a2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (lane == 0) {
+      const float xo = (float)(-a0 * g.cal), xd = (float)(-a1 * g.cal);
+      const float co = fmaxf(xo, 0.f);
+      const float t = co + fmaxf(xd, 0.f);
+      if (thb) thb[p] = t;
+      if (so2) so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
+      if (hbo) hbo[p] = xo;
+      if (hb) hb[p] = xd;
+      if (off) off[p] = (float)(-a2);
+    }
   }
 }
 
@@ -411,16 +401,17 @@ int launch_ll(const TIn* frames, int64_t batch, const LevelDims& d, double* ybar
 template <bool F32OUT>
 int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Workspace& w, int32_t* fits,
                   cudaStream_t s) {
-  const unsigned grid = grid_1d(nll, kEmThreads);
-  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
-  if (ops.L == 26) {
-    em_soa_kernel<26, F32OUT><<<grid, kEmThreads, smem, s>>>(ops, ybar, nll, w.S, w.Shi, w.Slo, fits);
-  } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(em_soa_kernel<0, F32OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    em_soa_kernel<0, F32OUT><<<grid, kEmThreads, smem, s>>>(ops, ybar, nll, w.S, w.Shi, w.Slo, fits);
-  }
-  return check_launch("hybrid_em");
+  EmIO io{};
+  io.y = ybar;
+  io.y_soa = 1;
+  io.n = nll;
+  io.S = w.S;
+  io.Shi = w.Shi;
+  io.Slo = w.Slo;
+  io.fits = fits;
+  constexpr SpecOut out = F32OUT ? SpecOut::kSoaF32Pair : SpecOut::kSoaF64;
+  if (ops.L == 26) return launch_em_persistent<26, out>(ops, io, s);
+  return launch_em_persistent<0, out>(ops, io, s);
 }
 
 template <int KL>
@@ -438,8 +429,8 @@ int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64
   }
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
-  px_fallback_kernel<KL><<<148 * 2, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, w.fb_count, w.fb_list,
-                                                         thb, so2, hbo, hb, off);
+  px_fallback_kernel<<<148 * 4, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, w.fb_count, w.fb_list,
+                                                     thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
 }
 

@@ -16,11 +16,11 @@
 // rank-3 update: 78+78 FMAs instead of a 676-FMA dense matvec.
 //
 // Performance shape (fp64-pipe bound): the expected spectrum e (L doubles)
-// lives in shared memory, not registers, and the band loops are only 2-way
-// unrolled around the table-driven exp/log of oxm_math.cuh, so the kernel is
-// ~70 registers (>= 7 warps / scheduler) and its loop fits the instruction
-// cache.  The stopping test compares squared norms (no sqrt/div); it differs
-// from the reference's rel < tol only when rel is within ~1e-16 of tol.
+// lives in shared memory, not registers, and the band loops are only 4-way
+// unrolled around the table-driven exp/log of oxm_math.cuh, so the kernel
+// stays near 64 registers and its loop fits the instruction cache.  The
+// stopping test compares squared norms (no sqrt/div); it differs from the
+// reference's rel < tol only when rel is within ~1e-16 of tol.
 #pragma once
 
 #include "oxm_common.cuh"
@@ -34,90 +34,188 @@ struct BandCount {
   __device__ __forceinline__ static int get(const DevOps& ops) { return KL > 0 ? KL : ops.L; }
 };
 
-// Runs the estimator for one coefficient.  `init` (stride 1) may be null.
-// `e` is this thread's shared-memory column (element l at e[l * es]).
-// On return x[] holds the final concentrations, fits the fit count, and the
-// final spectrum has been passed to `store(l, value)`.
-template <int KL, typename Store>
-__device__ __forceinline__ void em_coefficient(const DevOps& ops, const MathSmem& mt, double* __restrict__ e,
-                                               const int es, const double y0, const double y1, const double y2,
-                                               const double* init, double& x0, double& x1, double& x2, int& fits,
-                                               Store store) {
+// Dynamic shared memory of an EM kernel: tables + one e column per thread.
+__host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
+  return sizeof(MathSmem) + sizeof(double) * (size_t)L * (size_t)threads;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent, warp-refilled EM kernel.
+//
+// A one-thread-per-coefficient loop would leave a warp running until its slowest lane
+// converges (fit counts vary 11..15 per coefficient) and a CTA until its
+// slowest warp.  Here every warp owns a contiguous slice of the coefficients
+// and advances all its lanes one *fit* per step; a lane whose coefficient has
+// converged writes its result and immediately takes the next coefficient of
+// the slice.  The Tikhonov start is folded into the same step (e := solve y,
+// r := 0, so s = max(e + G r, eps) = max(solve y, eps) exactly), which keeps
+// the log/fit half of every step uniform across the warp.
+enum class SpecOut { kSoaF64, kSoaF32Pair, kAosF64 };
+
+struct EmIO {
+  const double* y;   // unit-scale low-pass data: SoA [3][n] (y_soa) or AoS (n, 3)
+  int y_soa;
+  const double* init;  // AoS (n, L) start spectra, or null (Tikhonov start)
+  int64_t n;
+  double* S;         // kSoaF64: [L][n];  kAosF64: (n, L)
+  float* Shi;        // kSoaF32Pair: [L][n] hi / lo
+  float* Slo;
+  double* x;         // (n, 3) or null
+  int32_t* fits;     // (n) or null
+  int64_t per_warp;  // slice length
+};
+
+constexpr int kEmThreads = 128;
+
+template <int KL, SpecOut OUT>
+__global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
+  double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
+  constexpr int es = kEmThreads;
+  load_math_tables(mt);
+  __syncthreads();
+
   const int L = BandCount<KL>::get(ops);
   const double eps = ops.eps;
-
-  // fit #1 of the (clamped) start spectrum
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll 2
-  for (int l = 0; l < L; ++l) {
-    double s = init ? init[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-    const double lg = log_tab(fmax(s, eps), mt);
-    a0 = fma(ops.fitm[0][l], lg, a0);
-    a1 = fma(ops.fitm[1][l], lg, a1);
-    a2 = fma(ops.fitm[2][l], lg, a2);
-  }
-  x0 = -a0;
-  x1 = -a1;
-  x2 = -a2;
-
   const double tol2 = ops.rel_tol * ops.rel_tol;
-  double r0 = 0.0, r1 = 0.0, r2 = 0.0;
-  int nfit = 1;
-  for (int it = 1; it < ops.max_iters; ++it) {
-    // expected spectrum e = exp(-xi x) and its RGB projection C e
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-#pragma unroll 2
-    for (int l = 0; l < L; ++l) {
-      // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
-      const double arg = fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2));
-      const double el = exp_tab(-arg, mt);
-      e[l * es] = el;
-      c0 = fma(ops.sens[0][l], el, c0);
-      c1 = fma(ops.sens[1][l], el, c1);
-      c2 = fma(ops.sens[2][l], el, c2);
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t warp = ((int64_t)blockIdx.x * kEmThreads + threadIdx.x) >> 5;
+  int64_t next = warp * io.per_warp;                 // next unassigned coefficient of the slice
+  const int64_t stop = min64(next + io.per_warp, io.n);
+
+  int64_t idx = next + lane < stop ? next + lane : -1;
+  next = min64(next + 32, stop);
+  bool init = true;
+  int nfit = 0;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, x0 = 0.0, x1 = 0.0, x2 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
+  auto load_y = [&](int64_t i) {
+    if (io.y_soa) {
+      y0 = io.y[i];
+      y1 = io.y[io.n + i];
+      y2 = io.y[2 * io.n + i];
+    } else {
+      y0 = io.y[3 * i];
+      y1 = io.y[3 * i + 1];
+      y2 = io.y[3 * i + 2];
     }
-    r0 = y0 - c0;
-    r1 = y1 - c1;
-    r2 = y2 - c2;
-    // shape-prior update and fit
+  };
+  if (idx >= 0) load_y(idx);
+
+  while (__any_sync(0xffffffffu, idx >= 0)) {
+    const bool live = idx >= 0;
+    // ---- phase A: expected spectrum e (or the start spectrum) and residual r
+    if (live) {
+      if (init) {
+        const double* ini = io.init ? io.init + idx * L : nullptr;
+#pragma unroll 4
+        for (int l = 0; l < L; ++l)
+          e[l * es] = ini ? ini[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
+        r0 = r1 = r2 = 0.0;
+      } else {
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll 4
+        for (int l = 0; l < L; ++l) {
+          // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
+          const double el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+          e[l * es] = el;
+          c0 = fma(ops.sens[0][l], el, c0);
+          c1 = fma(ops.sens[1][l], el, c1);
+          c2 = fma(ops.sens[2][l], el, c2);
+        }
+        r0 = y0 - c0;
+        r1 = y1 - c1;
+        r2 = y2 - c2;
+      }
+    }
+    // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
-#pragma unroll 2
-    for (int l = 0; l < L; ++l) {
-      const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
-      const double lg = log_tab(fmax(s, eps), mt);
-      n0 = fma(ops.fitm[0][l], lg, n0);
-      n1 = fma(ops.fitm[1][l], lg, n1);
-      n2 = fma(ops.fitm[2][l], lg, n2);
+    if (live) {
+#pragma unroll 4
+      for (int l = 0; l < L; ++l) {
+        const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
+        const double lg = log_tab(fmax(s, eps), mt);
+        n0 = fma(ops.fitm[0][l], lg, n0);
+        n1 = fma(ops.fitm[1][l], lg, n1);
+        n2 = fma(ops.fitm[2][l], lg, n2);
+      }
     }
     n0 = -n0;
     n1 = -n1;
     n2 = -n2;
-    ++nfit;
-    const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
-    const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
-    const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
-    x0 = n0;
-    x1 = n1;
-    x2 = n2;
-    if (dn2 < tol2 * fmax(xn2, 1e-16)) break;  // rel < rel_tol (bayes.py:200-204)
-  }
-  fits = nfit;
-
-  // final spectrum: the last update (recomputed from e, r) or the start
-  if (nfit > 1) {
-    for (int l = 0; l < L; ++l)
-      store(l, fmax(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps));
-  } else {
-    for (int l = 0; l < L; ++l) {
-      const double s = init ? init[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-      store(l, fmax(s, eps));
+    bool done = false;
+    if (live) {
+      if (init) {
+        init = false;
+        nfit = 1;
+        done = ops.max_iters <= 1;
+      } else {
+        ++nfit;
+        const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
+        const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+        const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
+        done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters;  // bayes.py:195-205
+      }
+      x0 = n0;
+      x1 = n1;
+      x2 = n2;
+      if (done) {
+        for (int l = 0; l < L; ++l) {
+          const double s =
+              fmax(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps);
+          if constexpr (OUT == SpecOut::kSoaF64) {
+            io.S[(int64_t)l * io.n + idx] = s;
+          } else if constexpr (OUT == SpecOut::kAosF64) {
+            io.S[idx * L + l] = s;
+          } else {
+            const float h = __double2float_rn(s);
+            io.Shi[(int64_t)l * io.n + idx] = h;
+            io.Slo[(int64_t)l * io.n + idx] = __double2float_rn(s - (double)h);
+          }
+        }
+        if (io.x) {
+          io.x[3 * idx] = x0;
+          io.x[3 * idx + 1] = x1;
+          io.x[3 * idx + 2] = x2;
+        }
+        if (io.fits) io.fits[idx] = nfit;
+      }
+    }
+    // ---- refill finished lanes from the warp's slice (no atomics)
+    const unsigned m = __ballot_sync(0xffffffffu, done);
+    if (m) {
+      if (done) {
+        const int64_t mine = next + __popc(m & lt_mask);
+        idx = mine < stop ? mine : -1;
+        init = true;
+        if (idx >= 0) load_y(idx);
+      }
+      next = min64(next + __popc(m), stop);
     }
   }
 }
 
-// Dynamic shared memory of an EM kernel: tables + one e column per thread.
-__host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
-  return sizeof(MathSmem) + sizeof(double) * (size_t)L * (size_t)threads;
+// Persistent launch geometry: enough CTAs to fill every SM once.
+template <int KL, SpecOut OUT>
+inline int launch_em_persistent(const DevOps& ops, EmIO io, cudaStream_t s) {
+  if (io.n <= 0) return OXM_OK;
+  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
+  auto kern = em_persistent_kernel<KL, OUT>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEmThreads, smem);
+  if (sms < 1) sms = 1;
+  if (per_sm < 1) per_sm = 1;
+  int64_t blocks = (int64_t)sms * per_sm;
+  const int64_t need = ceil_div(io.n, kEmThreads);
+  if (blocks > need) blocks = need;
+  const int64_t warps = blocks * (kEmThreads / 32);
+  io.per_warp = ceil_div(io.n, warps);
+  kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
+  return check_launch("em_persistent");
 }
 
 }  // namespace oxm

@@ -22,19 +22,18 @@ namespace oxm {
 constexpr double kLn2Hi42 = 0.693147180559890330187045037746;  // 0x3FE62E42FEFA3800
 constexpr double kLn2Lo42 = 5.4979230187083711552420206e-14;   // ln2 - kLn2Hi42
 
+// One shared-memory access per transcendental: exp reads 2^(j/64) (the lo
+// correction is dropped: +0.5 ulp), log reads (c_j, -ln c_j) as one 16-byte
+// word (the lo part of -ln c_j is below 2^-60 absolute and is dropped too).
 struct MathSmem {
-  double2 expt[64];     // 2^(j/64) = (hi, lo)
-  double logc[128];     // c_j
-  double loghi[128];    // -ln(c_j) hi
-  double loglo[128];    // -ln(c_j) lo
+  double expt[64];   // 2^(j/64)
+  double2 logt[128]; // (c_j, -ln(c_j))
 };
 
 __device__ __forceinline__ void load_math_tables(MathSmem& t) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) {
-    if (i < 64) t.expt[i] = make_double2(kExpTable[i][0], kExpTable[i][1]);
-    t.logc[i] = kLogTable[i][0];
-    t.loghi[i] = kLogTable[i][1];
-    t.loglo[i] = kLogTable[i][2];
+    if (i < 64) t.expt[i] = kExpTable[i][0];
+    t.logt[i] = make_double2(kLogTable[i][0], kLogTable[i][1] + kLogTable[i][2]);
   }
 }
 
@@ -50,8 +49,8 @@ __device__ __forceinline__ double exp_tab(const double z, const MathSmem& t) {
   q = fma(q, r, 1.0 / 6.0);
   q = fma(q, r, 0.5);
   const double p = fma(q, r * r, r);  // exp(r) - 1
-  const double2 T = t.expt[k & 63];
-  const double res = fma(T.x, p, T.y) + T.x;
+  const double T = t.expt[k & 63];
+  const double res = fma(T, p, T);
   const int m = k >> 6;  // floor(k / 64)
   return __hiloint2double(__double2hiint(res) + (m << 20), __double2loint(res));
 }
@@ -62,16 +61,16 @@ __device__ __forceinline__ double log_tab(const double x, const MathSmem& t) {
   const int e = (hi >> 20) - 1023;
   const int j = (hi >> 13) & 127;
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);  // [1, 2)
-  const double r = fma(m, t.logc[j], -1.0);
+  const double2 cj = t.logt[j];
+  const double r = fma(m, cj.x, -1.0);
   double q = fma(r, 1.0 / 7.0, -1.0 / 6.0);
   q = fma(q, r, 0.2);
   q = fma(q, r, -0.25);
   q = fma(q, r, 1.0 / 3.0);
   q = fma(q, r, -0.5);
   const double ed = (double)e;
-  const double h = fma(ed, kLn2Hi42, t.loghi[j]);
-  const double l = fma(ed, kLn2Lo42, t.loglo[j]);
-  return h + (r + fma(q, r * r, l));
+  const double h = fma(ed, kLn2Hi42, cj.y);
+  return h + (r + fma(q, r * r, ed * kLn2Lo42));
 }
 
 }  // namespace oxm
