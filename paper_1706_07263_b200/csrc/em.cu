@@ -47,6 +47,16 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   if (!ctx || n < 0 || (n > 0 && !y)) return OXM_ERR_ARGUMENT;
   if (n == 0) return OXM_OK;
   DeviceGuard dg(ctx->device);
+  if (!spectra) return OXM_ERR_ARGUMENT;
+  cudaStream_t s = as_stream(stream);
+  // scratch: x_prev [3][n] (+ fit counts when the caller does not want them)
+  void* scratch = nullptr;
+  const size_t bytes = sizeof(double) * 3 * (size_t)n + (fits ? 0 : sizeof(int32_t) * (size_t)n);
+  cudaError_t err = cudaMallocAsync(&scratch, bytes, s);
+  if (err != cudaSuccess) {
+    set_last_error("em_lowpass scratch", err);
+    return OXM_ERR_CUDA;
+  }
   EmIO io{};
   io.y = y;
   io.y_soa = 0;
@@ -54,11 +64,12 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   io.n = n;
   io.S = spectra;
   io.x = x;
-  io.fits = fits;
-  cudaStream_t s = as_stream(stream);
-  if (!spectra) return OXM_ERR_ARGUMENT;
-  if (ctx->ops.L == 26) return launch_em_persistent<26, SpecOut::kAosF64>(ctx->ops, io, s);
-  return launch_em_persistent<0, SpecOut::kAosF64>(ctx->ops, io, s);
+  io.xprev = static_cast<double*>(scratch);
+  io.fits = fits ? fits : reinterpret_cast<int32_t*>(io.xprev + 3 * n);
+  const int st = ctx->ops.L == 26 ? launch_em<26, SpecOut::kAosF64>(ctx->ops, io, s)
+                                  : launch_em<0, SpecOut::kAosF64>(ctx->ops, io, s);
+  cudaFreeAsync(scratch, s);
+  return st;
 }
 
 extern "C" int oxm_expectation_step(const oxm_ctx* ctx, const double* y, const double* e, int64_t n, double* out,

@@ -353,12 +353,15 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
 // Workspace (256-B aligned sections):
 //   ybar  3 x nll  double
 //   spectra  L x nll x 8 B   (fp64 S, or fp32 Shi followed by fp32 Slo)
+//   x_prev   3 x nll  double,  fit counts  nll  int32   (EM bookkeeping)
 //   fallback counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
 struct Workspace {
   double* ybar;
   double* S;
   float* Shi;
   float* Slo;
+  double* xprev;
+  int32_t* fits;
   uint32_t* fb_count;
   uint32_t* fb_list;
 };
@@ -367,7 +370,8 @@ inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 size_t workspace_bytes(int L, int64_t nll, int64_t npx) {
   return 256 + align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(double) * (size_t)L * (size_t)nll) +
-         256 + align256(sizeof(uint32_t) * (size_t)npx);
+         align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) + 256 +
+         align256(sizeof(uint32_t) * (size_t)npx);
 }
 
 Workspace carve(void* ws, int L, int64_t nll) {
@@ -379,6 +383,10 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.Shi = reinterpret_cast<float*>(p);
   w.Slo = w.Shi + (size_t)L * (size_t)nll;
   p += align256(sizeof(double) * (size_t)L * (size_t)nll);
+  w.xprev = reinterpret_cast<double*>(p);
+  p += align256(sizeof(double) * 3 * (size_t)nll);
+  w.fits = reinterpret_cast<int32_t*>(p);
+  p += align256(sizeof(int32_t) * (size_t)nll);
   w.fb_count = reinterpret_cast<uint32_t*>(p);
   w.fb_list = reinterpret_cast<uint32_t*>(p + 256);
   return w;
@@ -408,10 +416,11 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   io.S = w.S;
   io.Shi = w.Shi;
   io.Slo = w.Slo;
-  io.fits = fits;
+  io.xprev = w.xprev;
+  io.fits = fits ? fits : w.fits;
   constexpr SpecOut out = F32OUT ? SpecOut::kSoaF32Pair : SpecOut::kSoaF64;
-  if (ops.L == 26) return launch_em_persistent<26, out>(ops, io, s);
-  return launch_em_persistent<0, out>(ops, io, s);
+  if (ops.L == 26) return launch_em<26, out>(ops, io, s);
+  return launch_em<0, out>(ops, io, s);
 }
 
 template <int KL>

@@ -42,32 +42,43 @@ __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
 // ---------------------------------------------------------------------------
 // Persistent, warp-refilled EM kernel.
 //
-// A one-thread-per-coefficient loop would leave a warp running until its slowest lane
-// converges (fit counts vary 11..15 per coefficient) and a CTA until its
-// slowest warp.  Here every warp owns a contiguous slice of the coefficients
-// and advances all its lanes one *fit* per step; a lane whose coefficient has
-// converged writes its result and immediately takes the next coefficient of
-// the slice.  The Tikhonov start is folded into the same step (e := solve y,
-// r := 0, so s = max(e + G r, eps) = max(solve y, eps) exactly), which keeps
-// the log/fit half of every step uniform across the warp.
+// A one-thread-per-coefficient loop would leave a warp running until its
+// slowest lane converges (fit counts vary 11..15 per coefficient) and a CTA
+// until its slowest warp.  Here every warp owns a contiguous slice of the
+// coefficients and advances all its lanes one *fit* per step; a lane whose
+// coefficient has converged records it and immediately takes the next one.
+//
+// Every step is warp-uniform: the Tikhonov start is folded in as
+// e := solve y (or init), r := 0, so s = max(e + G r, eps) = max(solve y, eps)
+// exactly; lanes in their start step still evaluate (and discard) the exp.
+// Uniform control flow keeps the band counter in a uniform register, so the
+// operator entries are uniform-datapath constants (ULDC / UR operands) rather
+// than per-thread indexed LDCs feeding every DFMA.
+//
+// The final spectrum is not written here (that would be a 26-store divergent
+// branch in almost every step): the kernel stores x_prev -- the concentration
+// the final step started from -- and em_spectra_kernel rebuilds
+// s = max(exp(-xi x_prev) + G (y - C exp(-xi x_prev)), eps) with the same
+// exp_tab, bit-identically, with coalesced stores.
 enum class SpecOut { kSoaF64, kSoaF32Pair, kAosF64 };
 
 struct EmIO {
-  const double* y;   // unit-scale low-pass data: SoA [3][n] (y_soa) or AoS (n, 3)
+  const double* y;     // unit-scale low-pass data: SoA [3][n] (y_soa) or AoS (n, 3)
   int y_soa;
   const double* init;  // AoS (n, L) start spectra, or null (Tikhonov start)
   int64_t n;
-  double* S;         // kSoaF64: [L][n];  kAosF64: (n, L)
-  float* Shi;        // kSoaF32Pair: [L][n] hi / lo
+  double* S;           // kSoaF64: [L][n];  kAosF64: (n, L)
+  float* Shi;          // kSoaF32Pair: [L][n] hi / lo
   float* Slo;
-  double* x;         // (n, 3) or null
-  int32_t* fits;     // (n) or null
-  int64_t per_warp;  // slice length
+  double* x;           // (n, 3) final concentrations, or null
+  double* xprev;       // [3][n] concentration the final fit step started from (required)
+  int32_t* fits;       // (n) fit counts (required)
+  int64_t per_warp;    // slice length
 };
 
 constexpr int kEmThreads = 128;
 
-template <int KL, SpecOut OUT>
+template <int KL, bool HAS_INIT>
 __global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
@@ -82,14 +93,14 @@ __global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t warp = ((int64_t)blockIdx.x * kEmThreads + threadIdx.x) >> 5;
-  int64_t next = warp * io.per_warp;                 // next unassigned coefficient of the slice
+  int64_t next = warp * io.per_warp;  // next unassigned coefficient of the slice
   const int64_t stop = min64(next + io.per_warp, io.n);
 
   int64_t idx = next + lane < stop ? next + lane : -1;
   next = min64(next + 32, stop);
   bool init = true;
   int nfit = 0;
-  double y0 = 0.0, y1 = 0.0, y2 = 0.0, x0 = 0.0, x1 = 0.0, x2 = 0.0, r0 = 0.0, r1 = 0.0, r2 = 0.0;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
   auto load_y = [&](int64_t i) {
     if (io.y_soa) {
       y0 = io.y[i];
@@ -104,50 +115,44 @@ __global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_
   if (idx >= 0) load_y(idx);
 
   while (__any_sync(0xffffffffu, idx >= 0)) {
-    const bool live = idx >= 0;
     // ---- phase A: expected spectrum e (or the start spectrum) and residual r
-    if (live) {
-      if (init) {
-        const double* ini = io.init ? io.init + idx * L : nullptr;
-#pragma unroll 4
-        for (int l = 0; l < L; ++l)
-          e[l * es] = ini ? ini[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-        r0 = r1 = r2 = 0.0;
-      } else {
-        double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-#pragma unroll 4
-        for (int l = 0; l < L; ++l) {
-          // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
-          const double el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
-          e[l * es] = el;
-          c0 = fma(ops.sens[0][l], el, c0);
-          c1 = fma(ops.sens[1][l], el, c1);
-          c2 = fma(ops.sens[2][l], el, c2);
-        }
-        r0 = y0 - c0;
-        r1 = y1 - c1;
-        r2 = y2 - c2;
-      }
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    const double* ini = HAS_INIT && idx >= 0 ? io.init + idx * L : nullptr;
+#pragma unroll 2
+    for (int l = 0; l < L; ++l) {
+      // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
+      const double ex = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+      double st;
+      if constexpr (HAS_INIT)
+        st = ini ? ini[l] : 0.0;
+      else
+        st = fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
+      const double el = init ? st : ex;
+      e[l * es] = el;
+      c0 = fma(ops.sens[0][l], el, c0);
+      c1 = fma(ops.sens[1][l], el, c1);
+      c2 = fma(ops.sens[2][l], el, c2);
     }
+    const double r0 = init ? 0.0 : y0 - c0;
+    const double r1 = init ? 0.0 : y1 - c1;
+    const double r2 = init ? 0.0 : y2 - c2;
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
-    if (live) {
-#pragma unroll 4
-      for (int l = 0; l < L; ++l) {
-        const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
-        const double lg = log_tab(fmax(s, eps), mt);
-        n0 = fma(ops.fitm[0][l], lg, n0);
-        n1 = fma(ops.fitm[1][l], lg, n1);
-        n2 = fma(ops.fitm[2][l], lg, n2);
-      }
+#pragma unroll 2
+    for (int l = 0; l < L; ++l) {
+      const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
+      const double lg = log_tab(fmax(s, eps), mt);
+      n0 = fma(ops.fitm[0][l], lg, n0);
+      n1 = fma(ops.fitm[1][l], lg, n1);
+      n2 = fma(ops.fitm[2][l], lg, n2);
     }
     n0 = -n0;
     n1 = -n1;
     n2 = -n2;
+    // ---- bookkeeping: stopping rule of bayes.py:195-205
     bool done = false;
-    if (live) {
+    if (idx >= 0) {
       if (init) {
-        init = false;
         nfit = 1;
         done = ops.max_iters <= 1;
       } else {
@@ -155,33 +160,24 @@ __global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_
         const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
         const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
         const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
-        done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters;  // bayes.py:195-205
+        done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters;
       }
-      x0 = n0;
-      x1 = n1;
-      x2 = n2;
       if (done) {
-        for (int l = 0; l < L; ++l) {
-          const double s =
-              fmax(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps);
-          if constexpr (OUT == SpecOut::kSoaF64) {
-            io.S[(int64_t)l * io.n + idx] = s;
-          } else if constexpr (OUT == SpecOut::kAosF64) {
-            io.S[idx * L + l] = s;
-          } else {
-            const float h = __double2float_rn(s);
-            io.Shi[(int64_t)l * io.n + idx] = h;
-            io.Slo[(int64_t)l * io.n + idx] = __double2float_rn(s - (double)h);
-          }
-        }
+        io.xprev[idx] = x0;
+        io.xprev[io.n + idx] = x1;
+        io.xprev[2 * io.n + idx] = x2;
+        io.fits[idx] = nfit;
         if (io.x) {
-          io.x[3 * idx] = x0;
-          io.x[3 * idx + 1] = x1;
-          io.x[3 * idx + 2] = x2;
+          io.x[3 * idx] = n0;
+          io.x[3 * idx + 1] = n1;
+          io.x[3 * idx + 2] = n2;
         }
-        if (io.fits) io.fits[idx] = nfit;
       }
     }
+    x0 = n0;
+    x1 = n1;
+    x2 = n2;
+    init = false;
     // ---- refill finished lanes from the warp's slice (no atomics)
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if (m) {
@@ -196,13 +192,73 @@ __global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_
   }
 }
 
-// Persistent launch geometry: enough CTAs to fill every SM once.
+// Final spectra from (y, x_prev, fits): one thread per coefficient, the
+// same arithmetic as the last EM step, coalesced stores.
 template <int KL, SpecOut OUT>
-inline int launch_em_persistent(const DevOps& ops, EmIO io, cudaStream_t s) {
+__global__ void __launch_bounds__(kEmThreads) em_spectra_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
+  double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
+  constexpr int es = kEmThreads;
+  load_math_tables(mt);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
+  if (i >= io.n) return;
+  const int L = BandCount<KL>::get(ops);
+  double y0, y1, y2;
+  if (io.y_soa) {
+    y0 = io.y[i];
+    y1 = io.y[io.n + i];
+    y2 = io.y[2 * io.n + i];
+  } else {
+    y0 = io.y[3 * i];
+    y1 = io.y[3 * i + 1];
+    y2 = io.y[3 * i + 2];
+  }
+  const bool start_only = io.fits[i] <= 1;
+  const double x0 = io.xprev[i], x1 = io.xprev[io.n + i], x2 = io.xprev[2 * io.n + i];
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll 2
+  for (int l = 0; l < L; ++l) {
+    double el;
+    if (start_only)
+      el = io.init ? io.init[i * L + l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
+    else
+      el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+    e[l * es] = el;
+    c0 = fma(ops.sens[0][l], el, c0);
+    c1 = fma(ops.sens[1][l], el, c1);
+    c2 = fma(ops.sens[2][l], el, c2);
+  }
+  const double r0 = start_only ? 0.0 : y0 - c0;
+  const double r1 = start_only ? 0.0 : y1 - c1;
+  const double r2 = start_only ? 0.0 : y2 - c2;
+  for (int l = 0; l < L; ++l) {
+    const double s = fmax(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), ops.eps);
+    if constexpr (OUT == SpecOut::kSoaF64) {
+      io.S[(int64_t)l * io.n + i] = s;
+    } else if constexpr (OUT == SpecOut::kAosF64) {
+      io.S[i * L + l] = s;
+    } else {
+      const float h = __double2float_rn(s);
+      io.Shi[(int64_t)l * io.n + i] = h;
+      io.Slo[(int64_t)l * io.n + i] = __double2float_rn(s - (double)h);
+    }
+  }
+}
+
+// Persistent EM launch (enough CTAs to fill every SM once) + spectra kernel.
+template <int KL, SpecOut OUT>
+inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (io.n <= 0) return OXM_OK;
+  if (!io.xprev || !io.fits) return OXM_ERR_ARGUMENT;
   const size_t smem = em_smem_bytes(ops.L, kEmThreads);
-  auto kern = em_persistent_kernel<KL, OUT>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = io.init ? em_persistent_kernel<KL, true> : em_persistent_kernel<KL, false>;
+  auto kspec = em_spectra_kernel<KL, OUT>;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(kspec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -215,7 +271,10 @@ inline int launch_em_persistent(const DevOps& ops, EmIO io, cudaStream_t s) {
   const int64_t warps = blocks * (kEmThreads / 32);
   io.per_warp = ceil_div(io.n, warps);
   kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
-  return check_launch("em_persistent");
+  int st = check_launch("em_persistent");
+  if (st) return st;
+  kspec<<<(unsigned)need, kEmThreads, smem, s>>>(ops, io);
+  return check_launch("em_spectra");
 }
 
 }  // namespace oxm
