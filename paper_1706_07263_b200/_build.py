@@ -64,18 +64,22 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    """Compile (if stale) and return the path of the shared library."""
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines: tuple[str, ...] = (),
+          out: pathlib.Path | None = None) -> pathlib.Path:
+    """Compile (if stale) and return the path of the shared library.
+    ``defines``/``out`` build a tuning variant elsewhere (tools/em_variants.py)."""
+    libpath = LIBPATH if out is None else out
+    if out is None and not defines and not force and up_to_date():
         return LIBPATH
     nvcc = _nvcc()
-    OBJDIR.mkdir(parents=True, exist_ok=True)
-    LIBDIR.mkdir(parents=True, exist_ok=True)
+    objdir = OBJDIR if out is None else out.parent / "obj"
+    objdir.mkdir(parents=True, exist_ok=True)
+    libpath.parent.mkdir(parents=True, exist_ok=True)
     logs = {}
 
     def compile_one(src: pathlib.Path) -> pathlib.Path:
-        obj = OBJDIR / (src.stem + ".o")
-        cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         logs[src.name] = res.stdout + res.stderr
         if res.returncode != 0:
@@ -84,17 +88,18 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
         objs = list(pool.map(compile_one, _sources()))
-    tmp = LIBPATH.with_suffix(".so.tmp")
+    tmp = libpath.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH, "-shared", "--cudart", "static", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")
-    os.replace(tmp, LIBPATH)
-    (ROOT / "build" / "ptxas.log").write_text("\n".join(f"== {k}\n{v}" for k, v in sorted(logs.items())))
+    os.replace(tmp, libpath)
+    (libpath.parent / "ptxas.log" if out is not None else ROOT / "build" / "ptxas.log").write_text(
+        "\n".join(f"== {k}\n{v}" for k, v in sorted(logs.items())))
     if verbose:
         for k, v in sorted(logs.items()):
             print(f"== {k}\n{v}")
-    return LIBPATH
+    return libpath
 
 
 if __name__ == "__main__":

@@ -20,7 +20,11 @@ from .errors import (
     SingularOperatorError,
 )
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "_lib" / "liboximap_b200.so"
+import os
+
+# OXM_LIB_PATH overrides the in-tree library (tools/em_variants.py builds
+# tuning variants); the default is the in-tree build.
+LIB_PATH = pathlib.Path(os.environ.get("OXM_LIB_PATH") or pathlib.Path(__file__).resolve().parent / "_lib" / "liboximap_b200.so")
 HEADER_PATH = pathlib.Path(__file__).resolve().parent.parent / "include" / "oximap_b200.h"
 
 OXM_OK = 0

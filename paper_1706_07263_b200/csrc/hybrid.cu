@@ -157,13 +157,13 @@ __device__ __forceinline__ float lg2_approx(float v) {
 // fp32 map kernel.  CTA = kPxCols columns x R rows of one low-pass block row
 // of one frame; each thread owns one column and R rows and walks the bands
 // once, updating its R pixels per band (R independent MUFU/FMA chains).
-// The block spectrum (hi, lo) is read straight from L1/L2: the 2^n threads of
-// a block column share each line.
+// The block spectrum is L (hi, lo) float pairs, contiguous per coefficient:
+// 16-byte loads with immediate offsets, shared by the 2^n threads of a block
+// column through L1.
 template <int KL, int R>
 __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__ DevOps ops,
                                                          const float* __restrict__ frames, PxGeom g,
-                                                         const float* __restrict__ Shi,
-                                                         const float* __restrict__ Slo,
+                                                         const float2* __restrict__ Sp,
                                                          const double* __restrict__ ybar, float* __restrict__ thb,
                                                          float* __restrict__ so2, float* __restrict__ hbo,
                                                          float* __restrict__ hb, float* __restrict__ off,
@@ -198,11 +198,8 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
     }
     vmin[r] = 3.0e38f;
   }
-#pragma unroll(KL > 0 ? LM : 1)
-  for (int l = 0; l < LM; ++l) {
-    if (KL == 0 && l >= L) break;
-    const float sh = ldg(Shi + (int64_t)l * g.nll + bidx);
-    const float sl = ldg(Slo + (int64_t)l * g.nll + bidx);
+  const float2* sp = Sp + bidx * L;
+  auto band = [&](int l, float sh, float sl) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const float s = fmaf(ops.solve_f[l][2], d[r][2], fmaf(ops.solve_f[l][1], d[r][1], fmaf(ops.solve_f[l][0], d[r][0], sl))) + sh;
@@ -212,34 +209,59 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
       acc[r][1] = fmaf(ops.fitl2_f[1][l], lg, acc[r][1]);
       acc[r][2] = fmaf(ops.fitl2_f[2][l], lg, acc[r][2]);
     }
+  };
+  if constexpr (KL > 0 && KL % 2 == 0) {
+    // two bands per 16-byte load (row start is 16-B aligned: 8*L % 16 == 0)
+    const float4* sp4 = reinterpret_cast<const float4*>(sp);
+#pragma unroll
+    for (int q = 0; q < KL / 2; ++q) {
+      const float4 v = ldg(sp4 + q);
+      band(2 * q, v.x, v.y);
+      band(2 * q + 1, v.z, v.w);
+    }
+  } else {
+#pragma unroll(KL > 0 ? LM : 1)
+    for (int l = 0; l < LM; ++l) {
+      if (KL == 0 && l >= L) break;
+      const float2 v = ldg(sp + l);
+      band(l, v.x, v.y);
+    }
   }
   const float cal = (float)g.cal;
   const float thr = (float)ops.fallback_below;
-  const unsigned active = __activemask();
-  const int lane = threadIdx.x & 31;
+  bool any_fb = false;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const bool ok = r < nrow;
     const int64_t p = (f * g.H + row0 + r) * g.W + col;
-    if (ok) {
+    if (r < nrow) {
       const float xo = acc[r][0] * cal, xd = acc[r][1] * cal;
       const float co = fmaxf(xo, 0.f);
       const float t = co + fmaxf(xd, 0.f);
-      if (thb) thb[p] = t;
-      if (so2) so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
-      if (hbo) hbo[p] = xo;
-      if (hb) hb[p] = xd;
-      if (off) off[p] = acc[r][2];
+      thb[p] = t;
+      so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
+      if (hbo) {
+        hbo[p] = xo;
+        hb[p] = xd;
+        off[p] = acc[r][2];
+      }
+      any_fb |= vmin[r] < thr;
     }
-    // cancellation guard: queue the pixel for the fp64 fixup kernel
-    const bool need = ok && vmin[r] < thr;
-    const unsigned m = __ballot_sync(active, need);
-    if (m) {
-      const int leader = __ffs(m) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
-      base = __shfl_sync(active, base, leader);
-      if (need) fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)p;
+  }
+  // cancellation guard: queue pixels for the fp64 fixup kernel (rare)
+  const unsigned active = __activemask();
+  if (__any_sync(active, any_fb)) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool need = r < nrow && vmin[r] < thr;
+      const unsigned m = __ballot_sync(active, need);
+      if (m) {
+        const int leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
+        base = __shfl_sync(active, base, leader);
+        if (need) fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col);
+      }
     }
   }
 }
@@ -250,8 +272,7 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
 // constant-bank reads; the three fit sums are warp-reduced.
 __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
                                                                  const float* __restrict__ frames, PxGeom g,
-                                                                 const float* __restrict__ Shi,
-                                                                 const float* __restrict__ Slo,
+                                                                 const float2* __restrict__ Sp,
                                                                  const double* __restrict__ ybar,
                                                                  const uint32_t* __restrict__ fb_count,
                                                                  const uint32_t* __restrict__ fb_list,
@@ -280,8 +301,8 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
     const double D2 = (double)frames[3 * p + 2] - ybar[2 * g.nll + bidx];
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     for (int l = lane; l < L; l += 32) {
-      const int64_t q = (int64_t)l * g.nll + bidx;
-      const double S = (double)Shi[q] + (double)Slo[q];
+      const float2 v = Sp[bidx * L + l];
+      const double S = (double)v.x + (double)v.y;
       const double sp = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
       const double lg = log(fmax(sp, ops.eps));
       a0 = fma(F[0][l], lg, a0);
@@ -352,14 +373,13 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
 
 // Workspace (256-B aligned sections):
 //   ybar  3 x nll  double
-//   spectra  L x nll x 8 B   (fp64 S, or fp32 Shi followed by fp32 Slo)
+//   spectra  L x nll x 8 B   (fp64 SoA S[l][i], or fp32 (hi, lo) pairs Sp[i][l])
 //   x_prev   3 x nll  double,  fit counts  nll  int32   (EM bookkeeping)
 //   fallback counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
 struct Workspace {
   double* ybar;
   double* S;
-  float* Shi;
-  float* Slo;
+  float2* Sp;
   double* xprev;
   int32_t* fits;
   uint32_t* fb_count;
@@ -380,8 +400,7 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.ybar = reinterpret_cast<double*>(p);
   p += align256(sizeof(double) * 3 * (size_t)nll);
   w.S = reinterpret_cast<double*>(p);
-  w.Shi = reinterpret_cast<float*>(p);
-  w.Slo = w.Shi + (size_t)L * (size_t)nll;
+  w.Sp = reinterpret_cast<float2*>(p);
   p += align256(sizeof(double) * (size_t)L * (size_t)nll);
   w.xprev = reinterpret_cast<double*>(p);
   p += align256(sizeof(double) * 3 * (size_t)nll);
@@ -414,11 +433,10 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   io.y_soa = 1;
   io.n = nll;
   io.S = w.S;
-  io.Shi = w.Shi;
-  io.Slo = w.Slo;
+  io.Sp = w.Sp;
   io.xprev = w.xprev;
   io.fits = fits ? fits : w.fits;
-  constexpr SpecOut out = F32OUT ? SpecOut::kSoaF32Pair : SpecOut::kSoaF64;
+  constexpr SpecOut out = F32OUT ? SpecOut::kAosF32Pair : SpecOut::kSoaF64;
   if (ops.L == 26) return launch_em<26, out>(ops, io, s);
   return launch_em<0, out>(ops, io, s);
 }
@@ -432,13 +450,13 @@ int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64
   dim3 grid((unsigned)ceil_div(g.W, kPxCols), (unsigned)(g.hL * cpb), (unsigned)batch);
   if (g.hL * cpb > 65535 || batch > 65535) return OXM_ERR_ARGUMENT;
   switch (R) {
-    case 2: px_f32_kernel<KL, 2><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    case 4: px_f32_kernel<KL, 4><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    default: px_f32_kernel<KL, 8><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    case 2: px_f32_kernel<KL, 2><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Sp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    case 4: px_f32_kernel<KL, 4><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Sp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    default: px_f32_kernel<KL, 8><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Sp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
   }
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
-  px_fallback_kernel<<<148 * 4, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.ybar, w.fb_count, w.fb_list,
+  px_fallback_kernel<<<148 * 4, kFbThreads, 0, s>>>(ops, frames, g, w.Sp, w.ybar, w.fb_count, w.fb_list,
                                                      thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
 }

@@ -16,6 +16,10 @@ constexpr int kMaxBands = OXM_MAX_BANDS;
 // c[0x0][...] operand (uniform across the warp, no LDS/LDG).  ~9.3 KB, well
 // under the 32 KB kernel-parameter limit of CUDA >= 12.1.
 struct DevOps {
+  // fp32 copies first: low parameter-bank offsets encode directly in FFMA
+  float solve_f[kMaxBands][3];
+  float fitl2_f[3][kMaxBands];  // -ln(2) * fit_mat: x = sum_l fitl2 * log2(s)
+  float eps_f;
   int L;
   int max_iters;
   double eps;
@@ -26,9 +30,6 @@ struct DevOps {
   double xi[kMaxBands][3];     // chromophore basis, core.py:134-158
   double sens[3][kMaxBands];   // camera matrix C, core.py:112-131
   double gain[kMaxBands][3];   // N^-1 C^T, N = C^T C + beta D2^T D2 (bayes.py:117-129)
-  float solve_f[kMaxBands][3];
-  float fitl2_f[3][kMaxBands];  // -ln(2) * fit_mat: x = sum_l fitl2 * log2(s)
-  float eps_f;
 };
 
 struct oxm_ctx_impl {

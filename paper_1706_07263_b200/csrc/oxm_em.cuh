@@ -26,6 +26,14 @@
 #include "oxm_common.cuh"
 #include "oxm_math.cuh"
 
+// band-loop unroll of the EM step (tuned on B200; build knob for experiments)
+#ifndef OXM_EM_UNROLL
+#define OXM_EM_UNROLL 2
+#endif
+#ifndef OXM_EM_MIN_BLOCKS
+#define OXM_EM_MIN_BLOCKS 1
+#endif
+
 namespace oxm {
 
 template <int KL>
@@ -60,7 +68,7 @@ __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
 // the final step started from -- and em_spectra_kernel rebuilds
 // s = max(exp(-xi x_prev) + G (y - C exp(-xi x_prev)), eps) with the same
 // exp_tab, bit-identically, with coalesced stores.
-enum class SpecOut { kSoaF64, kSoaF32Pair, kAosF64 };
+enum class SpecOut { kSoaF64, kAosF32Pair, kAosF64 };
 
 struct EmIO {
   const double* y;     // unit-scale low-pass data: SoA [3][n] (y_soa) or AoS (n, 3)
@@ -68,8 +76,7 @@ struct EmIO {
   const double* init;  // AoS (n, L) start spectra, or null (Tikhonov start)
   int64_t n;
   double* S;           // kSoaF64: [L][n];  kAosF64: (n, L)
-  float* Shi;          // kSoaF32Pair: [L][n] hi / lo
-  float* Slo;
+  float2* Sp;          // kAosF32Pair: (n, L) of (hi, lo), hi + lo = s to 48 bits
   double* x;           // (n, 3) final concentrations, or null
   double* xprev;       // [3][n] concentration the final fit step started from (required)
   int32_t* fits;       // (n) fit counts (required)
@@ -77,9 +84,10 @@ struct EmIO {
 };
 
 constexpr int kEmThreads = 128;
+constexpr int kEmUnroll = OXM_EM_UNROLL;
 
 template <int KL, bool HAS_INIT>
-__global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+__global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
   double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_
     // ---- phase A: expected spectrum e (or the start spectrum) and residual r
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
     const double* ini = HAS_INIT && idx >= 0 ? io.init + idx * L : nullptr;
-#pragma unroll 2
+#pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
       // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
       const double ex = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
@@ -138,7 +146,7 @@ __global__ void __launch_bounds__(kEmThreads) em_persistent_kernel(const __grid_
     const double r2 = init ? 0.0 : y2 - c2;
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
-#pragma unroll 2
+#pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
       const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
       const double lg = log_tab(fmax(s, eps), mt);
@@ -241,8 +249,7 @@ __global__ void __launch_bounds__(kEmThreads) em_spectra_kernel(const __grid_con
       io.S[i * L + l] = s;
     } else {
       const float h = __double2float_rn(s);
-      io.Shi[(int64_t)l * io.n + i] = h;
-      io.Slo[(int64_t)l * io.n + i] = __double2float_rn(s - (double)h);
+      io.Sp[i * L + l] = make_float2(h, __double2float_rn(s - (double)h));
     }
   }
 }
