@@ -36,6 +36,9 @@
 
 namespace oxm {
 
+// max(s, eps) for finite s (no NaN handling: 3 instructions instead of ~8)
+__device__ __forceinline__ double clamp_eps(double s, double eps) { return s > eps ? s : eps; }
+
 template <int KL>
 struct BandCount {
   static constexpr int kMax = KL > 0 ? KL : kMaxBands;
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
       const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
-      const double lg = log_tab(fmax(s, eps), mt);
+      const double lg = log_tab(clamp_eps(s, eps), mt);
       n0 = fma(ops.fitm[0][l], lg, n0);
       n1 = fma(ops.fitm[1][l], lg, n1);
       n2 = fma(ops.fitm[2][l], lg, n2);

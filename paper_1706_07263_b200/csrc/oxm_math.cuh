@@ -18,9 +18,27 @@
 
 namespace oxm {
 
-// ln 2 split with a 42-bit high part so e * kLn2Hi42 is exact for |e| < 2^11
-constexpr double kLn2Hi42 = 0.693147180559890330187045037746;  // 0x3FE62E42FEFA3800
-constexpr double kLn2Lo42 = 5.4979230187083711552420206e-14;   // ln2 - kLn2Hi42
+// fp64 SASS instructions take 32-bit immediates (the high word of a double
+// whose low word is zero) but no constant-bank operands, so every other
+// constant must be (re)materialised in registers inside the loop.  Constants
+// below are therefore split or rounded to 20-bit-mantissa "immediate" doubles
+// wherever the accuracy budget allows; only four full-precision constants
+// remain (kExpLo, kInv6, kInv3, kLn2Lo20).
+constexpr double k64OverLn2I = 92.33245849609375;        // 0x4057154700000000 (rounding only)
+constexpr double kLn2Over64I = 0.010830417275428772;     // 0x3F862E4200000000 = hi part of ln2/64
+constexpr double kExpLo = 7.420820373486988e-09;         // ln2/64 - kLn2Over64I
+constexpr double kLn2I = 0.6931467056274414;             // 0x3FE62E4200000000 = hi part of ln2
+constexpr double kLn2Lo20 = 4.7493250390316726e-07;      // ln2 - kLn2I
+constexpr double kInv6 = 1.0 / 6.0;
+constexpr double kInv3 = 1.0 / 3.0;
+// 20-bit-mantissa polynomial tail coefficients: |error| contributions below
+// 1e-17 relative for |r| <= ln2/128 (exp) and |r| <= 2^-8 (log)
+constexpr double kC720 = 0.00138888880610466;
+constexpr double kC120 = 0.00833333283662796;
+constexpr double kC24 = 0.041666656732559204;
+constexpr double kC7 = 0.14285719394683838;
+constexpr double kCm6 = -0.16666662693023682;
+constexpr double kC5 = 0.20000004768371582;
 
 // One shared-memory access per transcendental: exp reads 2^(j/64) (the lo
 // correction is dropped: +0.5 ulp), log reads (c_j, -ln c_j) as one 16-byte
@@ -39,14 +57,14 @@ __device__ __forceinline__ void load_math_tables(MathSmem& t) {
 
 __device__ __forceinline__ double exp_tab(const double z, const MathSmem& t) {
   const double magic = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest integer trick
-  const double km = fma(z, k64OverLn2, magic);
+  const double km = fma(z, k64OverLn2I, magic);
   const int k = __double2loint(km);
   const double kd = km - magic;
-  double r = fma(-kd, kLn2Over64Hi, z);
-  r = fma(-kd, kLn2Over64Lo, r);
-  double q = fma(r, 1.0 / 720.0, 1.0 / 120.0);
-  q = fma(q, r, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);
+  double r = fma(-kd, kLn2Over64I, z);  // exact: kd * kLn2Over64I has <= 32 significant bits
+  r = fma(-kd, kExpLo, r);
+  double q = fma(r, kC720, kC120);
+  q = fma(q, r, kC24);
+  q = fma(q, r, kInv6);
   q = fma(q, r, 0.5);
   const double p = fma(q, r * r, r);  // exp(r) - 1
   const double T = t.expt[k & 63];
@@ -63,14 +81,14 @@ __device__ __forceinline__ double log_tab(const double x, const MathSmem& t) {
   const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, lo);  // [1, 2)
   const double2 cj = t.logt[j];
   const double r = fma(m, cj.x, -1.0);
-  double q = fma(r, 1.0 / 7.0, -1.0 / 6.0);
-  q = fma(q, r, 0.2);
+  double q = fma(r, kC7, kCm6);
+  q = fma(q, r, kC5);
   q = fma(q, r, -0.25);
-  q = fma(q, r, 1.0 / 3.0);
+  q = fma(q, r, kInv3);
   q = fma(q, r, -0.5);
   const double ed = (double)e;
-  const double h = fma(ed, kLn2Hi42, cj.y);
-  return h + (r + fma(q, r * r, ed * kLn2Lo42));
+  const double h = fma(ed, kLn2I, cj.y);  // ed * kLn2I exact (20 x 11 bits)
+  return h + (r + fma(q, r * r, ed * kLn2Lo20));
 }
 
 }  // namespace oxm

@@ -18,9 +18,9 @@ VARIANTS = {
     "u2": ("OXM_EM_UNROLL=2",),
     "u4": ("OXM_EM_UNROLL=4",),
     "u13": ("OXM_EM_UNROLL=13",),
-    "u26": ("OXM_EM_UNROLL=26",),
     "u26b5": ("OXM_EM_UNROLL=26", "OXM_EM_MIN_BLOCKS=5"),
-    "u26b6": ("OXM_EM_UNROLL=26", "OXM_EM_MIN_BLOCKS=6"),
+    "u2b6": ("OXM_EM_UNROLL=2", "OXM_EM_MIN_BLOCKS=6"),
+    "u4b5": ("OXM_EM_UNROLL=4", "OXM_EM_MIN_BLOCKS=5"),
 }
 
 
