@@ -28,7 +28,7 @@
 
 // band-loop unroll of the EM step (tuned on B200; build knob for experiments)
 #ifndef OXM_EM_UNROLL
-#define OXM_EM_UNROLL 2
+#define OXM_EM_UNROLL 13
 #endif
 #ifndef OXM_EM_MIN_BLOCKS
 #define OXM_EM_MIN_BLOCKS 1
