@@ -154,13 +154,12 @@ __device__ __forceinline__ float lg2_approx(float v) {
   return r;
 }
 
-// fp32 map kernel.  Each thread owns a column PAIR (2c, 2c+1) -- always
-// inside one low-pass block since blocks are 2^n >= 2 wide -- and R rows of
-// one block row: 2R pixels share one spectrum load, one set of block
-// constants and one epilogue, and give 2R independent MUFU/FMA chains per
-// band.  The block spectrum is L (hi, lo) float pairs, contiguous per
-// coefficient (16-byte loads with immediate offsets, shared through L1 by the
-// 2^(n-1) threads of a block column).
+// fp32 map kernel.  CTA = kPxCols columns x R rows of one low-pass block row
+// of one frame; each thread owns one column and R rows and walks the bands
+// once, updating its R pixels per band (R independent MUFU/FMA chains).
+// The block spectrum is L (hi, lo) float pairs, contiguous per coefficient:
+// 16-byte loads with immediate offsets, shared by the 2^n threads of a block
+// column through L1.
 template <int KL, int R>
 __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__ DevOps ops,
                                                          const float* __restrict__ frames, PxGeom g,
@@ -170,18 +169,16 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
                                                          float* __restrict__ hb, float* __restrict__ off,
                                                          uint32_t* __restrict__ fb_count, uint32_t* __restrict__ fb_list) {
   constexpr int LM = BandCount<KL>::kMax;
-  constexpr int P = 2 * R;                    // pixels per thread: p = 2 r + c
   const int L = BandCount<KL>::get(ops);
   const int64_t f = blockIdx.z;
-  const int64_t col0 = 2 * ((int64_t)blockIdx.x * kPxCols + threadIdx.x);
+  const int64_t col = (int64_t)blockIdx.x * kPxCols + threadIdx.x;
   const int bs = 1 << g.n;                    // rows per low-pass block
   const int cpb = bs > R ? bs / R : 1;        // row chunks per block row
   const int64_t by = blockIdx.y / cpb;
   const int64_t row0 = by * bs + (int64_t)(blockIdx.y - by * cpb) * R;
-  if (col0 >= g.W) return;
+  if (col >= g.W) return;
   const int nrow = (int)min64(min64(R, g.H - row0), (int64_t)bs);
-  const bool col1 = col0 + 1 < g.W;
-  const int64_t bidx = (f * g.hL + by) * g.wL + (col0 >> g.n);
+  const int64_t bidx = (f * g.hL + by) * g.wL + (col >> g.n);
 
   float yh[3], yl[3];
 #pragma unroll
@@ -190,39 +187,27 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
     yh[k] = __double2float_rn(v);
     yl[k] = __double2float_rn(v - (double)yh[k]);
   }
-  float d[P][3], acc[P][3], vmin[P];
+  float d[R][3], acc[R][3], vmin[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int64_t p = (f * g.H + row0 + min(r, nrow - 1)) * g.W + col0;
-    float v[6];
-    if (col1 && ((3 * p) & 1) == 0) {
-      const float2* q = reinterpret_cast<const float2*>(frames + 3 * p);
-      const float2 a = ldg(q), b = ldg(q + 1), c = ldg(q + 2);
-      v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y;
-    } else {
+    const int64_t p = (f * g.H + row0 + min(r, nrow - 1)) * g.W + col;
 #pragma unroll
-      for (int k = 0; k < 6; ++k) v[k] = ldg(frames + 3 * p + (col1 ? k : k % 3));
+    for (int k = 0; k < 3; ++k) {
+      d[r][k] = (ldg(frames + 3 * p + k) - yh[k]) - yl[k];
+      acc[r][k] = 0.f;
     }
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        d[2 * r + c][k] = (v[3 * c + k] - yh[k]) - yl[k];
-        acc[2 * r + c][k] = 0.f;
-      }
-      vmin[2 * r + c] = 3.0e38f;
-    }
+    vmin[r] = 3.0e38f;
   }
   const float2* sp = Sp + bidx * L;
   auto band = [&](int l, float sh, float sl) {
 #pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const float s = fmaf(ops.solve_f[l][2], d[q][2], fmaf(ops.solve_f[l][1], d[q][1], fmaf(ops.solve_f[l][0], d[q][0], sl))) + sh;
-      vmin[q] = fminf(vmin[q], s);
+    for (int r = 0; r < R; ++r) {
+      const float s = fmaf(ops.solve_f[l][2], d[r][2], fmaf(ops.solve_f[l][1], d[r][1], fmaf(ops.solve_f[l][0], d[r][0], sl))) + sh;
+      vmin[r] = fminf(vmin[r], s);
       const float lg = lg2_approx(fmaxf(s, ops.eps_f));
-      acc[q][0] = fmaf(ops.fitl2_f[0][l], lg, acc[q][0]);
-      acc[q][1] = fmaf(ops.fitl2_f[1][l], lg, acc[q][1]);
-      acc[q][2] = fmaf(ops.fitl2_f[2][l], lg, acc[q][2]);
+      acc[r][0] = fmaf(ops.fitl2_f[0][l], lg, acc[r][0]);
+      acc[r][1] = fmaf(ops.fitl2_f[1][l], lg, acc[r][1]);
+      acc[r][2] = fmaf(ops.fitl2_f[2][l], lg, acc[r][2]);
     }
   };
   if constexpr (KL > 0 && KL % 2 == 0) {
@@ -246,11 +231,10 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   const float thr = (float)ops.fallback_below;
   bool any_fb = false;
 #pragma unroll
-  for (int q = 0; q < P; ++q) {
-    const int r = q >> 1, c = q & 1;
-    if (r < nrow && (c == 0 || col1)) {
-      const int64_t p = (f * g.H + row0 + r) * g.W + col0 + c;
-      const float xo = acc[q][0] * cal, xd = acc[q][1] * cal;
+  for (int r = 0; r < R; ++r) {
+    const int64_t p = (f * g.H + row0 + r) * g.W + col;
+    if (r < nrow) {
+      const float xo = acc[r][0] * cal, xd = acc[r][1] * cal;
       const float co = fmaxf(xo, 0.f);
       const float t = co + fmaxf(xd, 0.f);
       thb[p] = t;
@@ -258,9 +242,9 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
       if (hbo) {
         hbo[p] = xo;
         hb[p] = xd;
-        off[p] = acc[q][2];
+        off[p] = acc[r][2];
       }
-      any_fb |= vmin[q] < thr;
+      any_fb |= vmin[r] < thr;
     }
   }
   // cancellation guard: queue pixels for the fp64 fixup kernel (rare)
@@ -268,17 +252,15 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   if (__any_sync(active, any_fb)) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int q = 0; q < P; ++q) {
-      const int r = q >> 1, c = q & 1;
-      const bool need = r < nrow && (c == 0 || col1) && vmin[q] < thr;
+    for (int r = 0; r < R; ++r) {
+      const bool need = r < nrow && vmin[r] < thr;
       const unsigned m = __ballot_sync(active, need);
       if (m) {
         const int leader = __ffs(m) - 1;
         uint32_t base = 0;
         if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
         base = __shfl_sync(active, base, leader);
-        if (need)
-          fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col0 + c);
+        if (need) fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col);
       }
     }
   }
@@ -465,7 +447,7 @@ int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64
   const int bs = 1 << g.n;
   const int R = bs >= 8 ? 8 : bs;
   const int64_t cpb = bs > R ? bs / R : 1;
-  dim3 grid((unsigned)ceil_div(g.W, 2 * kPxCols), (unsigned)(g.hL * cpb), (unsigned)batch);
+  dim3 grid((unsigned)ceil_div(g.W, kPxCols), (unsigned)(g.hL * cpb), (unsigned)batch);
   if (g.hL * cpb > 65535 || batch > 65535) return OXM_ERR_ARGUMENT;
   switch (R) {
     case 2: px_f32_kernel<KL, 2><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Sp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
