@@ -63,7 +63,9 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
   d.max_iters = o->max_iters;
   d.eps = o->epsilon;
   d.rel_tol = o->rel_tol;
-  d.fallback_below = o->fallback_below;
+  // the fp32 map path skips the eps clamp, which is only sound when every
+  // band below the fallback threshold is recomputed in fp64
+  d.fallback_below = o->fallback_below > o->epsilon ? o->fallback_below : o->epsilon;
   d.eps_f = static_cast<float>(o->epsilon);
   const double ln2 = 0.69314718055994530942;
   for (int l = 0; l < L; ++l) {

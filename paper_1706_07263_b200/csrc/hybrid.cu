@@ -157,13 +157,17 @@ __device__ __forceinline__ float lg2_approx(float v) {
 // fp32 map kernel.  CTA = kPxCols columns x R rows of one low-pass block row
 // of one frame; each thread owns one column and R rows and walks the bands
 // once, updating its R pixels per band (R independent MUFU/FMA chains).
-// The block spectrum is L (hi, lo) float pairs, contiguous per coefficient:
-// 16-byte loads with immediate offsets, shared by the 2^n threads of a block
-// column through L1.
-template <int KL, int R>
+// Per band and pixel: 3 FFMA (solve d, started from the block spectrum), one
+// 3-input min per band pair (fallback detection), MUFU lg2, 2 FFMA (hbo, hb;
+// +1 for the offset plane when requested).  No eps clamp: any pixel with a
+// band below fallback_below (>= eps) is recomputed in fp64 by the fixup
+// kernel, which applies the reference's clamp.  The block spectrum row
+// Shi[coef][Lp] is read with 16-byte loads (Lp = L rounded up to 4), shared
+// through L1 by the 2^n threads of a block column.
+template <int KL, int R, bool PLANES>
 __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__ DevOps ops,
                                                          const float* __restrict__ frames, PxGeom g,
-                                                         const float2* __restrict__ Sp,
+                                                         const float* __restrict__ Shi, int Lp,
                                                          const double* __restrict__ ybar, float* __restrict__ thb,
                                                          float* __restrict__ so2, float* __restrict__ hbo,
                                                          float* __restrict__ hb, float* __restrict__ off,
@@ -187,44 +191,59 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
     yh[k] = __double2float_rn(v);
     yl[k] = __double2float_rn(v - (double)yh[k]);
   }
-  float d[R][3], acc[R][3], vmin[R];
+  float d[R][3], a0[R], a1[R], a2[R], vmin[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + min(r, nrow - 1)) * g.W + col;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      d[r][k] = (ldg(frames + 3 * p + k) - yh[k]) - yl[k];
-      acc[r][k] = 0.f;
-    }
+    for (int k = 0; k < 3; ++k) d[r][k] = (ldg(frames + 3 * p + k) - yh[k]) - yl[k];
+    a0[r] = a1[r] = a2[r] = 0.f;
     vmin[r] = 3.0e38f;
   }
-  const float2* sp = Sp + bidx * L;
-  auto band = [&](int l, float sh, float sl) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const float s = fmaf(ops.solve_f[l][2], d[r][2], fmaf(ops.solve_f[l][1], d[r][1], fmaf(ops.solve_f[l][0], d[r][0], sl))) + sh;
-      vmin[r] = fminf(vmin[r], s);
-      const float lg = lg2_approx(fmaxf(s, ops.eps_f));
-      acc[r][0] = fmaf(ops.fitl2_f[0][l], lg, acc[r][0]);
-      acc[r][1] = fmaf(ops.fitl2_f[1][l], lg, acc[r][1]);
-      acc[r][2] = fmaf(ops.fitl2_f[2][l], lg, acc[r][2]);
-    }
+  auto spec = [&](int l, float sh, float& s_out, int r) {
+    s_out = fmaf(ops.solve_f[l][2], d[r][2], fmaf(ops.solve_f[l][1], d[r][1], fmaf(ops.solve_f[l][0], d[r][0], sh)));
   };
+  auto fit = [&](int l, float s, int r) {
+    const float lg = lg2_approx(s);
+    a0[r] = fmaf(ops.fitl2_f[0][l], lg, a0[r]);
+    a1[r] = fmaf(ops.fitl2_f[1][l], lg, a1[r]);
+    if constexpr (PLANES) a2[r] = fmaf(ops.fitl2_f[2][l], lg, a2[r]);
+  };
+  const float* sp = Shi + bidx * Lp;
   if constexpr (KL > 0 && KL % 2 == 0) {
-    // two bands per 16-byte load (row start is 16-B aligned: 8*L % 16 == 0)
     const float4* sp4 = reinterpret_cast<const float4*>(sp);
 #pragma unroll
-    for (int q = 0; q < KL / 2; ++q) {
+    for (int q = 0; q < (KL + 3) / 4; ++q) {
       const float4 v = ldg(sp4 + q);
-      band(2 * q, v.x, v.y);
-      band(2 * q + 1, v.z, v.w);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int h = 0; h < 4; h += 2) {
+        const int l = 4 * q + h;
+        if (l < KL) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            float s0, s1;
+            spec(l, vv[h], s0, r);
+            spec(l + 1, vv[h + 1], s1, r);
+            vmin[r] = fminf(vmin[r], fminf(s0, s1));
+            fit(l, s0, r);
+            fit(l + 1, s1, r);
+          }
+        }
+      }
     }
   } else {
 #pragma unroll(KL > 0 ? LM : 1)
     for (int l = 0; l < LM; ++l) {
       if (KL == 0 && l >= L) break;
-      const float2 v = ldg(sp + l);
-      band(l, v.x, v.y);
+      const float sh = ldg(sp + l);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        float s0;
+        spec(l, sh, s0, r);
+        vmin[r] = fminf(vmin[r], s0);
+        fit(l, s0, r);
+      }
     }
   }
   const float cal = (float)g.cal;
@@ -234,17 +253,17 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + r) * g.W + col;
     if (r < nrow) {
-      const float xo = acc[r][0] * cal, xd = acc[r][1] * cal;
+      const float xo = a0[r] * cal, xd = a1[r] * cal;
       const float co = fmaxf(xo, 0.f);
       const float t = co + fmaxf(xd, 0.f);
       thb[p] = t;
       so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
-      if (hbo) {
+      if constexpr (PLANES) {
         hbo[p] = xo;
         hb[p] = xd;
-        off[p] = acc[r][2];
+        off[p] = a2[r];
       }
-      any_fb |= vmin[r] < thr;
+      any_fb |= !(vmin[r] >= thr);  // also catches NaN
     }
   }
   // cancellation guard: queue pixels for the fp64 fixup kernel (rare)
@@ -253,7 +272,7 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool need = r < nrow && vmin[r] < thr;
+      const bool need = r < nrow && !(vmin[r] >= thr);
       const unsigned m = __ballot_sync(active, need);
       if (m) {
         const int leader = __ffs(m) - 1;
@@ -272,7 +291,8 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
 // constant-bank reads; the three fit sums are warp-reduced.
 __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
                                                                  const float* __restrict__ frames, PxGeom g,
-                                                                 const float2* __restrict__ Sp,
+                                                                 const float* __restrict__ Shi,
+                                                                 const float* __restrict__ Slo, int Lp,
                                                                  const double* __restrict__ ybar,
                                                                  const uint32_t* __restrict__ fb_count,
                                                                  const uint32_t* __restrict__ fb_list,
@@ -301,8 +321,7 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
     const double D2 = (double)frames[3 * p + 2] - ybar[2 * g.nll + bidx];
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     for (int l = lane; l < L; l += 32) {
-      const float2 v = Sp[bidx * L + l];
-      const double S = (double)v.x + (double)v.y;
+      const double S = (double)Shi[bidx * Lp + l] + (double)Slo[bidx * Lp + l];
       const double sp = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
       const double lg = log(fmax(sp, ops.eps));
       a0 = fma(F[0][l], lg, a0);
@@ -373,13 +392,16 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
 
 // Workspace (256-B aligned sections):
 //   ybar  3 x nll  double
-//   spectra  L x nll x 8 B   (fp64 SoA S[l][i], or fp32 (hi, lo) pairs Sp[i][l])
+//   spectra  fp64 SoA S[l][i] (fp64 path), or fp32 Shi[i][Lp] then Slo[i][Lp]
+//            (fp32 path; Lp = L rounded up to 4 for 16-byte row loads)
 //   x_prev   3 x nll  double,  fit counts  nll  int32   (EM bookkeeping)
 //   fallback counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
 struct Workspace {
   double* ybar;
   double* S;
-  float2* Sp;
+  float* Shi;
+  float* Slo;
+  int Lp;
   double* xprev;
   int32_t* fits;
   uint32_t* fb_count;
@@ -388,8 +410,11 @@ struct Workspace {
 
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+inline int padded_bands(int L) { return (L + 3) & ~3; }
+
 size_t workspace_bytes(int L, int64_t nll, int64_t npx) {
-  return 256 + align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(double) * (size_t)L * (size_t)nll) +
+  return 256 + align256(sizeof(double) * 3 * (size_t)nll) +
+         align256(sizeof(double) * (size_t)padded_bands(L) * (size_t)nll) +
          align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) + 256 +
          align256(sizeof(uint32_t) * (size_t)npx);
 }
@@ -400,8 +425,10 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.ybar = reinterpret_cast<double*>(p);
   p += align256(sizeof(double) * 3 * (size_t)nll);
   w.S = reinterpret_cast<double*>(p);
-  w.Sp = reinterpret_cast<float2*>(p);
-  p += align256(sizeof(double) * (size_t)L * (size_t)nll);
+  w.Lp = padded_bands(L);
+  w.Shi = reinterpret_cast<float*>(p);
+  w.Slo = w.Shi + (size_t)w.Lp * (size_t)nll;
+  p += align256(sizeof(double) * (size_t)w.Lp * (size_t)nll);
   w.xprev = reinterpret_cast<double*>(p);
   p += align256(sizeof(double) * 3 * (size_t)nll);
   w.fits = reinterpret_cast<int32_t*>(p);
@@ -433,31 +460,46 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   io.y_soa = 1;
   io.n = nll;
   io.S = w.S;
-  io.Sp = w.Sp;
+  io.Shi = w.Shi;
+  io.Slo = w.Slo;
+  io.Lp = w.Lp;
   io.xprev = w.xprev;
   io.fits = fits ? fits : w.fits;
-  constexpr SpecOut out = F32OUT ? SpecOut::kAosF32Pair : SpecOut::kSoaF64;
+  constexpr SpecOut out = F32OUT ? SpecOut::kAosF32HiLo : SpecOut::kSoaF64;
   if (ops.L == 26) return launch_em<26, out>(ops, io, s);
   return launch_em<0, out>(ops, io, s);
+}
+
+template <int KL, bool PLANES>
+void launch_px_rows(const DevOps& ops, const float* frames, const PxGeom& g, dim3 grid, int R, const Workspace& w,
+                    float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
+  switch (R) {
+    case 2: px_f32_kernel<KL, 2, PLANES><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    case 4: px_f32_kernel<KL, 4, PLANES><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    default: px_f32_kernel<KL, 8, PLANES><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+  }
 }
 
 template <int KL>
 int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64_t batch, const Workspace& w,
                   float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
+  if (!thb || !so2) return OXM_ERR_ARGUMENT;
+  // the planes are written all three or none
+  const bool planes = hbo || hb || off;
+  if (planes && !(hbo && hb && off)) return OXM_ERR_ARGUMENT;
   const int bs = 1 << g.n;
   const int R = bs >= 8 ? 8 : bs;
   const int64_t cpb = bs > R ? bs / R : 1;
   dim3 grid((unsigned)ceil_div(g.W, kPxCols), (unsigned)(g.hL * cpb), (unsigned)batch);
   if (g.hL * cpb > 65535 || batch > 65535) return OXM_ERR_ARGUMENT;
-  switch (R) {
-    case 2: px_f32_kernel<KL, 2><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Sp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    case 4: px_f32_kernel<KL, 4><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Sp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    default: px_f32_kernel<KL, 8><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Sp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-  }
+  if (planes)
+    launch_px_rows<KL, true>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
+  else
+    launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
-  px_fallback_kernel<<<148 * 4, kFbThreads, 0, s>>>(ops, frames, g, w.Sp, w.ybar, w.fb_count, w.fb_list,
-                                                     thb, so2, hbo, hb, off);
+  px_fallback_kernel<<<148 * 4, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
+                                                     w.fb_list, thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
 }
 

@@ -71,7 +71,7 @@ __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
 // the final step started from -- and em_spectra_kernel rebuilds
 // s = max(exp(-xi x_prev) + G (y - C exp(-xi x_prev)), eps) with the same
 // exp_tab, bit-identically, with coalesced stores.
-enum class SpecOut { kSoaF64, kAosF32Pair, kAosF64 };
+enum class SpecOut { kSoaF64, kAosF32HiLo, kAosF64 };
 
 struct EmIO {
   const double* y;     // unit-scale low-pass data: SoA [3][n] (y_soa) or AoS (n, 3)
@@ -79,7 +79,9 @@ struct EmIO {
   const double* init;  // AoS (n, L) start spectra, or null (Tikhonov start)
   int64_t n;
   double* S;           // kSoaF64: [L][n];  kAosF64: (n, L)
-  float2* Sp;          // kAosF32Pair: (n, L) of (hi, lo), hi + lo = s to 48 bits
+  float* Shi;          // kAosF32HiLo: (n, Lp) hi parts, then (n, Lp) lo parts:
+  float* Slo;          //   hi + lo = s to 48 bits (Lp = L rounded up to 4)
+  int Lp;
   double* x;           // (n, 3) final concentrations, or null
   double* xprev;       // [3][n] concentration the final fit step started from (required)
   int32_t* fits;       // (n) fit counts (required)
@@ -252,7 +254,8 @@ __global__ void __launch_bounds__(kEmThreads) em_spectra_kernel(const __grid_con
       io.S[i * L + l] = s;
     } else {
       const float h = __double2float_rn(s);
-      io.Sp[i * L + l] = make_float2(h, __double2float_rn(s - (double)h));
+      io.Shi[i * io.Lp + l] = h;
+      io.Slo[i * io.Lp + l] = __double2float_rn(s - (double)h);
     }
   }
 }
