@@ -206,56 +206,76 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 }
 
 // Final spectra from (y, x_prev, fits): one thread per coefficient, the
-// same arithmetic as the last EM step, coalesced stores.
+// same arithmetic as the last EM step.  Row-major outputs are staged through
+// shared memory (s overwrites the thread's e column) and written back by
+// the whole CTA as one contiguous block, so every store is coalesced.
 template <int KL, SpecOut OUT>
 __global__ void __launch_bounds__(kEmThreads) em_spectra_kernel(const __grid_constant__ DevOps ops, EmIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
-  double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
+  double* e_all = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem));
+  double* e = e_all + threadIdx.x;
   constexpr int es = kEmThreads;
   load_math_tables(mt);
   __syncthreads();
-  const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
-  if (i >= io.n) return;
+  const int64_t base = (int64_t)blockIdx.x * kEmThreads;
+  const int64_t i = base + threadIdx.x;
   const int L = BandCount<KL>::get(ops);
-  double y0, y1, y2;
-  if (io.y_soa) {
-    y0 = io.y[i];
-    y1 = io.y[io.n + i];
-    y2 = io.y[2 * io.n + i];
-  } else {
-    y0 = io.y[3 * i];
-    y1 = io.y[3 * i + 1];
-    y2 = io.y[3 * i + 2];
-  }
-  const bool start_only = io.fits[i] <= 1;
-  const double x0 = io.xprev[i], x1 = io.xprev[io.n + i], x2 = io.xprev[2 * io.n + i];
-  double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-#pragma unroll 2
-  for (int l = 0; l < L; ++l) {
-    double el;
-    if (start_only)
-      el = io.init ? io.init[i * L + l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-    else
-      el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
-    e[l * es] = el;
-    c0 = fma(ops.sens[0][l], el, c0);
-    c1 = fma(ops.sens[1][l], el, c1);
-    c2 = fma(ops.sens[2][l], el, c2);
-  }
-  const double r0 = start_only ? 0.0 : y0 - c0;
-  const double r1 = start_only ? 0.0 : y1 - c1;
-  const double r2 = start_only ? 0.0 : y2 - c2;
-  for (int l = 0; l < L; ++l) {
-    const double s = fmax(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), ops.eps);
-    if constexpr (OUT == SpecOut::kSoaF64) {
-      io.S[(int64_t)l * io.n + i] = s;
-    } else if constexpr (OUT == SpecOut::kAosF64) {
-      io.S[i * L + l] = s;
+  if (i < io.n) {
+    double y0, y1, y2;
+    if (io.y_soa) {
+      y0 = io.y[i];
+      y1 = io.y[io.n + i];
+      y2 = io.y[2 * io.n + i];
     } else {
-      const float h = __double2float_rn(s);
-      io.Shi[i * io.Lp + l] = h;
-      io.Slo[i * io.Lp + l] = __double2float_rn(s - (double)h);
+      y0 = io.y[3 * i];
+      y1 = io.y[3 * i + 1];
+      y2 = io.y[3 * i + 2];
+    }
+    const bool start_only = io.fits[i] <= 1;
+    const double x0 = io.xprev[i], x1 = io.xprev[io.n + i], x2 = io.xprev[2 * io.n + i];
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+#pragma unroll 2
+    for (int l = 0; l < L; ++l) {
+      double el;
+      if (start_only)
+        el = io.init ? io.init[i * L + l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
+      else
+        el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+      e[l * es] = el;
+      c0 = fma(ops.sens[0][l], el, c0);
+      c1 = fma(ops.sens[1][l], el, c1);
+      c2 = fma(ops.sens[2][l], el, c2);
+    }
+    const double r0 = start_only ? 0.0 : y0 - c0;
+    const double r1 = start_only ? 0.0 : y1 - c1;
+    const double r2 = start_only ? 0.0 : y2 - c2;
+    for (int l = 0; l < L; ++l) {
+      const double s =
+          fmax(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), ops.eps);
+      if constexpr (OUT == SpecOut::kSoaF64)
+        io.S[(int64_t)l * io.n + i] = s;  // SoA: already coalesced
+      else
+        e[l * es] = s;
+    }
+  }
+  if constexpr (OUT != SpecOut::kSoaF64) {
+    __syncthreads();
+    const int64_t rows = min64(kEmThreads, io.n - base);
+    if constexpr (OUT == SpecOut::kAosF64) {
+      for (int64_t q = threadIdx.x; q < rows * L; q += kEmThreads) {
+        const int64_t r = q / L, l = q - r * L;
+        io.S[base * L + q] = e_all[l * es + r];
+      }
+    } else {
+      const int Lp = io.Lp;
+      for (int64_t q = threadIdx.x; q < rows * Lp; q += kEmThreads) {
+        const int64_t r = q / Lp, l = q - r * Lp;
+        const double s = l < L ? e_all[l * es + r] : 0.0;
+        const float h = __double2float_rn(s);
+        io.Shi[base * Lp + q] = h;
+        io.Slo[base * Lp + q] = __double2float_rn(s - (double)h);
+      }
     }
   }
 }
