@@ -334,40 +334,38 @@ def run_ours(args):
         return
 
     peaks = probe_peaks(lib, torch, dev)
-    hbm = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("hbm_gbs") if (ROOT / "MEASURED_PEAKS.json").exists() else None
+    mp = ROOT / "MEASURED_PEAKS.json"
+    hbm = json.loads(mp.read_text()).get("hbm_gbs") if mp.exists() else None
     # per-stage algorithmic work
     px = B * H * W
     bytes_ll = px * 12 + nll * 3 * 8
-    bytes_px = px * 12 + px * 8 + nll * (26 + 3) * 8
-    flops_per_fit = 2 * DFMA_PER_FIT
-    em_flops = fits_total * flops_per_fit
-    stages = {
-        "ll_kernel": {"ms": stage_s[0] * 1e3, "GB/s": bytes_ll / stage_s[0] / 1e9},
-        "em_soa_kernel": {"ms": stage_s[1] * 1e3, "fits_per_coeff": fits_total / nll,
-                          "fp64_TFLOP/s": em_flops / stage_s[1] / 1e12},
-        "px_f32_kernel": {"ms": stage_s[2] * 1e3, "GB/s": bytes_px / stage_s[2] / 1e9,
-                          "lg2_T/s": px * 26 / stage_s[2] / 1e12},
+    em_flops = fits_total * FLOPS_PER_FIT + nll * FLOPS_SPECTRA
+    px_lg2 = px * 26
+    stage_t = {"ll_kernel": stage_s[0], "em": stage_s[1], "px_f32_kernel": stage_s[2]}
+    rooflines = {
+        "ll_kernel": {"bound": "hbm", "achieved": bytes_ll / stage_s[0] / 1e9, "peak": hbm, "unit": "GB/s",
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "em": {"bound": "fp64", "achieved": em_flops / stage_s[1] / 1e12, "peak": 2 * peaks["fp64_fma"] / 1e12,
+               "unit": "TFLOP/s", "peak_source": "fp64 FMA probe (oxm_probe_fp64_fma) in this run",
+               "kernels": "em_persistent_kernel + em_spectra_kernel",
+               "work": f"{fits_total} fits x {FLOPS_PER_FIT} + {nll} coefficients x {FLOPS_SPECTRA} fp64 flops"},
+        "px_f32_kernel": {"bound": "xu", "achieved": px_lg2 / stage_s[2] / 1e12, "peak": peaks["mufu_lg2"] / 1e12,
+                          "unit": "Tlg2/s", "peak_source": "MUFU lg2 probe (oxm_probe_mufu_lg2) in this run",
+                          "kernels": "px_f32_kernel + px_fallback_kernel", "work": f"{px} px x 26 lg2"},
     }
-    dominant = max(range(3), key=lambda i: stage_s[i])
-    traffic = None
+    for k, r in rooflines.items():
+        r["ms"] = stage_t[k] * 1e3
+        r["frac"] = r["achieved"] / r["peak"] if r["peak"] else None
+    traffic = {}
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(["ll_kernel", "em_soa_kernel", "px_f32_kernel"][dominant])
-    if dominant == 1:
-        peak = 2 * peaks["fp64_fma"] / 1e12
-        ach = em_flops / stage_s[1] / 1e12
-        roof = {"bound": "fp64", "kernel": "em_soa_kernel", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": traffic,
-                "peak_source": "measured in this run by oxm_probe_fp64_fma (MEASURED_PEAKS.json has no fp64 figure)",
-                "work": f"{DFMA_PER_FIT} fp64 FMA-equivalents per EM fit x {fits_total} fits"}
-    elif dominant == 2:
-        ach = bytes_px / stage_s[2] / 1e9
-        roof = {"bound": "hbm", "kernel": "px_f32_kernel", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm if hbm else None, "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    else:
-        ach = bytes_ll / stage_s[0] / 1e9
-        roof = {"bound": "hbm", "kernel": "ll_kernel", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm if hbm else None, "traffic": traffic, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        per_frame = json.loads(tf.read_text()).get("dram_bytes_per_frame", {})
+        traffic = {k: v * B for k, v in per_frame.items()}
+    dominant = max(stage_t, key=stage_t.get)
+    roof = dict(rooflines[dominant])
+    roof["kernel"] = dominant
+    roof["traffic"] = traffic.get(dominant)
+    roof["traffic_note"] = "ncu dram__bytes_read+write per launch (profiles/traffic.json, scaled to this batch)"
 
     cpu = None
     if world == 1 and not args.no_cpu:
@@ -385,7 +383,8 @@ def run_ours(args):
                    "l2": f"inputs {B * H * W * 12 / 1e6:.0f} MB per step > 126 MB L2 (no flush needed)",
                    "parallelism": f"frame-sharded x{world}, no data-path collective"},
         "roofline": roof,
-        "stages": stages,
+        "stage_rooflines": rooflines,
+        "fits_per_coefficient": fits_total / nll,
         "probes": {"fp64_fma_T/s": peaks["fp64_fma"] / 1e12, "mufu_lg2_T/s": peaks["mufu_lg2"] / 1e12},
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -397,10 +396,13 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-# fp64 FMA-equivalent operations per EM fit, counted from the em_soa_kernel
-# SASS loop body (tools/count_em_sass.py)
-DFMA_PER_FIT = 780
-HybridMapLaunches = 3
+# fp64 flops per EM fit of this implementation's formulation:
+# per band 62 (exp arg 4, table exp 20, C e 6, e + G r 6, table log 20, fit 6)
+# x 26 bands + 16 per step; the spectra kernel adds 36 per band per coefficient.
+FLOPS_PER_FIT = 62 * 26 + 16
+FLOPS_SPECTRA = 36 * 26
+# kernels launched per step: zero_u32, ll, em_persistent, em_spectra, px, fallback
+HybridMapLaunches = 6
 
 
 def main():

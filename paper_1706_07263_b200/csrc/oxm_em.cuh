@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kEmThreads) em_spectra_kernel(const __grid_con
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
   double* e_all = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem));
   double* e = e_all + threadIdx.x;
-  constexpr int es = kEmThreads;
+  constexpr int es = kEmThreads + 1;  // odd stride: conflict-free transpose reads below
   load_math_tables(mt);
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kEmThreads;
@@ -290,8 +290,9 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   auto kspec = em_spectra_kernel<KL, OUT>;
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(kspec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
+  const size_t smem_spec = em_smem_bytes(ops.L, kEmThreads + 1);
+  if (smem_spec > 48 * 1024) cudaFuncSetAttribute(kspec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_spec);
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -306,7 +307,7 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
   int st = check_launch("em_persistent");
   if (st) return st;
-  kspec<<<(unsigned)need, kEmThreads, smem, s>>>(ops, io);
+  kspec<<<(unsigned)need, kEmThreads, smem_spec, s>>>(ops, io);
   return check_launch("em_spectra");
 }
 
