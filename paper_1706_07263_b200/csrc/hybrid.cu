@@ -498,7 +498,7 @@ int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64
     launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
-  px_fallback_kernel<<<148 * 4, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
+  px_fallback_kernel<<<148 * 32, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
                                                      w.fb_list, thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
 }
