@@ -24,7 +24,10 @@ from . import _native
 from .errors import ArgumentError, IllConditionedPriorError
 
 COND_LIMIT = 1e13  # bayes.py:33
-DEFAULT_FALLBACK_BELOW = 1e-2  # fp32 map path: fp64 recompute below this band value
+# fp32 map path: pixels whose smallest reconstructed band is below this are
+# recomputed in fp64 (profiles/r01_fallback_threshold_study.txt: fp32 error
+# <= 2e-6 THb rel / 1.2e-6 SO2 abs for bands >= 1e-3, fails below 1e-4)
+DEFAULT_FALLBACK_BELOW = 2e-3
 
 
 def second_difference(count: int) -> np.ndarray:
