@@ -266,6 +266,7 @@ def run_ours(args):
 
     import paper_1706_07263_b200 as ox
     from paper_1706_07263_b200 import _native
+    from paper_1706_07263_b200.parallel import max_over_ranks
 
     lib = _native.load()
     sens, basis = operators()
@@ -296,10 +297,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     elapsed = start.elapsed_time(stop) * 1e-3
-    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_max = float(t.item())
+    elapsed_max = max_over_ranks(elapsed, dev)
     stage_s = [statistics.mean(e[i].elapsed_time(e[i + 1]) * 1e-3 for e in ev) for i in range(3)]
     fits_total = int(out.fits.sum().item())
     eng.check_flags(out)
@@ -320,11 +318,8 @@ def run_ours(args):
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             eng.maps_from_host(host_in, thb_h, so2_h, chunk=chunk, _state=state)
-        e2e_dt = time.perf_counter() - t0
-        te = torch.tensor([e2e_dt], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * B * e2e_steps / float(te.item()), "unit": UNIT,
+        e2e_dt = max_over_ranks(time.perf_counter() - t0, dev)
+        e2e = {"value": world * B * e2e_steps / e2e_dt, "unit": UNIT,
                "h2d_bytes_per_step": B * H * W * 3 * 4, "d2h_bytes_per_step": B * H * W * 2 * 4,
                "steps": e2e_steps, "chunk_frames": chunk, "api": "HybridMapEngine.maps_from_host -> oxm_hybrid_maps_f32"}
 

@@ -1,0 +1,64 @@
+"""Multi-GPU plumbing for video batches.
+
+Frames are independent (no temporal coupling), so a video is
+split into contiguous per-rank blocks and every rank runs the hybrid path on
+its own frames with no data-path collective.  The only collectives are the
+timing reduction (max over ranks, as the benchmark contract requires) and an
+optional gather of finished maps to one rank.  One process per GPU,
+torch.distributed (NCCL on GPUs, gloo for the CPU tests).
+"""
+
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def world() -> tuple[int, int, int]:
+    """(world_size, rank, local_rank) from the torchrun environment."""
+    return (int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def shard_range(n_frames: int, rank: int, world_size: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of frames owned by ``rank``; blocks differ in
+    size by at most one frame and cover 0..n_frames exactly once."""
+    if world_size < 1 or not 0 <= rank < world_size or n_frames < 0:
+        raise ValueError(f"bad shard request n={n_frames} rank={rank} world={world_size}")
+    base, extra = divmod(n_frames, world_size)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def max_over_ranks(value: float, device: torch.device | None = None) -> float:
+    """Max of a per-rank scalar (step time) over all ranks; identity when
+    torch.distributed is not initialised."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_to_root(local: torch.Tensor, n_frames: int, root: int = 0) -> torch.Tensor | None:
+    """Gather per-rank map blocks (frames, H, W) into the full (n_frames, H, W)
+    tensor on ``root`` (None elsewhere).  Ranks send their contiguous block
+    with point-to-point sends, so uneven blocks need no padding."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return local
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    if rank != root:
+        dist.send(local.contiguous(), dst=root)
+        return None
+    out = torch.empty((n_frames,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    for r in range(ws):
+        lo, hi = shard_range(n_frames, r, ws)
+        if r == root:
+            out[lo:hi] = local
+        elif hi > lo:
+            buf = torch.empty((hi - lo,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+            dist.recv(buf, src=r)
+            out[lo:hi] = buf
+    return out
