@@ -394,7 +394,7 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
 //   ybar  3 x nll  double
 //   spectra  fp64 SoA S[l][i] (fp64 path), or fp32 Shi[i][Lp] then Slo[i][Lp]
 //            (fp32 path; Lp = L rounded up to 4 for 16-byte row loads)
-//   x_prev   3 x nll  double,  fit counts  nll  int32   (EM bookkeeping)
+//   x_prev, x_init   3 x nll double each,  fit counts  nll int32   (EM bookkeeping)
 //   fallback counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
 struct Workspace {
   double* ybar;
@@ -403,6 +403,7 @@ struct Workspace {
   float* Slo;
   int Lp;
   double* xprev;
+  double* xinit;
   int32_t* fits;
   uint32_t* fb_count;
   uint32_t* fb_list;
@@ -415,7 +416,7 @@ inline int padded_bands(int L) { return (L + 3) & ~3; }
 size_t workspace_bytes(int L, int64_t nll, int64_t npx) {
   return 256 + align256(sizeof(double) * 3 * (size_t)nll) +
          align256(sizeof(double) * (size_t)padded_bands(L) * (size_t)nll) +
-         align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) + 256 +
+         2 * align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) + 256 +
          align256(sizeof(uint32_t) * (size_t)npx);
 }
 
@@ -430,6 +431,8 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.Slo = w.Shi + (size_t)w.Lp * (size_t)nll;
   p += align256(sizeof(double) * (size_t)w.Lp * (size_t)nll);
   w.xprev = reinterpret_cast<double*>(p);
+  p += align256(sizeof(double) * 3 * (size_t)nll);
+  w.xinit = reinterpret_cast<double*>(p);
   p += align256(sizeof(double) * 3 * (size_t)nll);
   w.fits = reinterpret_cast<int32_t*>(p);
   p += align256(sizeof(int32_t) * (size_t)nll);
@@ -464,6 +467,7 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   io.Slo = w.Slo;
   io.Lp = w.Lp;
   io.xprev = w.xprev;
+  io.xinit = w.xinit;
   io.fits = fits ? fits : w.fits;
   constexpr SpecOut out = F32OUT ? SpecOut::kAosF32HiLo : SpecOut::kSoaF64;
   if (ops.L == 26) return launch_em<26, out>(ops, io, s);

@@ -59,12 +59,11 @@ __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
 // coefficients and advances all its lanes one *fit* per step; a lane whose
 // coefficient has converged records it and immediately takes the next one.
 //
-// Every step is warp-uniform: the Tikhonov start is folded in as
-// e := solve y (or init), r := 0, so s = max(e + G r, eps) = max(solve y, eps)
-// exactly; lanes in their start step still evaluate (and discard) the exp.
-// Uniform control flow keeps the band counter in a uniform register, so the
-// operator entries are uniform-datapath constants (ULDC / UR operands) rather
-// than per-thread indexed LDCs feeding every DFMA.
+// Fit #1 (the Tikhonov start) runs beforehand in em_init_kernel, so every
+// persistent step is the same exp/prior/log/fit step and control flow is
+// warp-uniform: the band counter stays in a uniform register and operator
+// entries are uniform-datapath constants (ULDC / UR operands) rather than
+// per-thread indexed LDCs feeding every DFMA.
 //
 // The final spectrum is not written here (that would be a 26-store divergent
 // branch in almost every step): the kernel stores x_prev -- the concentration
@@ -84,6 +83,7 @@ struct EmIO {
   int Lp;
   double* x;           // (n, 3) final concentrations, or null
   double* xprev;       // [3][n] concentration the final fit step started from (required)
+  double* xinit;       // [3][n] fit #1 of the start spectrum (em_init_kernel output, required)
   int32_t* fits;       // (n) fit counts (required)
   int64_t per_warp;    // slice length
 };
@@ -91,8 +91,45 @@ struct EmIO {
 constexpr int kEmThreads = 128;
 constexpr int kEmUnroll = OXM_EM_UNROLL;
 
-template <int KL, bool HAS_INIT>
-__global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+// Fit #1 (bayes.py:241-250, 193): x_init = -F log(max(start, eps)) with the
+// Tikhonov start solve y or the caller's init spectra; one thread per
+// coefficient, fully parallel (no divergence), before the persistent loop.
+template <int KL>
+__global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+  __shared__ MathSmem mt;
+  load_math_tables(mt);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
+  if (i >= io.n) return;
+  const int L = BandCount<KL>::get(ops);
+  double y0, y1, y2;
+  if (io.y_soa) {
+    y0 = io.y[i];
+    y1 = io.y[io.n + i];
+    y2 = io.y[2 * io.n + i];
+  } else {
+    y0 = io.y[3 * i];
+    y1 = io.y[3 * i + 1];
+    y2 = io.y[3 * i + 2];
+  }
+  const double* ini = io.init ? io.init + i * L : nullptr;
+  double n0 = 0.0, n1 = 0.0, n2 = 0.0;
+#pragma unroll(KL > 0 ? KL : 2)
+  for (int l = 0; l < L; ++l) {
+    const double st = ini ? ini[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
+    const double lg = log_tab(clamp_eps(st, ops.eps), mt);
+    n0 = fma(ops.fitm[0][l], lg, n0);
+    n1 = fma(ops.fitm[1][l], lg, n1);
+    n2 = fma(ops.fitm[2][l], lg, n2);
+  }
+  io.xinit[i] = -n0;
+  io.xinit[io.n + i] = -n1;
+  io.xinit[2 * io.n + i] = -n2;
+}
+
+template <int KL>
+__global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_kernel(const __grid_constant__ DevOps ops,
+                                                                                        EmIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
   double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
@@ -109,12 +146,21 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   int64_t next = warp * io.per_warp;  // next unassigned coefficient of the slice
   const int64_t stop = min64(next + io.per_warp, io.n);
 
+  if (ops.max_iters <= 1) {  // fit #1 is the answer (bayes.py:195 runs no iteration)
+    for (int64_t i = next + lane; i < stop; i += 32) {
+      for (int k = 0; k < 3; ++k) io.xprev[k * io.n + i] = io.xinit[k * io.n + i];
+      if (io.x)
+        for (int k = 0; k < 3; ++k) io.x[3 * i + k] = io.xinit[k * io.n + i];
+      io.fits[i] = 1;
+    }
+    return;
+  }
+
   int64_t idx = next + lane < stop ? next + lane : -1;
   next = min64(next + 32, stop);
-  bool init = true;
-  int nfit = 0;
+  int nfit = 1;
   double y0 = 0.0, y1 = 0.0, y2 = 0.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
-  auto load_y = [&](int64_t i) {
+  auto load = [&](int64_t i) {
     if (io.y_soa) {
       y0 = io.y[i];
       y1 = io.y[io.n + i];
@@ -124,31 +170,25 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
       y1 = io.y[3 * i + 1];
       y2 = io.y[3 * i + 2];
     }
+    x0 = io.xinit[i];
+    x1 = io.xinit[io.n + i];
+    x2 = io.xinit[2 * io.n + i];
   };
-  if (idx >= 0) load_y(idx);
+  if (idx >= 0) load(idx);
 
   while (__any_sync(0xffffffffu, idx >= 0)) {
-    // ---- phase A: expected spectrum e (or the start spectrum) and residual r
+    // ---- phase A: expected spectrum e = exp(-xi x) and residual r = y - C e
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    const double* ini = HAS_INIT && idx >= 0 ? io.init + idx * L : nullptr;
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
       // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
-      const double ex = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
-      double st;
-      if constexpr (HAS_INIT)
-        st = ini ? ini[l] : 0.0;
-      else
-        st = fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-      const double el = init ? st : ex;
+      const double el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
       e[l * es] = el;
       c0 = fma(ops.sens[0][l], el, c0);
       c1 = fma(ops.sens[1][l], el, c1);
       c2 = fma(ops.sens[2][l], el, c2);
     }
-    const double r0 = init ? 0.0 : y0 - c0;
-    const double r1 = init ? 0.0 : y1 - c1;
-    const double r2 = init ? 0.0 : y2 - c2;
+    const double r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
@@ -165,16 +205,11 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     // ---- bookkeeping: stopping rule of bayes.py:195-205
     bool done = false;
     if (idx >= 0) {
-      if (init) {
-        nfit = 1;
-        done = ops.max_iters <= 1;
-      } else {
-        ++nfit;
-        const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
-        const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
-        const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
-        done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters;
-      }
+      ++nfit;
+      const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
+      const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+      const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
+      done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters;
       if (done) {
         io.xprev[idx] = x0;
         io.xprev[io.n + idx] = x1;
@@ -190,15 +225,14 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     x0 = n0;
     x1 = n1;
     x2 = n2;
-    init = false;
     // ---- refill finished lanes from the warp's slice (no atomics)
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if (m) {
       if (done) {
         const int64_t mine = next + __popc(m & lt_mask);
         idx = mine < stop ? mine : -1;
-        init = true;
-        if (idx >= 0) load_y(idx);
+        nfit = 1;
+        if (idx >= 0) load(idx);
       }
       next = min64(next + __popc(m), stop);
     }
@@ -284,9 +318,9 @@ __global__ void __launch_bounds__(kEmThreads) em_spectra_kernel(const __grid_con
 template <int KL, SpecOut OUT>
 inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (io.n <= 0) return OXM_OK;
-  if (!io.xprev || !io.fits) return OXM_ERR_ARGUMENT;
+  if (!io.xprev || !io.fits || !io.xinit) return OXM_ERR_ARGUMENT;
   const size_t smem = em_smem_bytes(ops.L, kEmThreads);
-  auto kern = io.init ? em_persistent_kernel<KL, true> : em_persistent_kernel<KL, false>;
+  auto kern = em_persistent_kernel<KL>;
   auto kspec = em_spectra_kernel<KL, OUT>;
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -304,6 +338,9 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (blocks > need) blocks = need;
   const int64_t warps = blocks * (kEmThreads / 32);
   io.per_warp = ceil_div(io.n, warps);
+  em_init_kernel<KL><<<(unsigned)need, kEmThreads, 0, s>>>(ops, io);
+  int st0 = check_launch("em_init");
+  if (st0) return st0;
   kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
   int st = check_launch("em_persistent");
   if (st) return st;
