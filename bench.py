@@ -55,6 +55,12 @@ def parse():
     return p.parse_args()
 
 
+def workload_config(args) -> dict:
+    """The `config` object, identical for both arms (the driver pairs lines on it)."""
+    return {"workload": WORKLOAD, "height": args.height, "width": args.width, "levels": args.levels,
+            "texture_density": args.texture}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -217,8 +223,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "height": args.height, "width": args.width, "levels": args.levels,
-                   "frames_per_step": 1, "texture_density": args.texture},
+        "config": workload_config(args),
+        "run": {"frames_per_step": 1, "arm": "oracle port of the reference on host cores"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"1 frame per step ({args.height}x{args.width}, n={args.levels}) through the "
                                    "oracle port of the reference (bit-identical outputs), threads=all cores, BLAS 1"},
@@ -334,7 +340,7 @@ def run_ours(args):
     # per-stage algorithmic work
     px = B * H * W
     bytes_ll = px * 12 + nll * 3 * 8
-    em_flops = fits_total * FLOPS_PER_FIT + nll * FLOPS_SPECTRA
+    em_flops = (fits_total - nll) * FLOPS_PER_FIT + nll * (FLOPS_INIT + FLOPS_SPECTRA)
     px_lg2 = px * 26
     stage_t = {"ll_kernel": stage_s[0], "em": stage_s[1], "px_f32_kernel": stage_s[2]}
     rooflines = {
@@ -343,7 +349,8 @@ def run_ours(args):
         "em": {"bound": "fp64", "achieved": em_flops / stage_s[1] / 1e12, "peak": 2 * peaks["fp64_fma"] / 1e12,
                "unit": "TFLOP/s", "peak_source": "fp64 FMA probe (oxm_probe_fp64_fma) in this run",
                "kernels": "em_persistent_kernel + em_spectra_kernel",
-               "work": f"{fits_total} fits x {FLOPS_PER_FIT} + {nll} coefficients x {FLOPS_SPECTRA} fp64 flops"},
+               "work": f"({fits_total} fits - {nll} start fits) x {FLOPS_PER_FIT} + {nll} coefficients x "
+                       f"({FLOPS_INIT} start fit + {FLOPS_SPECTRA} final spectrum) fp64 flops"},
         "px_f32_kernel": {"bound": "xu", "achieved": px_lg2 / stage_s[2] / 1e12, "peak": peaks["mufu_lg2"] / 1e12,
                           "unit": "Tlg2/s", "peak_source": "MUFU lg2 probe (oxm_probe_mufu_lg2) in this run",
                           "kernels": "px_f32_kernel + px_fallback_kernel", "work": f"{px} px x 26 lg2"},
@@ -373,10 +380,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed_max / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64 EM + f32 per-pixel (f64 fallback)",
         "data": "synthetic (tissue phantoms, seeded; forward model + noise on GPU)",
-        "config": {"workload": WORKLOAD, "height": H, "width": W, "levels": n, "frames_per_step_per_gpu": B,
-                   "global_batch": world * B, "texture_density": args.texture,
-                   "l2": f"inputs {B * H * W * 12 / 1e6:.0f} MB per step > 126 MB L2 (no flush needed)",
-                   "parallelism": f"frame-sharded x{world}, no data-path collective"},
+        "config": workload_config(args),
+        "run": {"frames_per_step_per_gpu": B, "global_batch": world * B,
+                "l2": f"inputs {B * H * W * 12 / 1e6:.0f} MB per step > 126 MB L2 (no flush needed)",
+                "parallelism": f"frame-sharded x{world}, no data-path collective"},
         "roofline": roof,
         "stage_rooflines": rooflines,
         "fits_per_coefficient": fits_total / nll,
@@ -395,9 +402,10 @@ def run_ours(args):
 # per band 62 (exp arg 4, table exp 20, C e 6, e + G r 6, table log 20, fit 6)
 # x 26 bands + 16 per step; the spectra kernel adds 36 per band per coefficient.
 FLOPS_PER_FIT = 62 * 26 + 16
+FLOPS_INIT = 32 * 26   # fit #1: solve y 6, table log 20, fit 6 per band (em_init_kernel)
 FLOPS_SPECTRA = 36 * 26
-# kernels launched per step: zero_u32, ll, em_persistent, em_spectra, px, fallback
-HybridMapLaunches = 6
+# kernels launched per step: zero_u32, ll, em_init, em_persistent, em_spectra, px, fallback
+HybridMapLaunches = 7
 
 
 def main():
