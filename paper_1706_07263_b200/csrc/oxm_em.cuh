@@ -30,6 +30,9 @@
 #ifndef OXM_EM_UNROLL
 #define OXM_EM_UNROLL 13
 #endif
+#ifndef OXM_EM_UNROLL_B
+#define OXM_EM_UNROLL_B OXM_EM_UNROLL
+#endif
 #ifndef OXM_EM_MIN_BLOCKS
 #define OXM_EM_MIN_BLOCKS 1
 #endif
@@ -90,6 +93,7 @@ struct EmIO {
 
 constexpr int kEmThreads = 128;
 constexpr int kEmUnroll = OXM_EM_UNROLL;
+constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 
 // Fit #1 (bayes.py:241-250, 193): x_init = -F log(max(start, eps)) with the
 // Tikhonov start solve y or the caller's init spectra; one thread per
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     const double r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
-#pragma unroll(KL > 0 ? kEmUnroll : 2)
+#pragma unroll(KL > 0 ? kEmUnrollB : 2)
     for (int l = 0; l < L; ++l) {
       const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
       const double lg = log_tab(clamp_eps(s, eps), mt);
