@@ -49,9 +49,9 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   DeviceGuard dg(ctx->device);
   if (!spectra) return OXM_ERR_ARGUMENT;
   cudaStream_t s = as_stream(stream);
-  // scratch: x_prev, x_init [3][n] (+ fit counts when the caller does not want them)
+  // scratch: x_init [3][n] (+ fit counts when the caller does not want them)
   void* scratch = nullptr;
-  const size_t bytes = sizeof(double) * 6 * (size_t)n + (fits ? 0 : sizeof(int32_t) * (size_t)n);
+  const size_t bytes = sizeof(double) * 3 * (size_t)n + (fits ? 0 : sizeof(int32_t) * (size_t)n);
   cudaError_t err = cudaMallocAsync(&scratch, bytes, s);
   if (err != cudaSuccess) {
     set_last_error("em_lowpass scratch", err);
@@ -64,9 +64,8 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   io.n = n;
   io.S = spectra;
   io.x = x;
-  io.xprev = static_cast<double*>(scratch);
-  io.xinit = io.xprev + 3 * n;
-  io.fits = fits ? fits : reinterpret_cast<int32_t*>(io.xprev + 6 * n);
+  io.xinit = static_cast<double*>(scratch);
+  io.fits = fits ? fits : reinterpret_cast<int32_t*>(io.xinit + 3 * n);
   const int st = ctx->ops.L == 26 ? launch_em<26, SpecOut::kAosF64>(ctx->ops, io, s)
                                   : launch_em<0, SpecOut::kAosF64>(ctx->ops, io, s);
   cudaFreeAsync(scratch, s);

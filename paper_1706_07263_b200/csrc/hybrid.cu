@@ -462,11 +462,13 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   io.y = ybar;
   io.y_soa = 1;
   io.n = nll;
-  io.S = w.S;
-  io.Shi = w.Shi;
-  io.Slo = w.Slo;
-  io.Lp = w.Lp;
-  io.xprev = w.xprev;
+  if (F32OUT) {
+    io.Shi = w.Shi;
+    io.Slo = w.Slo;
+    io.Lp = w.Lp;
+  } else {
+    io.S = w.S;
+  }
   io.xinit = w.xinit;
   io.fits = fits ? fits : w.fits;
   constexpr SpecOut out = F32OUT ? SpecOut::kAosF32HiLo : SpecOut::kSoaF64;

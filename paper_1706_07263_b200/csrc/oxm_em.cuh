@@ -28,13 +28,13 @@
 
 // band-loop unroll of the EM step (tuned on B200; build knob for experiments)
 #ifndef OXM_EM_UNROLL
-#define OXM_EM_UNROLL 13
+#define OXM_EM_UNROLL 26
 #endif
 #ifndef OXM_EM_UNROLL_B
-#define OXM_EM_UNROLL_B OXM_EM_UNROLL
+#define OXM_EM_UNROLL_B 4
 #endif
 #ifndef OXM_EM_MIN_BLOCKS
-#define OXM_EM_MIN_BLOCKS 1
+#define OXM_EM_MIN_BLOCKS 6
 #endif
 
 namespace oxm {
@@ -68,11 +68,10 @@ __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
 // entries are uniform-datapath constants (ULDC / UR operands) rather than
 // per-thread indexed LDCs feeding every DFMA.
 //
-// The final spectrum is not written here (that would be a 26-store divergent
-// branch in almost every step): the kernel stores x_prev -- the concentration
-// the final step started from -- and em_spectra_kernel rebuilds
-// s = max(exp(-xi x_prev) + G (y - C exp(-xi x_prev)), eps) with the same
-// exp_tab, bit-identically, with coalesced stores.
+// The final spectrum is not written by its own lane (a 26-store divergent
+// branch in almost every step): phase B leaves s = max(e + G r, eps) in the
+// lane's shared-memory column, and when lanes finish the whole warp copies
+// their rows out together (write_spectra: coalesced, ~2 rounds per step).
 enum class SpecOut { kSoaF64, kAosF32HiLo, kAosF64 };
 
 struct EmIO {
@@ -84,8 +83,8 @@ struct EmIO {
   float* Shi;          // kAosF32HiLo: (n, Lp) hi parts, then (n, Lp) lo parts:
   float* Slo;          //   hi + lo = s to 48 bits (Lp = L rounded up to 4)
   int Lp;
+  SpecOut fmt;         // set by launch_em from its OUT parameter
   double* x;           // (n, 3) final concentrations, or null
-  double* xprev;       // [3][n] concentration the final fit step started from (required)
   double* xinit;       // [3][n] fit #1 of the start spectrum (em_init_kernel output, required)
   int32_t* fits;       // (n) fit counts (required)
   int64_t per_warp;    // slice length
@@ -129,9 +128,59 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
   io.xinit[i] = -n0;
   io.xinit[io.n + i] = -n1;
   io.xinit[2 * io.n + i] = -n2;
+  if (ops.max_iters <= 1) {  // bayes.py:195 runs no iteration: fit #1 and the start spectrum are final
+    io.fits[i] = 1;
+    if (io.x) {
+      io.x[3 * i] = -n0;
+      io.x[3 * i + 1] = -n1;
+      io.x[3 * i + 2] = -n2;
+    }
+    for (int l = 0; l < L; ++l) {
+      const double st = clamp_eps(ini ? ini[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0)), ops.eps);
+      if (io.fmt == SpecOut::kSoaF64) {
+        io.S[(int64_t)l * io.n + i] = st;
+      } else if (io.fmt == SpecOut::kAosF64) {
+        io.S[i * L + l] = st;
+      } else {
+        const float h = __double2float_rn(st);
+        io.Shi[i * io.Lp + l] = h;
+        io.Slo[i * io.Lp + l] = __double2float_rn(st - (double)h);
+      }
+    }
+  }
 }
 
-template <int KL>
+// Copy the spectra of the lanes in `done_mask` from their shared-memory
+// columns (column j holds lane j's s_l at ecol0[l * es + j]) to global memory.
+// All 32 lanes take part; consecutive lanes handle consecutive bands of a
+// row, so row-major outputs are written with coalesced stores.
+template <SpecOut OUT>
+__device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol0, int es, int L, unsigned done_mask,
+                                              int64_t idx, int lane) {
+  const int k = __popc(done_mask);
+  const int items = k * L;
+  for (int base = 0; base < items; base += 32) {  // uniform trip count
+    const int q = base + lane;
+    const int j = q < items ? q / L : 0;
+    const int l = q - j * L;
+    const int owner = __fns(done_mask, 0, j + 1);  // lane of the (j+1)-th finished lane
+    const int64_t oidx = __shfl_sync(0xffffffffu, idx, owner < 32 ? owner : 0);
+    if (q < items) {
+      const double s = ecol0[l * es + owner];
+      if constexpr (OUT == SpecOut::kSoaF64) {
+        io.S[(int64_t)l * io.n + oidx] = s;
+      } else if constexpr (OUT == SpecOut::kAosF64) {
+        io.S[oidx * L + l] = s;
+      } else {
+        const float h = __double2float_rn(s);
+        io.Shi[oidx * io.Lp + l] = h;
+        io.Slo[oidx * io.Lp + l] = __double2float_rn(s - (double)h);
+      }
+    }
+  }
+}
+
+template <int KL, SpecOut OUT>
 __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_kernel(const __grid_constant__ DevOps ops,
                                                                                         EmIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -150,15 +199,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   int64_t next = warp * io.per_warp;  // next unassigned coefficient of the slice
   const int64_t stop = min64(next + io.per_warp, io.n);
 
-  if (ops.max_iters <= 1) {  // fit #1 is the answer (bayes.py:195 runs no iteration)
-    for (int64_t i = next + lane; i < stop; i += 32) {
-      for (int k = 0; k < 3; ++k) io.xprev[k * io.n + i] = io.xinit[k * io.n + i];
-      if (io.x)
-        for (int k = 0; k < 3; ++k) io.x[3 * i + k] = io.xinit[k * io.n + i];
-      io.fits[i] = 1;
-    }
-    return;
-  }
+  if (ops.max_iters <= 1) return;  // fit #1 is the answer: written by em_init_kernel
 
   int64_t idx = next + lane < stop ? next + lane : -1;
   next = min64(next + 32, stop);
@@ -197,8 +238,9 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll(KL > 0 ? kEmUnrollB : 2)
     for (int l = 0; l < L; ++l) {
-      const double s = fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es])));
-      const double lg = log_tab(clamp_eps(s, eps), mt);
+      const double s = clamp_eps(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps);
+      e[l * es] = s;  // this step's spectrum, written out below if the lane finishes
+      const double lg = log_tab(s, mt);
       n0 = fma(ops.fitm[0][l], lg, n0);
       n1 = fma(ops.fitm[1][l], lg, n1);
       n2 = fma(ops.fitm[2][l], lg, n2);
@@ -215,9 +257,6 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
       const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
       done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters;
       if (done) {
-        io.xprev[idx] = x0;
-        io.xprev[io.n + idx] = x1;
-        io.xprev[2 * io.n + idx] = x2;
         io.fits[idx] = nfit;
         if (io.x) {
           io.x[3 * idx] = n0;
@@ -229,9 +268,11 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     x0 = n0;
     x1 = n1;
     x2 = n2;
-    // ---- refill finished lanes from the warp's slice (no atomics)
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if (m) {
+      // ---- the whole warp streams the finished lanes' spectra (smem columns) out
+      write_spectra<OUT>(io, e - lane, es, L, m, idx, lane);
+      // ---- refill finished lanes from the warp's slice (no atomics)
       if (done) {
         const int64_t mine = next + __popc(m & lt_mask);
         idx = mine < stop ? mine : -1;
@@ -243,94 +284,15 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   }
 }
 
-// Final spectra from (y, x_prev, fits): one thread per coefficient, the
-// same arithmetic as the last EM step.  Row-major outputs are staged through
-// shared memory (s overwrites the thread's e column) and written back by
-// the whole CTA as one contiguous block, so every store is coalesced.
-template <int KL, SpecOut OUT>
-__global__ void __launch_bounds__(kEmThreads) em_spectra_kernel(const __grid_constant__ DevOps ops, EmIO io) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
-  double* e_all = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem));
-  double* e = e_all + threadIdx.x;
-  constexpr int es = kEmThreads + 1;  // odd stride: conflict-free transpose reads below
-  load_math_tables(mt);
-  __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kEmThreads;
-  const int64_t i = base + threadIdx.x;
-  const int L = BandCount<KL>::get(ops);
-  if (i < io.n) {
-    double y0, y1, y2;
-    if (io.y_soa) {
-      y0 = io.y[i];
-      y1 = io.y[io.n + i];
-      y2 = io.y[2 * io.n + i];
-    } else {
-      y0 = io.y[3 * i];
-      y1 = io.y[3 * i + 1];
-      y2 = io.y[3 * i + 2];
-    }
-    const bool start_only = io.fits[i] <= 1;
-    const double x0 = io.xprev[i], x1 = io.xprev[io.n + i], x2 = io.xprev[2 * io.n + i];
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-#pragma unroll 2
-    for (int l = 0; l < L; ++l) {
-      double el;
-      if (start_only)
-        el = io.init ? io.init[i * L + l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-      else
-        el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
-      e[l * es] = el;
-      c0 = fma(ops.sens[0][l], el, c0);
-      c1 = fma(ops.sens[1][l], el, c1);
-      c2 = fma(ops.sens[2][l], el, c2);
-    }
-    const double r0 = start_only ? 0.0 : y0 - c0;
-    const double r1 = start_only ? 0.0 : y1 - c1;
-    const double r2 = start_only ? 0.0 : y2 - c2;
-    for (int l = 0; l < L; ++l) {
-      const double s =
-          fmax(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), ops.eps);
-      if constexpr (OUT == SpecOut::kSoaF64)
-        io.S[(int64_t)l * io.n + i] = s;  // SoA: already coalesced
-      else
-        e[l * es] = s;
-    }
-  }
-  if constexpr (OUT != SpecOut::kSoaF64) {
-    __syncthreads();
-    const int64_t rows = min64(kEmThreads, io.n - base);
-    if constexpr (OUT == SpecOut::kAosF64) {
-      for (int64_t q = threadIdx.x; q < rows * L; q += kEmThreads) {
-        const int64_t r = q / L, l = q - r * L;
-        io.S[base * L + q] = e_all[l * es + r];
-      }
-    } else {
-      const int Lp = io.Lp;
-      for (int64_t q = threadIdx.x; q < rows * Lp; q += kEmThreads) {
-        const int64_t r = q / Lp, l = q - r * Lp;
-        const double s = l < L ? e_all[l * es + r] : 0.0;
-        const float h = __double2float_rn(s);
-        io.Shi[base * Lp + q] = h;
-        io.Slo[base * Lp + q] = __double2float_rn(s - (double)h);
-      }
-    }
-  }
-}
-
 // Persistent EM launch (enough CTAs to fill every SM once) + spectra kernel.
 template <int KL, SpecOut OUT>
 inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (io.n <= 0) return OXM_OK;
-  if (!io.xprev || !io.fits || !io.xinit) return OXM_ERR_ARGUMENT;
+  if (!io.fits || !io.xinit) return OXM_ERR_ARGUMENT;
+  io.fmt = OUT;
   const size_t smem = em_smem_bytes(ops.L, kEmThreads);
-  auto kern = em_persistent_kernel<KL>;
-  auto kspec = em_spectra_kernel<KL, OUT>;
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  }
-  const size_t smem_spec = em_smem_bytes(ops.L, kEmThreads + 1);
-  if (smem_spec > 48 * 1024) cudaFuncSetAttribute(kspec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_spec);
+  auto kern = em_persistent_kernel<KL, OUT>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -346,10 +308,7 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   int st0 = check_launch("em_init");
   if (st0) return st0;
   kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
-  int st = check_launch("em_persistent");
-  if (st) return st;
-  kspec<<<(unsigned)need, kEmThreads, smem_spec, s>>>(ops, io);
-  return check_launch("em_spectra");
+  return check_launch("em_persistent");
 }
 
 }  // namespace oxm

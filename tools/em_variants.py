@@ -15,12 +15,12 @@ import sys
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {
-    "a13b13": ("OXM_EM_UNROLL=13", "OXM_EM_UNROLL_B=13"),
-    "a13b2": ("OXM_EM_UNROLL=13", "OXM_EM_UNROLL_B=2"),
-    "a13b4": ("OXM_EM_UNROLL=13", "OXM_EM_UNROLL_B=4"),
-    "a13b6": ("OXM_EM_UNROLL=13", "OXM_EM_UNROLL_B=6"),
     "a26b4": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4"),
-    "a8b4": ("OXM_EM_UNROLL=8", "OXM_EM_UNROLL_B=4"),
+    "a26b2": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=2"),
+    "a26b1": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=1"),
+    "a26b4m6": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=6"),
+    "a26b2m6": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=2", "OXM_EM_MIN_BLOCKS=6"),
+    "a26b4m4": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=4"),
 }
 
 
