@@ -31,7 +31,7 @@
 #define OXM_EM_UNROLL 26
 #endif
 #ifndef OXM_EM_UNROLL_B
-#define OXM_EM_UNROLL_B 4
+#define OXM_EM_UNROLL_B 6
 #endif
 #ifndef OXM_EM_MIN_BLOCKS
 #define OXM_EM_MIN_BLOCKS 6

@@ -15,12 +15,12 @@ import sys
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {
-    "a26b4": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4"),
-    "a26b2": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=2"),
-    "a26b1": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=1"),
     "a26b4m6": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=6"),
-    "a26b2m6": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=2", "OXM_EM_MIN_BLOCKS=6"),
-    "a26b4m4": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=4"),
+    "a26b4m7": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=7"),
+    "a26b4m8": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=8"),
+    "a26b6m6": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=6", "OXM_EM_MIN_BLOCKS=6"),
+    "a26b2m7": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=2", "OXM_EM_MIN_BLOCKS=7"),
+    "a13b4m7": ("OXM_EM_UNROLL=13", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=7"),
 }
 
 
@@ -33,8 +33,6 @@ def build() -> None:
 
     for name, defs in VARIANTS.items():
         _build.build(force=True, defines=defs, out=lib(name))
-        log = (lib(name).parent / "ptxas.log").read_text()
-        regs = [ln for ln in log.splitlines() if "em_persistent_kernelILi26ELb0" in ln]
         print(name, "built")
 
 
