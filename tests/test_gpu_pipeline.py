@@ -206,3 +206,55 @@ def test_engine_planes_match_fp64(cuda, golden, sensitivity, basis):
     assert np.max(np.abs(hbo - x[..., 0])) <= 1e-4 * np.max(np.abs(x[..., 0]))
     off = out.offset[0].double().cpu().numpy()
     assert np.max(np.abs(off - x[..., 2])) <= 1e-4
+
+
+# ---------------------------------------------------------------- less-travelled paths
+def test_engine_generic_band_count(cuda):
+    """Fused path with L != 26 (runtime-L kernels) against the oracle."""
+    from paper_1706_07263_b200 import WavelengthGrid, fixtures
+
+    grid = WavelengthGrid(440.0, 9.0, 31)
+    sens, bas = fixtures.default_sensitivity(grid), fixtures.default_basis(grid)
+    frames = np.stack([synth.phantom_rgb_f32(48, 40, s, sens, bas) for s in (3, 4)])
+    _engine_vs_oracle(cuda, sens, bas, frames, 2)
+    cube, cmap = ox.estimate_frame(ox.RgbImage(frames[0]), sens, bas, ox.PipelineConfig(n_levels=2))
+    ref = O.estimate_frame(frames[0], sens.c, bas.xi, n_levels=2)
+    assert np.max(np.abs(cube.data - ref["cube"])) <= 1e-9
+    assert np.max(np.abs(cmap.stacked() - ref["x"])) <= 1e-7
+
+
+@pytest.mark.parametrize("n", [4, 5])
+def test_deep_pyramids(cuda, sensitivity, basis, n):
+    """n >= 4 uses the runtime-recursive low-pass chain."""
+    frames = np.stack([synth.phantom_rgb_f32(70, 97, 8, sensitivity, basis)])
+    _engine_vs_oracle(cuda, sensitivity, basis, frames, n)
+    cube, cmap = ox.estimate_frame(ox.RgbImage(frames[0]), sensitivity, basis, ox.PipelineConfig(n_levels=n))
+    ref = O.estimate_frame(frames[0], sensitivity.c, basis.xi, n_levels=n)
+    assert np.max(np.abs(cube.data - ref["cube"])) <= 1e-9
+
+
+def test_single_iteration_and_knobs(cuda, sensitivity, basis):
+    """max_iters=1 (start fit only), non-default beta/tol/eps/calibration through the fused path."""
+    rgb = synth.phantom_rgb_f32(32, 48, 9, sensitivity, basis)
+    for bc, cal in [(ox.BayesConfig(max_iters=1), 1.0), (ox.BayesConfig(beta=0.5, max_iters=7, rel_tol=1e-6, epsilon=1e-4), 2.5)]:
+        cfg = ox.PipelineConfig(n_levels=1, bayes=bc, calibration_scale=cal)
+        cube, cmap = ox.estimate_frame(ox.RgbImage(rgb), sensitivity, basis, cfg)
+        ref = O.estimate_frame(rgb, sensitivity.c, basis.xi, n_levels=1, beta=bc.beta, max_iters=bc.max_iters,
+                               rel_tol=bc.rel_tol, eps=bc.epsilon, cal=cal)
+        assert np.max(np.abs(cube.data - ref["cube"])) <= 1e-9
+        assert np.max(np.abs(cmap.stacked() - ref["x"])) <= 1e-7 * cal
+        eng = ox.HybridMapEngine(sensitivity, basis, cfg)
+        out = eng.run(torch.from_numpy(rgb[None].astype(np.float32)).to(cuda), fits=True)
+        assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), ref["thb"], ref["so2"])
+        assert np.array_equal(out.fits[0].cpu().numpy(), ref["fits"])
+
+
+def test_tiny_and_empty(cuda, sensitivity, basis):
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=1))
+    empty = eng.run(torch.zeros((0, 8, 8, 3), device=cuda))
+    assert empty.thb.shape == (0, 8, 8)
+    for H, W in [(2, 2), (3, 2), (2, 5)]:
+        rgb = synth.phantom_rgb_f32(H, W, 11, sensitivity, basis, texture_density=0.0)
+        out = eng.run(torch.from_numpy(rgb[None].astype(np.float32)).to(cuda))
+        ref = O.estimate_frame(rgb, sensitivity.c, basis.xi, n_levels=1)
+        assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), ref["thb"], ref["so2"])
