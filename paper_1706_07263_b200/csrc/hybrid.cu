@@ -516,7 +516,7 @@ inline void mark(void* const* ev, int i, cudaStream_t s) {
 template <typename TIn>
 int hybrid_prologue(const oxm_ctx* ctx, const TIn* frames, int64_t batch, int64_t H, int64_t W, int n,
                     void* ws, size_t ws_bytes, LevelDims& d, int64_t& nll, Workspace& w) {
-  if (!ctx || batch < 0 || !frames) return OXM_ERR_ARGUMENT;
+  if (!ctx || batch < 0 || (batch > 0 && !frames)) return OXM_ERR_ARGUMENT;
   if (n < 1 || n > kMaxLevels) return OXM_ERR_ARGUMENT;
   // pipeline.py:177-181: frame must be at least 2^n in both dimensions
   if (H < ((int64_t)1 << n) || W < ((int64_t)1 << n)) return OXM_ERR_ARGUMENT;
@@ -524,6 +524,7 @@ int hybrid_prologue(const oxm_ctx* ctx, const TIn* frames, int64_t batch, int64_
   if (st) return st;
   nll = batch * d.h[n] * d.w[n];
   const int L = ctx->ops.L;
+  if (batch == 0) return OXM_OK;
   if (!ws || ws_bytes < workspace_bytes(L, nll, batch * H * W)) return OXM_ERR_WORKSPACE;
   w = carve(ws, L, nll);
   return OXM_OK;
