@@ -22,10 +22,10 @@ THB_REL = 1e-4
 SO2_ABS = 1e-5
 
 
-def assert_maps_close(thb, so2, ref_thb, ref_so2, thb_rel=THB_REL, so2_abs=SO2_ABS):
+def assert_maps_close(thb, so2, ref_thb, ref_so2, thb_rel=THB_REL, so2_abs=SO2_ABS, thb_atol=1e-12):
     assert np.array_equal(np.isnan(so2), np.isnan(ref_so2)), "SO2 NaN pattern differs"
     err = np.abs(thb - ref_thb)
-    assert np.all(err <= thb_rel * np.abs(ref_thb) + 1e-12), f"THb max rel err {np.max(err / np.maximum(np.abs(ref_thb), 1e-12)):.3e}"
+    assert np.all(err <= thb_rel * np.abs(ref_thb) + thb_atol), f"THb max rel err {np.max(err / np.maximum(np.abs(ref_thb), 1e-12)):.3e}"
     ok = ~np.isnan(ref_so2)
     assert np.max(np.abs(so2[ok] - ref_so2[ok]), initial=0.0) <= so2_abs
 
@@ -245,7 +245,9 @@ def test_single_iteration_and_knobs(cuda, sensitivity, basis):
         assert np.max(np.abs(cmap.stacked() - ref["x"])) <= 1e-7 * cal
         eng = ox.HybridMapEngine(sensitivity, basis, cfg)
         out = eng.run(torch.from_numpy(rgb[None].astype(np.float32)).to(cuda), fits=True)
-        assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), ref["thb"], ref["so2"])
+        # max_iters=1 leaves the unphysical Tikhonov start (THb ~ 0 almost everywhere): a
+        # relative bound is ill-posed at THb ~ 0, so allow 1e-5 g/l absolute on top
+        assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), ref["thb"], ref["so2"], thb_atol=1e-5)
         assert np.array_equal(out.fits[0].cpu().numpy(), ref["fits"])
 
 
