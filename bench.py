@@ -328,6 +328,21 @@ def run_ours(args):
         e2e = {"value": world * B * e2e_steps / e2e_dt, "unit": UNIT,
                "h2d_bytes_per_step": B * H * W * 3 * 4, "d2h_bytes_per_step": B * H * W * 2 * 4,
                "steps": e2e_steps, "chunk_frames": chunk, "api": "HybridMapEngine.maps_from_host -> oxm_hybrid_maps_f32"}
+        # the CLI's own input format: 16-bit PPM rasters (io.py:88-162), decoded on the device
+        scale = float(frames.max().item()) / 65535.0
+        counts = torch.clamp(torch.round(frames / scale), 0, 65535).to(torch.int32).to(torch.uint16)
+        host_u16 = counts.cpu().pin_memory()
+        del counts
+        eng.maps_from_host(host_u16, thb_h, so2_h, chunk=chunk, _state=state, scale=scale, big_endian=False)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            eng.maps_from_host(host_u16, thb_h, so2_h, chunk=chunk, _state=state, scale=scale, big_endian=False)
+        e2e_dt16 = max_over_ranks(time.perf_counter() - t0, dev)
+        e2e["ppm_u16"] = {"value": world * B * e2e_steps / e2e_dt16, "unit": UNIT,
+                          "h2d_bytes_per_step": B * H * W * 3 * 2, "d2h_bytes_per_step": B * H * W * 2 * 4,
+                          "api": "maps_from_host(uint16 PPM counts) -> oxm_hybrid_maps_u16"}
 
     if rank != 0:
         if world > 1:

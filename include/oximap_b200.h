@@ -176,6 +176,14 @@ OXM_API int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t
                         size_t workspace_bytes, float* thb, float* so2, float* hbo, float* hb,
                         float* offset, int32_t* fits, uint32_t* flags, void* stream,
                         void* const* stage_events);
+/* 16-bit PPM rasters (the CLI's input format, io.py:88-162): `frames` holds
+ * (batch, H, W, 3) u16 counts, big-endian as stored in the file when
+ * big_endian != 0; sample value = count * scale computed in fp64 exactly as
+ * read_ppm does.  Halves host->device bytes versus fp32 frames. */
+OXM_API int oxm_hybrid_maps_u16(const oxm_ctx* ctx, const uint16_t* frames, int big_endian, double scale,
+                        int64_t batch, int64_t height, int64_t width, int n_levels, double calibration,
+                        void* workspace, size_t workspace_bytes, float* thb, float* so2, float* hbo, float* hb,
+                        float* offset, int32_t* fits, uint32_t* flags, void* stream, void* const* stage_events);
 /* f64 variant used by the drop-in estimate_frame: everything in fp64, and the
  * (H, W, L) spectral cube (pipeline.py:207-208) is produced when cube != NULL. */
 OXM_API int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, int64_t batch, int64_t height,

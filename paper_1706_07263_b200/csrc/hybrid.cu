@@ -44,55 +44,78 @@ struct LevelDims {
   int64_t h[kMaxLevels + 1], w[kMaxLevels + 1];  // [0] = frame
 };
 
+// Frame sample accessors.  `at(i)` returns sample i (HWC order) as the fp64
+// value the reference sees: the float itself, or count * scale for 16-bit PPM
+// rasters (io.py:139-162 reads big-endian u16 counts and multiplies by the
+// `# scale` comment in fp64).
+template <typename T>
+struct PlainSrc {
+  const T* p;
+  static constexpr bool kF32 = sizeof(T) == 4;
+  __device__ __forceinline__ double at(int64_t i) const { return (double)ldg(p + i); }
+  __device__ __forceinline__ float atf(int64_t i) const { return (float)ldg(p + i); }
+};
+
+struct PpmSrc {
+  const uint16_t* p;
+  double scale;
+  int big_endian;
+  static constexpr bool kF32 = false;
+  __device__ __forceinline__ double at(int64_t i) const {
+    unsigned v = ldg(p + i);
+    if (big_endian) v = ((v & 0xffu) << 8) | (v >> 8);
+    return (double)v * scale;
+  }
+};
+
 // Low-pass value at level K, position (i, j), channel c, with the per-level
 // edge replication of haar.py:80-85 (the odd partner falls back to its twin).
-template <typename TIn, int K>
+template <typename Src, int K>
 struct LowPass {
-  __device__ __forceinline__ static double at(const TIn* img, const LevelDims& d, int64_t i, int64_t j, int c,
-                                              bool& bad) {
+  __device__ __forceinline__ static double at(const Src& img, int64_t base, const LevelDims& d, int64_t i, int64_t j,
+                                              int c, bool& bad) {
     const int64_t i1 = min(2 * i + 1, d.h[K - 1] - 1);
     const int64_t j1 = min(2 * j + 1, d.w[K - 1] - 1);
-    const double a = LowPass<TIn, K - 1>::at(img, d, 2 * i, 2 * j, c, bad);
-    const double b = LowPass<TIn, K - 1>::at(img, d, 2 * i, j1, c, bad);
-    const double cc = LowPass<TIn, K - 1>::at(img, d, i1, 2 * j, c, bad);
-    const double dd = LowPass<TIn, K - 1>::at(img, d, i1, j1, c, bad);
+    const double a = LowPass<Src, K - 1>::at(img, base, d, 2 * i, 2 * j, c, bad);
+    const double b = LowPass<Src, K - 1>::at(img, base, d, 2 * i, j1, c, bad);
+    const double cc = LowPass<Src, K - 1>::at(img, base, d, i1, 2 * j, c, bad);
+    const double dd = LowPass<Src, K - 1>::at(img, base, d, i1, j1, c, bad);
     return 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b), cc), dd);
   }
 };
 
-template <typename TIn>
-struct LowPass<TIn, 0> {
-  __device__ __forceinline__ static double at(const TIn* img, const LevelDims& d, int64_t i, int64_t j, int c,
-                                              bool& bad) {
-    const double v = (double)ldg(img + (i * d.w[0] + j) * 3 + c);
+template <typename Src>
+struct LowPass<Src, 0> {
+  __device__ __forceinline__ static double at(const Src& img, int64_t base, const LevelDims& d, int64_t i, int64_t j,
+                                              int c, bool& bad) {
+    const double v = img.at(base + (i * d.w[0] + j) * 3 + c);
     bad |= !isfinite(v);
     return v;
   }
 };
 
-// Same recursion with a runtime depth (n > 4; rare, correctness path).
-template <typename TIn>
-__device__ __noinline__ double low_pass_rt(const TIn* img, const LevelDims& d, int k, int64_t i, int64_t j, int c,
-                                           bool& bad) {
+// Same recursion with a runtime depth (n > 3; rare, correctness path).
+template <typename Src>
+__device__ __noinline__ double low_pass_rt(const Src& img, int64_t base, const LevelDims& d, int k, int64_t i,
+                                           int64_t j, int c, bool& bad) {
   if (k == 0) {
-    const double v = (double)ldg(img + (i * d.w[0] + j) * 3 + c);
+    const double v = img.at(base + (i * d.w[0] + j) * 3 + c);
     bad |= !isfinite(v);
     return v;
   }
   const int64_t i1 = min(2 * i + 1, d.h[k - 1] - 1);
   const int64_t j1 = min(2 * j + 1, d.w[k - 1] - 1);
-  const double a = low_pass_rt(img, d, k - 1, 2 * i, 2 * j, c, bad);
-  const double b = low_pass_rt(img, d, k - 1, 2 * i, j1, c, bad);
-  const double cc = low_pass_rt(img, d, k - 1, i1, 2 * j, c, bad);
-  const double dd = low_pass_rt(img, d, k - 1, i1, j1, c, bad);
+  const double a = low_pass_rt(img, base, d, k - 1, 2 * i, 2 * j, c, bad);
+  const double b = low_pass_rt(img, base, d, k - 1, 2 * i, j1, c, bad);
+  const double cc = low_pass_rt(img, base, d, k - 1, i1, 2 * j, c, bad);
+  const double dd = low_pass_rt(img, base, d, k - 1, i1, j1, c, bad);
   return 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b), cc), dd);
 }
 
 // ybar[c][idx] = LL_n[b, c] / 2^n for every coefficient of every frame.
-template <typename TIn, int NLV>
-__global__ void __launch_bounds__(kLlThreads) ll_kernel(const TIn* __restrict__ frames, int64_t batch,
-                                                        LevelDims d, double* __restrict__ ybar, int64_t nll,
-                                                        uint32_t* flags) {
+template <typename Src, int NLV>
+__global__ void __launch_bounds__(kLlThreads) ll_kernel(const Src frames, int64_t batch, LevelDims d,
+                                                        double* __restrict__ ybar, int64_t nll, uint32_t* flags) {
   const int64_t idx = (int64_t)blockIdx.x * kLlThreads + threadIdx.x;
   if (idx >= nll) return;
   const int n = d.n;
@@ -101,7 +124,7 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const TIn* __restrict__ 
   const int64_t f = idx / per;
   const int64_t rem = idx - f * per;
   const int64_t by = rem / wL, bx = rem - by * wL;
-  const TIn* img = frames + f * d.h[0] * d.w[0] * 3;
+  const int64_t base = f * d.h[0] * d.w[0] * 3;
   const double inv = ldexp(1.0, -n);  // exact
   bool bad = false;
   bool neg = false;
@@ -109,9 +132,9 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const TIn* __restrict__ 
   for (int c = 0; c < 3; ++c) {
     double v;
     if constexpr (NLV > 0)
-      v = LowPass<TIn, NLV>::at(img, d, by, bx, c, bad);
+      v = LowPass<Src, NLV>::at(frames, base, d, by, bx, c, bad);
     else
-      v = low_pass_rt<TIn>(img, d, n, by, bx, c, bad);
+      v = low_pass_rt<Src>(frames, base, d, n, by, bx, c, bad);
     v *= inv;
     neg |= v < 0.0;
     ybar[c * nll + idx] = v;
@@ -164,9 +187,9 @@ __device__ __forceinline__ float lg2_approx(float v) {
 // kernel, which applies the reference's clamp.  The block spectrum row
 // Shi[coef][Lp] is read with 16-byte loads (Lp = L rounded up to 4), shared
 // through L1 by the 2^n threads of a block column.
-template <int KL, int R, bool PLANES>
+template <int KL, int R, bool PLANES, typename Src>
 __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__ DevOps ops,
-                                                         const float* __restrict__ frames, PxGeom g,
+                                                         const Src frames, PxGeom g,
                                                          const float* __restrict__ Shi, int Lp,
                                                          const double* __restrict__ ybar, float* __restrict__ thb,
                                                          float* __restrict__ so2, float* __restrict__ hbo,
@@ -184,19 +207,25 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   const int nrow = (int)min64(min64(R, g.H - row0), (int64_t)bs);
   const int64_t bidx = (f * g.hL + by) * g.wL + (col >> g.n);
 
+  double yb[3];
   float yh[3], yl[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const double v = ybar[(int64_t)k * g.nll + bidx];
-    yh[k] = __double2float_rn(v);
-    yl[k] = __double2float_rn(v - (double)yh[k]);
+    yb[k] = ybar[(int64_t)k * g.nll + bidx];
+    yh[k] = __double2float_rn(yb[k]);
+    yl[k] = __double2float_rn(yb[k] - (double)yh[k]);
   }
   float d[R][3], a0[R], a1[R], a2[R], vmin[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + min(r, nrow - 1)) * g.W + col;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) d[r][k] = (ldg(frames + 3 * p + k) - yh[k]) - yl[k];
+    for (int k = 0; k < 3; ++k) {
+      if constexpr (Src::kF32)
+        d[r][k] = (frames.atf(3 * p + k) - yh[k]) - yl[k];  // exact-ish: rgb is an fp32 value
+      else
+        d[r][k] = __double2float_rn(frames.at(3 * p + k) - yb[k]);  // decoded sample in fp64
+    }
     a0[r] = a1[r] = a2[r] = 0.f;
     vmin[r] = 3.0e38f;
   }
@@ -289,8 +318,9 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
 // (the 26 band loads and logs of a pixel proceed in parallel), operators
 // staged in shared memory so the per-lane band index does not serialise
 // constant-bank reads; the three fit sums are warp-reduced.
+template <typename Src>
 __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
-                                                                 const float* __restrict__ frames, PxGeom g,
+                                                                 const Src frames, PxGeom g,
                                                                  const float* __restrict__ Shi,
                                                                  const float* __restrict__ Slo, int Lp,
                                                                  const double* __restrict__ ybar,
@@ -316,9 +346,9 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
     const int64_t rem = p - f * plane;
     const int64_t row = rem / g.W, col = rem - row * g.W;
     const int64_t bidx = (f * g.hL + (row >> g.n)) * g.wL + (col >> g.n);
-    const double D0 = (double)frames[3 * p] - ybar[bidx];
-    const double D1 = (double)frames[3 * p + 1] - ybar[g.nll + bidx];
-    const double D2 = (double)frames[3 * p + 2] - ybar[2 * g.nll + bidx];
+    const double D0 = frames.at(3 * p) - ybar[bidx];
+    const double D1 = frames.at(3 * p + 1) - ybar[g.nll + bidx];
+    const double D2 = frames.at(3 * p + 2) - ybar[2 * g.nll + bidx];
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     for (int l = lane; l < L; l += 32) {
       const double S = (double)Shi[bidx * Lp + l] + (double)Slo[bidx * Lp + l];
@@ -442,15 +472,15 @@ Workspace carve(void* ws, int L, int64_t nll) {
 }
 
 // zeroes the fallback counter as part of the low-pass launch (no memset node)
-template <typename TIn>
-int launch_ll(const TIn* frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll, uint32_t* flags,
+template <typename Src>
+int launch_ll(const Src& frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll, uint32_t* flags,
               cudaStream_t s) {
   const unsigned grid = grid_1d(nll, kLlThreads);
   switch (d.n) {
-    case 1: ll_kernel<TIn, 1><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
-    case 2: ll_kernel<TIn, 2><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
-    case 3: ll_kernel<TIn, 3><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
-    default: ll_kernel<TIn, 0><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
+    case 1: ll_kernel<Src, 1><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
+    case 2: ll_kernel<Src, 2><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
+    case 3: ll_kernel<Src, 3><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
+    default: ll_kernel<Src, 0><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
   }
   return check_launch("hybrid_ll");
 }
@@ -476,18 +506,18 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   return launch_em<0, out>(ops, io, s);
 }
 
-template <int KL, bool PLANES>
-void launch_px_rows(const DevOps& ops, const float* frames, const PxGeom& g, dim3 grid, int R, const Workspace& w,
+template <int KL, bool PLANES, typename Src>
+void launch_px_rows(const DevOps& ops, const Src& frames, const PxGeom& g, dim3 grid, int R, const Workspace& w,
                     float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
   switch (R) {
-    case 2: px_f32_kernel<KL, 2, PLANES><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    case 4: px_f32_kernel<KL, 4, PLANES><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    default: px_f32_kernel<KL, 8, PLANES><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    case 2: px_f32_kernel<KL, 2, PLANES, Src><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    case 4: px_f32_kernel<KL, 4, PLANES, Src><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
+    default: px_f32_kernel<KL, 8, PLANES, Src><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
   }
 }
 
-template <int KL>
-int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64_t batch, const Workspace& w,
+template <int KL, typename Src>
+int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t batch, const Workspace& w,
                   float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
   if (!thb || !so2) return OXM_ERR_ARGUMENT;
   // the planes are written all three or none
@@ -504,7 +534,7 @@ int launch_px_f32(const DevOps& ops, const float* frames, const PxGeom& g, int64
     launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
-  px_fallback_kernel<<<148 * 32, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
+  px_fallback_kernel<Src><<<148 * 32, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
                                                      w.fb_list, thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
 }
@@ -513,8 +543,7 @@ inline void mark(void* const* ev, int i, cudaStream_t s) {
   if (ev && ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
 }
 
-template <typename TIn>
-int hybrid_prologue(const oxm_ctx* ctx, const TIn* frames, int64_t batch, int64_t H, int64_t W, int n,
+int hybrid_prologue(const oxm_ctx* ctx, const void* frames, int64_t batch, int64_t H, int64_t W, int n,
                     void* ws, size_t ws_bytes, LevelDims& d, int64_t& nll, Workspace& w) {
   if (!ctx || batch < 0 || (batch > 0 && !frames)) return OXM_ERR_ARGUMENT;
   if (n < 1 || n > kMaxLevels) return OXM_ERR_ARGUMENT;
@@ -545,15 +574,17 @@ extern "C" size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, 
   return workspace_bytes(ctx->ops.L, batch * d.h[n_levels] * d.w[n_levels], batch * height * width);
 }
 
-extern "C" int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,
-                                   int64_t width, int n_levels, double calibration, void* workspace,
-                                   size_t workspace_bytes_, float* thb, float* so2, float* hbo, float* hb,
-                                   float* offset, int32_t* fits, uint32_t* flags, void* stream,
-                                   void* const* ev) {
+namespace oxm {
+namespace {
+template <typename Src>
+int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t batch, int64_t height, int64_t width,
+                int n_levels, double calibration, void* workspace, size_t workspace_bytes_, float* thb, float* so2,
+                float* hbo, float* hb, float* offset, int32_t* fits, uint32_t* flags, void* stream,
+                void* const* ev) {
   LevelDims d;
   int64_t nll;
   Workspace w;
-  int st = hybrid_prologue<float>(ctx, frames, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
+  int st = hybrid_prologue(ctx, raw, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
   if (st) return st;
   if (batch == 0) return OXM_OK;
   // the fallback list stores 32-bit pixel indices
@@ -562,17 +593,38 @@ extern "C" int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int6
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
   zero_u32<<<1, 1, 0, s>>>(w.fb_count);
-  if ((st = launch_ll<float>(frames, batch, d, w.ybar, nll, flags, s))) return st;
+  if ((st = launch_ll(src, batch, d, w.ybar, nll, flags, s))) return st;
   mark(ev, 1, s);
   if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
   mark(ev, 2, s);
   PxGeom g{height, width, d.h[n_levels], d.w[n_levels], nll, n_levels, calibration};
   if (ctx->ops.L == 26)
-    st = launch_px_f32<26>(ctx->ops, frames, g, batch, w, thb, so2, hbo, hb, offset, s);
+    st = launch_px_f32<26>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s);
   else
-    st = launch_px_f32<0>(ctx->ops, frames, g, batch, w, thb, so2, hbo, hb, offset, s);
+    st = launch_px_f32<0>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s);
   mark(ev, 3, s);
   return st;
+}
+}  // namespace
+}  // namespace oxm
+
+extern "C" int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,
+                                   int64_t width, int n_levels, double calibration, void* workspace,
+                                   size_t workspace_bytes_, float* thb, float* so2, float* hbo, float* hb,
+                                   float* offset, int32_t* fits, uint32_t* flags, void* stream,
+                                   void* const* ev) {
+  return hybrid_maps(ctx, frames, PlainSrc<float>{frames}, batch, height, width, n_levels, calibration, workspace,
+                     workspace_bytes_, thb, so2, hbo, hb, offset, fits, flags, stream, ev);
+}
+
+extern "C" int oxm_hybrid_maps_u16(const oxm_ctx* ctx, const uint16_t* frames, int big_endian, double scale,
+                                   int64_t batch, int64_t height, int64_t width, int n_levels, double calibration,
+                                   void* workspace, size_t workspace_bytes_, float* thb, float* so2, float* hbo,
+                                   float* hb, float* offset, int32_t* fits, uint32_t* flags, void* stream,
+                                   void* const* ev) {
+  if (!(scale > 0.0)) return OXM_ERR_DATA;  // io.py:101-102
+  return hybrid_maps(ctx, frames, PpmSrc{frames, scale, big_endian}, batch, height, width, n_levels, calibration,
+                     workspace, workspace_bytes_, thb, so2, hbo, hb, offset, fits, flags, stream, ev);
 }
 
 extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, int64_t batch, int64_t height,
@@ -582,13 +634,13 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
   LevelDims d;
   int64_t nll;
   Workspace w;
-  int st = hybrid_prologue<double>(ctx, frames, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
+  int st = hybrid_prologue(ctx, frames, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
   if (st) return st;
   if (batch == 0) return OXM_OK;
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  if ((st = launch_ll<double>(frames, batch, d, w.ybar, nll, flags, s))) return st;
+  if ((st = launch_ll(PlainSrc<double>{frames}, batch, d, w.ybar, nll, flags, s))) return st;
   mark(ev, 1, s);
   if ((st = launch_em_soa<false>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
   mark(ev, 2, s);

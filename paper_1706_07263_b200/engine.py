@@ -102,10 +102,15 @@ class HybridMapEngine:
 
     # ---- device-resident path ---------------------------------------------
     def launch(self, frames: torch.Tensor, out: MapBatch, *, stream: torch.cuda.Stream | None = None,
-               stage_events=None) -> None:
-        """Enqueue the three kernels on ``stream``; no host synchronisation."""
-        if frames.dtype != torch.float32 or frames.dim() != 4 or frames.shape[-1] != 3 or not frames.is_cuda:
-            raise ArgumentError("frames must be a CUDA float32 (B, H, W, 3) tensor")
+               stage_events=None, scale: float = 1.0, big_endian: bool = True) -> None:
+        """Enqueue the hybrid kernels on ``stream``; no host synchronisation.
+
+        ``frames``: CUDA (B, H, W, 3) float32 values, or uint16 PPM counts
+        (sample = count * ``scale``; ``big_endian`` as stored in the file)."""
+        if frames.dim() != 4 or frames.shape[-1] != 3 or not frames.is_cuda:
+            raise ArgumentError("frames must be a CUDA (B, H, W, 3) tensor")
+        if frames.dtype not in (torch.float32, torch.uint16):
+            raise ArgumentError("frames must be float32 values or uint16 PPM counts")
         if not frames.is_contiguous():
             raise ArgumentError("frames must be contiguous")
         B, H, W, _ = frames.shape
@@ -114,12 +119,14 @@ class HybridMapEngine:
             raise ArgumentError(f"frame {H}x{W} is smaller than 2^{n} in one dimension")
         nbytes = self.workspace_bytes(B, H, W)
         ws = self._workspace(nbytes)
-        st = self._lib.oxm_hybrid_maps_f32(
-            self.ctx.handle, ptr(frames), B, H, W, n, float(self.cfg.calibration_scale), ptr(ws), nbytes,
-            ptr(out.thb), ptr(out.so2), ptr(out.hbo), ptr(out.hb), ptr(out.offset), ptr(out.fits), ptr(out.flags),
-            stream_handle(stream), _event_array(stage_events),
-        )
-        _native.check(st, "hybrid_maps_f32")
+        tail = (B, H, W, n, float(self.cfg.calibration_scale), ptr(ws), nbytes, ptr(out.thb), ptr(out.so2),
+                ptr(out.hbo), ptr(out.hb), ptr(out.offset), ptr(out.fits), ptr(out.flags), stream_handle(stream),
+                _event_array(stage_events))
+        if frames.dtype == torch.float32:
+            st = self._lib.oxm_hybrid_maps_f32(self.ctx.handle, ptr(frames), *tail)
+        else:
+            st = self._lib.oxm_hybrid_maps_u16(self.ctx.handle, ptr(frames), int(big_endian), float(scale), *tail)
+        _native.check(st, "hybrid_maps")
 
     def check_flags(self, out: MapBatch) -> None:
         f = int(out.flags.item())
@@ -128,10 +135,11 @@ class HybridMapEngine:
         if f & _native.FLAG_NEGATIVE_LL:
             raise ArgumentError("low-pass coefficients must be finite and non-negative")
 
-    def run(self, frames: torch.Tensor, *, planes: bool = False, fits: bool = False, check: bool = True) -> MapBatch:
+    def run(self, frames: torch.Tensor, *, planes: bool = False, fits: bool = False, check: bool = True,
+            scale: float = 1.0, big_endian: bool = True) -> MapBatch:
         B, H, W, _ = frames.shape
         out = self.allocate(B, H, W, planes=planes, fits=fits)
-        self.launch(frames, out)
+        self.launch(frames, out, scale=scale, big_endian=big_endian)
         if check:
             self.check_flags(out)
         return out
@@ -145,8 +153,12 @@ class HybridMapEngine:
         *,
         chunk: int = 8,
         _state: dict | None = None,
+        scale: float = 1.0,
+        big_endian: bool = True,
     ) -> None:
-        """Host (pinned) float32 (B, H, W, 3) -> host THb / SO2 (B, H, W).
+        """Host (pinned) (B, H, W, 3) frames -> host THb / SO2 (B, H, W).
+
+        Frames are float32 values or uint16 PPM counts (value = count * scale).
 
         Chunks of ``chunk`` frames are pipelined over three streams: H2D of
         chunk i+1 and D2H of chunk i-1 overlap the kernels of chunk i.  Blocks
@@ -156,7 +168,7 @@ class HybridMapEngine:
             raise ArgumentError("maps_from_host takes host tensors")
         B, H, W, _ = frames.shape
         st = _state if _state is not None else {}
-        key = (chunk, H, W)
+        key = (chunk, H, W, frames.dtype)
         if st.get("key") != key:
             dev = self.device
             st.clear()
@@ -164,7 +176,7 @@ class HybridMapEngine:
             st["h2d"] = torch.cuda.Stream(device=dev)
             st["comp"] = torch.cuda.Stream(device=dev)
             st["d2h"] = torch.cuda.Stream(device=dev)
-            st["in"] = [torch.empty((chunk, H, W, 3), dtype=torch.float32, device=dev) for _ in range(2)]
+            st["in"] = [torch.empty((chunk, H, W, 3), dtype=frames.dtype, device=dev) for _ in range(2)]
             st["out"] = [self.allocate(chunk, H, W) for _ in range(2)]
             st["flags"] = torch.zeros(1, dtype=torch.int32, device=dev)
         h2d, comp, d2h = st["h2d"], st["comp"], st["d2h"]
@@ -193,7 +205,7 @@ class HybridMapEngine:
                 o = outs[k]
                 o.flags = flags
                 view = MapBatch(thb=o.thb[:nb], so2=o.so2[:nb], flags=flags)
-                self.launch(ins[k][:nb], view, stream=comp)
+                self.launch(ins[k][:nb], view, stream=comp, scale=scale, big_endian=big_endian)
                 ev = torch.cuda.Event()
                 ev.record(comp)
                 consumed[k] = ev

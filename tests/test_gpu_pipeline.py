@@ -260,3 +260,35 @@ def test_tiny_and_empty(cuda, sensitivity, basis):
         out = eng.run(torch.from_numpy(rgb[None].astype(np.float32)).to(cuda))
         ref = O.estimate_frame(rgb, sensitivity.c, basis.xi, n_levels=1)
         assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), ref["thb"], ref["so2"])
+
+
+def _ppm_counts(rgb: np.ndarray):
+    """write_ppm's quantisation (io.py:88-109): counts = round(v / scale), scale = max / 65535."""
+    scale = float(rgb.max()) / 65535.0
+    counts = np.clip(np.round(rgb / scale), 0, 65535).astype(np.uint16)
+    return counts, scale
+
+
+def test_ppm_u16_path(cuda, sensitivity, basis):
+    """16-bit PPM rasters decoded on the device (value = count * scale in fp64,
+    exactly read_ppm) match the oracle run on the decoded values."""
+    frames = np.stack([synth.phantom_rgb_f32(1080, 1920, 21, sensitivity, basis),
+                       synth.phantom_rgb_f32(576, 720, 22, sensitivity, basis)[:540, :960]])
+    for n in (1, 2):
+        counts, scale = _ppm_counts(frames[:1] if n == 2 else frames[1:])
+        values = counts.astype(np.float64) * scale  # io.py:161
+        eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=n))
+        be = torch.from_numpy(counts.byteswap().view(np.uint16)).to(cuda)  # big-endian file order
+        out = eng.run(be, scale=scale, big_endian=True, fits=True)
+        ref = O.estimate_frame(values[0], sensitivity.c, basis.xi, n_levels=n, want_cube=False,
+                               threads=O.default_threads())
+        assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), ref["thb"], ref["so2"])
+        assert np.array_equal(out.fits[0].cpu().numpy(), ref["fits"])
+        le = eng.run(torch.from_numpy(counts).to(cuda), scale=scale, big_endian=False)
+        assert torch.equal(le.thb, out.thb)
+        # pipelined host path with u16 frames
+        host = torch.from_numpy(counts.byteswap().view(np.uint16)).pin_memory()
+        thb = torch.empty(counts.shape[:3], dtype=torch.float32).pin_memory()
+        so2 = torch.empty(counts.shape[:3], dtype=torch.float32).pin_memory()
+        eng.maps_from_host(host, thb, so2, chunk=1, scale=scale, big_endian=True)
+        assert torch.equal(thb, out.thb.cpu())
