@@ -94,50 +94,35 @@ struct LowPass<Src, 0> {
   }
 };
 
-// Same recursion with a runtime depth (n > 3; rare, correctness path).
-template <typename Src>
-__device__ __noinline__ double low_pass_rt(const Src& img, int64_t base, const LevelDims& d, int k, int64_t i,
-                                           int64_t j, int c, bool& bad) {
-  if (k == 0) {
-    const double v = img.at(base + (i * d.w[0] + j) * 3 + c);
-    bad |= !isfinite(v);
-    return v;
-  }
-  const int64_t i1 = min(2 * i + 1, d.h[k - 1] - 1);
-  const int64_t j1 = min(2 * j + 1, d.w[k - 1] - 1);
-  const double a = low_pass_rt(img, base, d, k - 1, 2 * i, 2 * j, c, bad);
-  const double b = low_pass_rt(img, base, d, k - 1, 2 * i, j1, c, bad);
-  const double cc = low_pass_rt(img, base, d, k - 1, i1, 2 * j, c, bad);
-  const double dd = low_pass_rt(img, base, d, k - 1, i1, j1, c, bad);
-  return 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b), cc), dd);
-}
-
-// ybar[c][idx] = LL_n[b, c] / 2^n for every coefficient of every frame.
-template <typename Src, int NLV>
+// Low-pass of NLV more levels for every position of the output plane of
+// every frame.  OUT_YBAR: ybar[c][idx] = LL * 2^-scale_exp (SoA, final);
+// otherwise an unscaled HWC fp64 plane feeding the next pass (n > 3 is done
+// as a chain of <= 3-level passes, no recursion on the device stack).
+template <typename Src, int NLV, bool OUT_YBAR>
 __global__ void __launch_bounds__(kLlThreads) ll_kernel(const Src frames, int64_t batch, LevelDims d,
-                                                        double* __restrict__ ybar, int64_t nll, uint32_t* flags) {
+                                                        double* __restrict__ out, int64_t nll, int scale_exp,
+                                                        uint32_t* flags) {
   const int64_t idx = (int64_t)blockIdx.x * kLlThreads + threadIdx.x;
   if (idx >= nll) return;
-  const int n = d.n;
-  const int64_t hL = d.h[n], wL = d.w[n];
+  const int64_t hL = d.h[NLV], wL = d.w[NLV];
   const int64_t per = hL * wL;
   const int64_t f = idx / per;
   const int64_t rem = idx - f * per;
   const int64_t by = rem / wL, bx = rem - by * wL;
   const int64_t base = f * d.h[0] * d.w[0] * 3;
-  const double inv = ldexp(1.0, -n);  // exact
+  const double inv = ldexp(1.0, -scale_exp);  // exact
   bool bad = false;
   bool neg = false;
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    double v;
-    if constexpr (NLV > 0)
-      v = LowPass<Src, NLV>::at(frames, base, d, by, bx, c, bad);
-    else
-      v = low_pass_rt<Src>(frames, base, d, n, by, bx, c, bad);
-    v *= inv;
-    neg |= v < 0.0;
-    ybar[c * nll + idx] = v;
+    double v = LowPass<Src, NLV>::at(frames, base, d, by, bx, c, bad);
+    if constexpr (OUT_YBAR) {
+      v *= inv;
+      neg |= v < 0.0;
+      out[c * nll + idx] = v;
+    } else {
+      out[3 * idx + c] = v;
+    }
   }
   if (flags && (bad || neg)) atomicOr(flags, (bad ? OXM_FLAG_NONFINITE : 0u) | (neg ? OXM_FLAG_NEGATIVE_LL : 0u));
 }
@@ -472,17 +457,64 @@ Workspace carve(void* ws, int L, int64_t nll) {
 }
 
 // zeroes the fallback counter as part of the low-pass launch (no memset node)
+template <typename Src, bool OUT_YBAR>
+void launch_ll_pass(const Src& src, int64_t batch, const LevelDims& d, int nlv, double* out, int64_t count,
+                    int scale_exp, uint32_t* flags, cudaStream_t s) {
+  const unsigned grid = grid_1d(count, kLlThreads);
+  switch (nlv) {
+    case 1: ll_kernel<Src, 1, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(src, batch, d, out, count, scale_exp, flags); break;
+    case 2: ll_kernel<Src, 2, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(src, batch, d, out, count, scale_exp, flags); break;
+    default: ll_kernel<Src, 3, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(src, batch, d, out, count, scale_exp, flags); break;
+  }
+}
+
+// LL chain: one launch for n <= 3; for deeper pyramids, 3-level passes through
+// fp64 HWC intermediate planes (stream-ordered scratch), the last one writing
+// ybar.  The add order per level is the reference's in every pass.
 template <typename Src>
 int launch_ll(const Src& frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll, uint32_t* flags,
               cudaStream_t s) {
-  const unsigned grid = grid_1d(nll, kLlThreads);
-  switch (d.n) {
-    case 1: ll_kernel<Src, 1><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
-    case 2: ll_kernel<Src, 2><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
-    case 3: ll_kernel<Src, 3><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
-    default: ll_kernel<Src, 0><<<grid, kLlThreads, 0, s>>>(frames, batch, d, ybar, nll, flags); break;
+  const int n = d.n;
+  if (n <= 3) {
+    launch_ll_pass<Src, true>(frames, batch, d, n, ybar, nll, n, flags, s);
+    return check_launch("hybrid_ll");
   }
-  return check_launch("hybrid_ll");
+  double* prev = nullptr;
+  int done = 0;
+  int st = OXM_OK;
+  while (done < n) {
+    const int nl = n - done > 3 ? 3 : n - done;
+    LevelDims dp{};
+    dp.n = nl;
+    for (int k = 0; k <= nl; ++k) {
+      dp.h[k] = d.h[done + k];
+      dp.w[k] = d.w[done + k];
+    }
+    const bool last = done + nl == n;
+    const int64_t count = batch * dp.h[nl] * dp.w[nl];
+    double* next = nullptr;
+    if (!last) {
+      cudaError_t err = cudaMallocAsync(reinterpret_cast<void**>(&next), sizeof(double) * 3 * (size_t)count, s);
+      if (err != cudaSuccess) {
+        set_last_error("hybrid_ll scratch", err);
+        st = OXM_ERR_CUDA;
+        break;
+      }
+    }
+    if (done == 0)
+      launch_ll_pass<Src, false>(frames, batch, dp, nl, next, count, 0, flags, s);
+    else if (last)
+      launch_ll_pass<PlainSrc<double>, true>(PlainSrc<double>{prev}, batch, dp, nl, ybar, count, n, flags, s);
+    else
+      launch_ll_pass<PlainSrc<double>, false>(PlainSrc<double>{prev}, batch, dp, nl, next, count, 0, flags, s);
+    st = check_launch("hybrid_ll");
+    if (prev) cudaFreeAsync(prev, s);
+    prev = next;
+    if (st) break;
+    done += nl;
+  }
+  if (prev) cudaFreeAsync(prev, s);
+  return st;
 }
 
 template <bool F32OUT>

@@ -272,10 +272,8 @@ def _ppm_counts(rgb: np.ndarray):
 def test_ppm_u16_path(cuda, sensitivity, basis):
     """16-bit PPM rasters decoded on the device (value = count * scale in fp64,
     exactly read_ppm) match the oracle run on the decoded values."""
-    frames = np.stack([synth.phantom_rgb_f32(1080, 1920, 21, sensitivity, basis),
-                       synth.phantom_rgb_f32(576, 720, 22, sensitivity, basis)[:540, :960]])
-    for n in (1, 2):
-        counts, scale = _ppm_counts(frames[:1] if n == 2 else frames[1:])
+    for n, (H, W, seed) in ((2, (1080, 1920, 21)), (1, (576, 720, 22))):
+        counts, scale = _ppm_counts(synth.phantom_rgb_f32(H, W, seed, sensitivity, basis)[None])
         values = counts.astype(np.float64) * scale  # io.py:161
         eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=n))
         be = torch.from_numpy(counts.byteswap().view(np.uint16)).to(cuda)  # big-endian file order
