@@ -29,7 +29,7 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 def upload(arr: np.ndarray, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
     """Host array -> contiguous device tensor of ``dtype``."""
-    host = torch.from_numpy(np.ascontiguousarray(arr))
+    host = torch.from_numpy(np.require(arr, requirements=("C", "W")))  # copies read-only / strided views
     return host.to(device=device, dtype=dtype, non_blocking=False).contiguous()
 
 
