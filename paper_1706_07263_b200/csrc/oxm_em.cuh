@@ -227,7 +227,11 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
       // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
+#ifdef OXM_EXP2LEVEL
+      const double el = exp_tab2(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+#else
       const double el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+#endif
       e[l * es] = el;
       c0 = fma(ops.sens[0][l], el, c0);
       c1 = fma(ops.sens[1][l], el, c1);

@@ -46,11 +46,15 @@ constexpr double kC5 = 0.20000004768371582;
 struct MathSmem {
   double expt[64];   // 2^(j/64)
   double2 logt[128]; // (c_j, -ln(c_j))
+  double expt2[64];  // 2^(j/4096) (2-level exp)
 };
 
 __device__ __forceinline__ void load_math_tables(MathSmem& t) {
   for (int i = threadIdx.x; i < 128; i += blockDim.x) {
-    if (i < 64) t.expt[i] = kExpTable[i][0];
+    if (i < 64) {
+      t.expt[i] = kExpTable[i][0];
+      t.expt2[i] = kExpTable2[i];
+    }
     t.logt[i] = make_double2(kLogTable[i][0], kLogTable[i][1] + kLogTable[i][2]);
   }
 }
@@ -70,6 +74,23 @@ __device__ __forceinline__ double exp_tab(const double z, const MathSmem& t) {
   const double T = t.expt[k & 63];
   const double res = fma(T, p, T);
   const int m = k >> 6;  // floor(k / 64)
+  return __hiloint2double(__double2hiint(res) + (m << 20), __double2loint(res));
+}
+
+// 2-level variant: z = (4096 m + 64 j1 + j2) ln2/4096 + r, |r| <= ln2/8192,
+// exp(r) - 1 = r + r^2/2 + r^3/6 (next term 2e-18): 9 fp64 ops + 2 lookups.
+__device__ __forceinline__ double exp_tab2(const double z, const MathSmem& t) {
+  const double magic = 6755399441055744.0;
+  const double km = fma(z, k4096OverLn2I, magic);
+  const int k = __double2loint(km);
+  const double kd = km - magic;
+  double r = fma(-kd, kLn2Over4096I, z);  // exact: kd * kLn2Over4096I has <= 40 significant bits
+  r = fma(-kd, kExp2Lo, r);
+  const double q = fma(r, kInv6, 0.5);
+  const double p = fma(q, r * r, r);
+  const double T = t.expt[(k >> 6) & 63] * t.expt2[k & 63];
+  const double res = fma(T, p, T);
+  const int m = k >> 12;
   return __hiloint2double(__double2hiint(res) + (m << 20), __double2loint(res));
 }
 

@@ -15,12 +15,8 @@ import sys
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {
-    "a26b4m6": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=6"),
-    "a26b4m7": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=7"),
-    "a26b4m8": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=8"),
-    "a26b6m6": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=6", "OXM_EM_MIN_BLOCKS=6"),
-    "a26b2m7": ("OXM_EM_UNROLL=26", "OXM_EM_UNROLL_B=2", "OXM_EM_MIN_BLOCKS=7"),
-    "a13b4m7": ("OXM_EM_UNROLL=13", "OXM_EM_UNROLL_B=4", "OXM_EM_MIN_BLOCKS=7"),
+    "base": (),
+    "exp2l": ("OXM_EXP2LEVEL",),
 }
 
 
