@@ -79,6 +79,16 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
       d.fitl2_f[k][l] = static_cast<float>(-ln2 * d.fitm[k][l]);
     }
   }
+  for (int l = 0; l < L; ++l) {
+    d.em_a[l][0] = d.xi[l][0];
+    d.em_a[l][1] = d.xi[l][1];
+    for (int k = 0; k < 3; ++k) {
+      d.em_a[l][2 + k] = d.sens[k][l];
+      d.em_b[l][k] = d.gain[l][k];
+      d.em_b[l][3 + k] = d.fitm[k][l];
+    }
+    d.em_a[l][5] = 0.0;
+  }
   // the EM kernels use xi[:, 2] == 1 (ChromophoreBasis contract, core.py:152-153)
   for (int l = 0; l < L; ++l)
     if (d.xi[l][2] != 1.0) {

@@ -227,27 +227,42 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
       // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
-#ifdef OXM_EXP2LEVEL
-      const double el = exp_tab2(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+#ifdef OXM_EM_PACKED
+      const double* ka = ops.em_a[l];
+      const double el = exp_tab(-fma(ka[0], x0, fma(ka[1], x1, x2)), mt);
+      e[l * es] = el;
+      c0 = fma(ka[2], el, c0);
+      c1 = fma(ka[3], el, c1);
+      c2 = fma(ka[4], el, c2);
 #else
       const double el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
-#endif
       e[l * es] = el;
       c0 = fma(ops.sens[0][l], el, c0);
       c1 = fma(ops.sens[1][l], el, c1);
       c2 = fma(ops.sens[2][l], el, c2);
+#endif
     }
     const double r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll(KL > 0 ? kEmUnrollB : 2)
     for (int l = 0; l < L; ++l) {
+#ifdef OXM_EM_PACKED
+      const double* kb = ops.em_b[l];
+      const double s = clamp_eps(fma(kb[2], r2, fma(kb[1], r1, fma(kb[0], r0, e[l * es]))), eps);
+      e[l * es] = s;  // this step's spectrum, written out below if the lane finishes
+      const double lg = log_tab(s, mt);
+      n0 = fma(kb[3], lg, n0);
+      n1 = fma(kb[4], lg, n1);
+      n2 = fma(kb[5], lg, n2);
+#else
       const double s = clamp_eps(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps);
       e[l * es] = s;  // this step's spectrum, written out below if the lane finishes
       const double lg = log_tab(s, mt);
       n0 = fma(ops.fitm[0][l], lg, n0);
       n1 = fma(ops.fitm[1][l], lg, n1);
       n2 = fma(ops.fitm[2][l], lg, n2);
+#endif
     }
     n0 = -n0;
     n1 = -n1;

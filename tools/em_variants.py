@@ -16,7 +16,9 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {
     "base": (),
-    "exp2l": ("OXM_EXP2LEVEL",),
+    "packed": ("OXM_EM_PACKED",),
+    "packed_b4": ("OXM_EM_PACKED", "OXM_EM_UNROLL_B=4"),
+    "packed_m5": ("OXM_EM_PACKED", "OXM_EM_MIN_BLOCKS=5"),
 }
 
 
