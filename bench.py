@@ -152,7 +152,8 @@ class ClockSampler:
 # ---------------------------------------------------------------- inputs
 def make_frames(batch, H, W, texture, rank, device):
     """(batch, H, W, 3) float32 phantom frames on `device`: 4 distinct truth
-    maps per rank (seeded), forward model + per-frame noise on the GPU."""
+    maps per rank (seeded), forward model + per-frame Philox noise by the
+    oxm_synth_frames_f32 kernel (untimed input staging)."""
     import torch
 
     from paper_1706_07263_b200 import synth

@@ -192,6 +192,19 @@ OXM_API int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, int64
                          double* offset, int32_t* fits, uint32_t* flags, void* stream,
                          void* const* stage_events);
 
+/* ---- off-path helpers ------------------------------------
+ * Synthetic frames on the device: synth.py:150-184 (forward model exp(-xi x),
+ * Gaussian reflectance noise floored at 1e-6, camera projection x exposure)
+ * for `count` frames of one (H, W, 3) truth map (hbo, hb, offset), fp32.
+ * Noise: Philox4x32-10 keyed by `seed`, indexed by (frame0 + f, pixel, band). */
+OXM_API int oxm_synth_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t height, int64_t width,
+                         int64_t count, double noise_sigma, double exposure, uint64_t seed,
+                         uint64_t frame0, float* out, void* stream);
+/* Patch-mean THb trace: timeseries.py:44-73 -- per frame, the sum and count
+ * of finite THb values in rect (x, y, w, h) of (batch, H, W) maps. */
+OXM_API int oxm_patch_mean_f32(const float* thb, int64_t batch, int64_t height, int64_t width, int x, int y,
+                       int w, int h, double* sums, unsigned long long* counts, void* stream);
+
 /* ---- roofline probes ------------------------------------------------------
  * Measure the pipe peaks the non-GEMM kernels are bound by, on this device:
  * fp64 FMA throughput (EM) and fp32 MUFU lg2 throughput (per-pixel fit).

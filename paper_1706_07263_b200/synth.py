@@ -200,23 +200,28 @@ def device_frames(
     *,
     noise_sigma: float = 0.01,
     seed: int = 0,
+    frame0: int = 0,
+    exposure: float = 1.0,
     device=None,
 ):
-    """(count, H, W, 3) float32 CUDA batch: forward model + per-frame noise +
-    camera projection with torch ops (benchmark input staging, untimed)."""
+    """(count, H, W, 3) float32 CUDA frames of one truth map, generated by the
+    oxm_synth_frames_f32 kernel: forward model, Philox reflectance noise floored
+    at REFLECTANCE_FLOOR, camera projection (synth.py:150-184).  Frame k uses
+    noise stream index frame0 + k, so long videos can be generated in chunks."""
     import torch
 
+    from . import _native
+    from .device import ptr, stream_handle
+    from .operators import context, make_operator_set
+
+    check_grids(sensitivity.grid, basis.grid)
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-    x = torch.from_numpy(truth.stacked()).to(dev, torch.float32)
-    xi = torch.from_numpy(basis.xi).to(dev, torch.float32)
-    c = torch.from_numpy(sensitivity.c).to(dev, torch.float32)
-    clean = torch.exp(-(x @ xi.T))  # (H, W, L)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(seed)
+    ops = make_operator_set(n_bands=basis.grid.count, xi=basis.xi, sens=sensitivity.c)
+    ctx = context(ops, dev.index)
+    x = torch.from_numpy(np.ascontiguousarray(truth.stacked(), dtype=np.float32)).to(dev)
     H, W = truth.hbo.shape
     out = torch.empty((count, H, W, 3), dtype=torch.float32, device=dev)
-    for k in range(count):
-        cube = clean + noise_sigma * torch.randn(clean.shape, generator=gen, device=dev)
-        cube.clamp_(min=REFLECTANCE_FLOOR)
-        out[k] = cube @ c.T
+    st = _native.load().oxm_synth_frames_f32(ctx.handle, ptr(x), H, W, count, float(noise_sigma), float(exposure),
+                                             int(seed) & (2**64 - 1), int(frame0), ptr(out), stream_handle())
+    _native.check(st, "synth_frames")
     return out
