@@ -260,6 +260,25 @@ def probe_peaks(lib, torch, dev):
     return out
 
 
+def copy_bandwidth(torch, dev) -> dict:
+    """Pinned H2D / D2H GB/s with both directions running (the e2e roofline)."""
+    n = 256 * 2**20
+    h_in, h_out = torch.empty(n, dtype=torch.uint8).pin_memory(), torch.empty(n, dtype=torch.uint8).pin_memory()
+    d_a, d_b = torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+    for rep in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            with torch.cuda.stream(s1):
+                d_a.copy_(h_in, non_blocking=True)
+            with torch.cuda.stream(s2):
+                h_out.copy_(d_b, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    return {"h2d_gbs": 3 * n / dt / 1e9, "d2h_gbs": 3 * n / dt / 1e9}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -344,6 +363,13 @@ def run_ours(args):
         e2e["ppm_u16"] = {"value": world * B * e2e_steps / e2e_dt16, "unit": UNIT,
                           "h2d_bytes_per_step": B * H * W * 3 * 2, "d2h_bytes_per_step": B * H * W * 2 * 4,
                           "api": "maps_from_host(uint16 PPM counts) -> oxm_hybrid_maps_u16"}
+        bw = copy_bandwidth(torch, dev)
+        for rec in (e2e, e2e["ppm_u16"]):
+            bound = world * B / max(rec["h2d_bytes_per_step"] / (bw["h2d_gbs"] * 1e9),
+                                    rec["d2h_bytes_per_step"] / (bw["d2h_gbs"] * 1e9))
+            rec["pcie_bound"] = bound
+            rec["frac_of_pcie_bound"] = rec["value"] / bound
+        e2e["copy_bandwidth_concurrent"] = bw
 
     if rank != 0:
         if world > 1:

@@ -4,8 +4,9 @@ Input generation only (SURVEY §2 marks synth out of the hot-path scope); it
 restates the reference generator (synth.py:28-184) with the same seeded draw
 order, but renders the thousands of capillary-scale blobs in one vectorised
 scatter-add instead of a Python loop per blob, so 1080p phantoms take about a
-second.  ``device_frames`` runs the forward model on the GPU with torch ops
-to build large benchmark batches quickly.
+second.  ``device_frames`` runs the forward model, Philox noise and camera
+projection in the oxm_synth_frames_f32 kernel to build large
+benchmark batches on the device.
 """
 
 from __future__ import annotations
