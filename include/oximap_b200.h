@@ -205,6 +205,10 @@ OXM_API int oxm_synth_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t
 OXM_API int oxm_patch_mean_f32(const float* thb, int64_t batch, int64_t height, int64_t width, int x, int y,
                        int w, int h, double* sums, unsigned long long* counts, void* stream);
 
+/* SPC1 map payload (io.py:34-39, 79-80): interleave hbo, hb, offset planes
+ * (n each) into the file's (H, W, 3) little-endian fp32 layout. */
+OXM_API int oxm_pack_hwc3_f32(const float* a, const float* b, const float* c, int64_t n, float* out, void* stream);
+
 /* ---- roofline probes ------------------------------------------------------
  * Measure the pipe peaks the non-GEMM kernels are bound by, on this device:
  * fp64 FMA throughput (EM) and fp32 MUFU lg2 throughput (per-pixel fit).

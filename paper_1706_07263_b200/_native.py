@@ -97,6 +97,7 @@ _SIGNATURES = {
     ),
     "oxm_synth_frames_f32": (_i32, [_vp, _vp, _i64, _i64, _i64, _f64, _f64, ctypes.c_uint64, ctypes.c_uint64, _vp, _vp]),
     "oxm_patch_mean_f32": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "oxm_pack_hwc3_f32": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "oxm_probe_fp64_fma": (_i32, [_i32, _i32, _vp, _vp, _vp]),
     "oxm_probe_mufu_lg2": (_i32, [_i32, _i32, _vp, _vp, _vp]),
 }

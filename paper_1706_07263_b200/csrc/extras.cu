@@ -149,10 +149,29 @@ __global__ void patch_mean_finish(const double* __restrict__ psum, const unsigne
   counts[f] = c;
 }
 
+// SPC1 map payload (io.py:34-39, 79-80): (H, W, 3) little-endian fp32 in
+// (hbo, hb, offset) order, interleaved from the three planes on the device.
+__global__ void pack_hwc3_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                 const float* __restrict__ c, int64_t n, float* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[3 * i] = ldg(a + i);
+  out[3 * i + 1] = ldg(b + i);
+  out[3 * i + 2] = ldg(c + i);
+}
+
 }  // namespace
 }  // namespace oxm
 
 using namespace oxm;
+
+extern "C" int oxm_pack_hwc3_f32(const float* a, const float* b, const float* c, int64_t n, float* out,
+                                 void* stream) {
+  if (n < 0 || (n > 0 && (!a || !b || !c || !out))) return OXM_ERR_ARGUMENT;
+  if (n == 0) return OXM_OK;
+  pack_hwc3_kernel<<<grid_1d(n, 256), 256, 0, as_stream(stream)>>>(a, b, c, n, out);
+  return check_launch("pack_hwc3");
+}
 
 extern "C" int oxm_synth_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t height, int64_t width,
                                     int64_t count, double noise_sigma, double exposure, uint64_t seed,

@@ -210,7 +210,20 @@ def estimate_sequence(
         elif dims != shape:
             raise DataError(f"frame dimensions changed mid-stream: {shape} -> {dims}")
         t0 = time.perf_counter()
-        _, cmap = estimate_frame(frame, sensitivity, basis, cfg)
+        cmap = _frame_map(frame, sensitivity, basis, cfg)
         if timings is not None:
             timings.append(time.perf_counter() - t0)
         yield cmap
+
+
+def _frame_map(frame, sensitivity, basis, cfg: PipelineConfig) -> ConcentrationMap:
+    """estimate_frame's map only: the sequence API discards the cube
+    (pipeline.py:241-245), so the hybrid path skips materialising it."""
+    if cfg.mode != "hybrid" or not isinstance(frame, RgbImage):
+        return estimate_frame(frame, sensitivity, basis, cfg)[1]
+    check_grids(sensitivity.grid, basis.grid)
+    ops = _hybrid_operators(sensitivity, basis, cfg)
+    out = hybrid_device(upload(frame.data[None], torch.float64, require_cuda()), ops, cfg.n_levels,
+                        cfg.calibration_scale, want_cube=False)
+    xs = download(out["x"][:, 0])
+    return ConcentrationMap(hbo=xs[0], hb=xs[1], offset=xs[2])

@@ -59,3 +59,30 @@ def test_patch_mean(cuda, rng):
     assert len(tr2) == 3
     with pytest.raises(ox.ArgumentError):
         patch_means_device(torch.from_numpy(thb).to(cuda), (50, 0, 20, 5))
+
+
+def test_ppm_to_spc1_files(cuda, tmp_path, sensitivity, basis):
+    """GPU-native `oximap estimate`: PPM written in the reference format ->
+    SPC1 maps, compared with the oracle on the decoded frame."""
+    from oracle import oximap_oracle as O
+    from paper_1706_07263_b200.io import estimate_files, read_ppm_raw
+
+    rgb = synth.phantom_rgb_f32(72, 100, 5, sensitivity, basis)
+    scale = float(rgb.max()) / 65535.0
+    counts = np.clip(np.round(rgb / scale), 0, 65535).astype(">u2")
+    src = tmp_path / "f.ppm"
+    src.write_bytes(f"P6\n# scale {scale!r}\n100 72\n65535\n".encode("ascii") + counts.tobytes())
+    raw, sc = read_ppm_raw(src)
+    assert sc == scale and raw.shape == (72, 100, 3)
+    dst = tmp_path / "m.spc"
+    assert estimate_files([src], [dst], sensitivity, basis, ox.PipelineConfig(n_levels=2)) == 1
+    buf = dst.read_bytes()
+    header, payload = buf.split(b"\n", 1)
+    assert header.split() == [b"SPC1", b"72", b"100", b"3", b"0.0", b"1.0"]
+    maps = np.frombuffer(payload, dtype="<f4").reshape(72, 100, 3).astype(np.float64)
+    ref = O.estimate_frame(counts.astype(np.float64) * scale, sensitivity.c, basis.xi, n_levels=2)
+    assert np.max(np.abs(maps[..., :2] - ref["x"][..., :2])) <= 1e-4 * np.max(np.abs(ref["x"][..., :2]))
+    with pytest.raises(ox.DataError):
+        bad = tmp_path / "b.ppm"
+        bad.write_bytes(b"P6\n100 72\n255\n" + b"\0" * 10)
+        read_ppm_raw(bad)
