@@ -99,9 +99,15 @@ struct LowPass<Src, 0> {
 // otherwise an unscaled HWC fp64 plane feeding the next pass (n > 3 is done
 // as a chain of <= 3-level passes, no recursion on the device stack).
 template <typename Src, int NLV, bool OUT_YBAR>
-__global__ void __launch_bounds__(kLlThreads) ll_kernel(const Src frames, int64_t batch, LevelDims d,
-                                                        double* __restrict__ out, int64_t nll, int scale_exp,
-                                                        uint32_t* flags) {
+__global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ DevOps ops, const Src frames,
+                                                        int64_t batch, LevelDims d, double* __restrict__ out,
+                                                        int64_t nll, int scale_exp, uint32_t* flags,
+                                                        double* __restrict__ xinit) {
+  __shared__ MathSmem mt;
+  if (OUT_YBAR && xinit) {
+    load_math_tables(mt);
+    __syncthreads();
+  }
   const int64_t idx = (int64_t)blockIdx.x * kLlThreads + threadIdx.x;
   if (idx >= nll) return;
   const int64_t hL = d.h[NLV], wL = d.w[NLV];
@@ -113,6 +119,7 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const Src frames, int64_
   const double inv = ldexp(1.0, -scale_exp);  // exact
   bool bad = false;
   bool neg = false;
+  double yv[3];
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
     double v = LowPass<Src, NLV>::at(frames, base, d, by, bx, c, bad);
@@ -123,8 +130,22 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const Src frames, int64_
     } else {
       out[3 * idx + c] = v;
     }
+    yv[c] = v;
   }
   if (flags && (bad || neg)) atomicOr(flags, (bad ? OXM_FLAG_NONFINITE : 0u) | (neg ? OXM_FLAG_NEGATIVE_LL : 0u));
+  if constexpr (OUT_YBAR) {
+    // fit #1 of the EM (bayes.py:241-250) while the frame streams in
+    if (xinit) {
+      double x0, x1, x2;
+      if (ops.L == 26)
+        start_fit<26>(ops, mt, yv[0], yv[1], yv[2], nullptr, x0, x1, x2);
+      else
+        start_fit<0>(ops, mt, yv[0], yv[1], yv[2], nullptr, x0, x1, x2);
+      xinit[idx] = x0;
+      xinit[nll + idx] = x1;
+      xinit[2 * nll + idx] = x2;
+    }
+  }
 }
 
 // Per-pixel fp64 spectrum + fit (used by the fp64 kernel and as the fp32
@@ -458,13 +479,13 @@ Workspace carve(void* ws, int L, int64_t nll) {
 
 // zeroes the fallback counter as part of the low-pass launch (no memset node)
 template <typename Src, bool OUT_YBAR>
-void launch_ll_pass(const Src& src, int64_t batch, const LevelDims& d, int nlv, double* out, int64_t count,
-                    int scale_exp, uint32_t* flags, cudaStream_t s) {
+void launch_ll_pass(const DevOps& ops, const Src& src, int64_t batch, const LevelDims& d, int nlv, double* out,
+                    int64_t count, int scale_exp, uint32_t* flags, double* xinit, cudaStream_t s) {
   const unsigned grid = grid_1d(count, kLlThreads);
   switch (nlv) {
-    case 1: ll_kernel<Src, 1, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(src, batch, d, out, count, scale_exp, flags); break;
-    case 2: ll_kernel<Src, 2, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(src, batch, d, out, count, scale_exp, flags); break;
-    default: ll_kernel<Src, 3, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(src, batch, d, out, count, scale_exp, flags); break;
+    case 1: ll_kernel<Src, 1, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit); break;
+    case 2: ll_kernel<Src, 2, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit); break;
+    default: ll_kernel<Src, 3, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit); break;
   }
 }
 
@@ -472,11 +493,11 @@ void launch_ll_pass(const Src& src, int64_t batch, const LevelDims& d, int nlv, 
 // fp64 HWC intermediate planes (stream-ordered scratch), the last one writing
 // ybar.  The add order per level is the reference's in every pass.
 template <typename Src>
-int launch_ll(const Src& frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll, uint32_t* flags,
-              cudaStream_t s) {
+int launch_ll(const DevOps& ops, const Src& frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll,
+              uint32_t* flags, double* xinit, cudaStream_t s) {
   const int n = d.n;
   if (n <= 3) {
-    launch_ll_pass<Src, true>(frames, batch, d, n, ybar, nll, n, flags, s);
+    launch_ll_pass<Src, true>(ops, frames, batch, d, n, ybar, nll, n, flags, xinit, s);
     return check_launch("hybrid_ll");
   }
   double* prev = nullptr;
@@ -502,11 +523,11 @@ int launch_ll(const Src& frames, int64_t batch, const LevelDims& d, double* ybar
       }
     }
     if (done == 0)
-      launch_ll_pass<Src, false>(frames, batch, dp, nl, next, count, 0, flags, s);
+      launch_ll_pass<Src, false>(ops, frames, batch, dp, nl, next, count, 0, flags, nullptr, s);
     else if (last)
-      launch_ll_pass<PlainSrc<double>, true>(PlainSrc<double>{prev}, batch, dp, nl, ybar, count, n, flags, s);
+      launch_ll_pass<PlainSrc<double>, true>(ops, PlainSrc<double>{prev}, batch, dp, nl, ybar, count, n, flags, xinit, s);
     else
-      launch_ll_pass<PlainSrc<double>, false>(PlainSrc<double>{prev}, batch, dp, nl, next, count, 0, flags, s);
+      launch_ll_pass<PlainSrc<double>, false>(ops, PlainSrc<double>{prev}, batch, dp, nl, next, count, 0, flags, nullptr, s);
     st = check_launch("hybrid_ll");
     if (prev) cudaFreeAsync(prev, s);
     prev = next;
@@ -532,6 +553,7 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
     io.S = w.S;
   }
   io.xinit = w.xinit;
+  io.xinit_ready = 1;  // computed by the low-pass kernel
   io.fits = fits ? fits : w.fits;
   constexpr SpecOut out = F32OUT ? SpecOut::kAosF32HiLo : SpecOut::kSoaF64;
   if (ops.L == 26) return launch_em<26, out>(ops, io, s);
@@ -625,7 +647,7 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
   zero_u32<<<1, 1, 0, s>>>(w.fb_count);
-  if ((st = launch_ll(src, batch, d, w.ybar, nll, flags, s))) return st;
+  if ((st = launch_ll(ctx->ops, src, batch, d, w.ybar, nll, flags, w.xinit, s))) return st;
   mark(ev, 1, s);
   if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
   mark(ev, 2, s);
@@ -672,7 +694,7 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  if ((st = launch_ll(PlainSrc<double>{frames}, batch, d, w.ybar, nll, flags, s))) return st;
+  if ((st = launch_ll(ctx->ops, PlainSrc<double>{frames}, batch, d, w.ybar, nll, flags, w.xinit, s))) return st;
   mark(ev, 1, s);
   if ((st = launch_em_soa<false>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
   mark(ev, 2, s);

@@ -88,15 +88,35 @@ struct EmIO {
   double* xinit;       // [3][n] fit #1 of the start spectrum (em_init_kernel output, required)
   int32_t* fits;       // (n) fit counts (required)
   int64_t per_warp;    // slice length
+  int xinit_ready;     // x_init already computed (fused into the low-pass kernel)
 };
 
 constexpr int kEmThreads = 128;
 constexpr int kEmUnroll = OXM_EM_UNROLL;
 constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 
-// Fit #1 (bayes.py:241-250, 193): x_init = -F log(max(start, eps)) with the
-// Tikhonov start solve y or the caller's init spectra; one thread per
-// coefficient, fully parallel (no divergence), before the persistent loop.
+// Fit #1 of one coefficient (bayes.py:241-250, 193): x = -F log(max(start, eps))
+// with start = solve y (or ini[0..L) when given).
+template <int KL>
+__device__ __forceinline__ void start_fit(const DevOps& ops, const MathSmem& mt, double y0, double y1, double y2,
+                                          const double* ini, double& x0, double& x1, double& x2) {
+  const int L = BandCount<KL>::get(ops);
+  double n0 = 0.0, n1 = 0.0, n2 = 0.0;
+#pragma unroll(KL > 0 ? KL : 2)
+  for (int l = 0; l < L; ++l) {
+    const double st = ini ? ini[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
+    const double lg = log_tab(clamp_eps(st, ops.eps), mt);
+    n0 = fma(ops.fitm[0][l], lg, n0);
+    n1 = fma(ops.fitm[1][l], lg, n1);
+    n2 = fma(ops.fitm[2][l], lg, n2);
+  }
+  x0 = -n0;
+  x1 = -n1;
+  x2 = -n2;
+}
+
+// Fit #1 for every coefficient, fully parallel, before the persistent loop
+// (the fused video path does this inside its low-pass kernel instead).
 template <int KL>
 __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_constant__ DevOps ops, EmIO io) {
   __shared__ MathSmem mt;
@@ -116,15 +136,11 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
     y2 = io.y[3 * i + 2];
   }
   const double* ini = io.init ? io.init + i * L : nullptr;
-  double n0 = 0.0, n1 = 0.0, n2 = 0.0;
-#pragma unroll(KL > 0 ? KL : 2)
-  for (int l = 0; l < L; ++l) {
-    const double st = ini ? ini[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-    const double lg = log_tab(clamp_eps(st, ops.eps), mt);
-    n0 = fma(ops.fitm[0][l], lg, n0);
-    n1 = fma(ops.fitm[1][l], lg, n1);
-    n2 = fma(ops.fitm[2][l], lg, n2);
-  }
+  double n0, n1, n2;
+  start_fit<KL>(ops, mt, y0, y1, y2, ini, n0, n1, n2);
+  n0 = -n0;
+  n1 = -n1;
+  n2 = -n2;
   io.xinit[i] = -n0;
   io.xinit[io.n + i] = -n1;
   io.xinit[2 * io.n + i] = -n2;
@@ -323,9 +339,11 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (blocks > need) blocks = need;
   const int64_t warps = blocks * (kEmThreads / 32);
   io.per_warp = ceil_div(io.n, warps);
-  em_init_kernel<KL><<<(unsigned)need, kEmThreads, 0, s>>>(ops, io);
-  int st0 = check_launch("em_init");
-  if (st0) return st0;
+  if (!io.xinit_ready || ops.max_iters <= 1) {
+    em_init_kernel<KL><<<(unsigned)need, kEmThreads, 0, s>>>(ops, io);
+    int st0 = check_launch("em_init");
+    if (st0) return st0;
+  }
   kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
   return check_launch("em_persistent");
 }
