@@ -382,17 +382,17 @@ def run_ours(args):
     # per-stage algorithmic work
     px = B * H * W
     bytes_ll = px * 12 + nll * 3 * 8
-    em_flops = (fits_total - nll) * FLOPS_PER_FIT + nll * (FLOPS_INIT + FLOPS_SPECTRA)
+    em_flops = (fits_total - nll) * FLOPS_PER_FIT  # fit #1 runs in the low-pass stage
     px_lg2 = px * 26
     stage_t = {"ll_kernel": stage_s[0], "em": stage_s[1], "px_f32_kernel": stage_s[2]}
     rooflines = {
         "ll_kernel": {"bound": "hbm", "achieved": bytes_ll / stage_s[0] / 1e9, "peak": hbm, "unit": "GB/s",
-                      "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+                      "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                      "note": f"low-pass chain + fused EM fit #1 ({nll} x {FLOPS_INIT} fp64 flops)"},
         "em": {"bound": "fp64", "achieved": em_flops / stage_s[1] / 1e12, "peak": 2 * peaks["fp64_fma"] / 1e12,
                "unit": "TFLOP/s", "peak_source": "fp64 FMA probe (oxm_probe_fp64_fma) in this run",
-               "kernels": "em_persistent_kernel + em_spectra_kernel",
-               "work": f"({fits_total} fits - {nll} start fits) x {FLOPS_PER_FIT} + {nll} coefficients x "
-                       f"({FLOPS_INIT} start fit + {FLOPS_SPECTRA} final spectrum) fp64 flops"},
+               "kernels": "em_persistent_kernel",
+               "work": f"({fits_total} fits - {nll} start fits) x {FLOPS_PER_FIT} fp64 flops"},
         "px_f32_kernel": {"bound": "xu", "achieved": px_lg2 / stage_s[2] / 1e12, "peak": peaks["mufu_lg2"] / 1e12,
                           "unit": "Tlg2/s", "peak_source": "MUFU lg2 probe (oxm_probe_mufu_lg2) in this run",
                           "kernels": "px_f32_kernel + px_fallback_kernel", "work": f"{px} px x 26 lg2"},
@@ -444,10 +444,9 @@ def run_ours(args):
 # per band 62 (exp arg 4, table exp 20, C e 6, e + G r 6, table log 20, fit 6)
 # x 26 bands + 16 per step; the spectra kernel adds 36 per band per coefficient.
 FLOPS_PER_FIT = 62 * 26 + 16
-FLOPS_INIT = 32 * 26   # fit #1: solve y 6, table log 20, fit 6 per band (em_init_kernel)
-FLOPS_SPECTRA = 36 * 26
-# kernels launched per step: zero_u32, ll, em_init, em_persistent, em_spectra, px, fallback
-HybridMapLaunches = 7
+FLOPS_INIT = 32 * 26   # fit #1: solve y 6, table log 20, fit 6 per band (fused into ll_kernel)
+# kernels launched per step: zero_u32, ll (+ fit #1), em_persistent, px, fallback
+HybridMapLaunches = 5
 
 
 def main():
