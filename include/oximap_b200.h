@@ -176,6 +176,16 @@ OXM_API int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t
                         size_t workspace_bytes, float* thb, float* so2, float* hbo, float* hb,
                         float* offset, int32_t* fits, uint32_t* flags, void* stream,
                         void* const* stage_events);
+/* Split launch for sub-batch pipelining: low-pass chain + EM on stream_em,
+ * then (after an event) the per-pixel stage on stream_px, so the caller can
+ * overlap the per-pixel stage of sub-batch k (MUFU/FMA pipes) with the EM of
+ * sub-batch k+1 (fp64 pipe).  em_reserve leaves that many CTA slots per SM
+ * free during the persistent EM for the concurrent kernel. */
+OXM_API int oxm_hybrid_maps_f32_split(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,
+                              int64_t width, int n_levels, double calibration, void* workspace,
+                              size_t workspace_bytes, float* thb, float* so2, float* hbo, float* hb,
+                              float* offset, int32_t* fits, uint32_t* flags, void* stream_em, void* stream_px,
+                              int em_reserve);
 /* 16-bit PPM rasters (the CLI's input format, io.py:88-162): `frames` holds
  * (batch, H, W, 3) u16 counts, big-endian as stored in the file when
  * big_endian != 0; sample value = count * scale computed in fp64 exactly as

@@ -91,6 +91,10 @@ _SIGNATURES = {
         _i32,
         [_vp, _vp, _i64, _i64, _i64, _i32, _f64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     ),
+    "oxm_hybrid_maps_f32_split": (
+        _i32,
+        [_vp, _vp, _i64, _i64, _i64, _i32, _f64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32],
+    ),
     "oxm_hybrid_maps_u16": (
         _i32,
         [_vp, _vp, _i32, _f64, _i64, _i64, _i64, _i32, _f64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

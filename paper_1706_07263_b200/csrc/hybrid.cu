@@ -540,8 +540,9 @@ int launch_ll(const DevOps& ops, const Src& frames, int64_t batch, const LevelDi
 
 template <bool F32OUT>
 int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Workspace& w, int32_t* fits,
-                  cudaStream_t s) {
+                  cudaStream_t s, int reserve = 0) {
   EmIO io{};
+  io.em_reserve = reserve;
   io.y = ybar;
   io.y_soa = 1;
   io.n = nll;
@@ -634,7 +635,7 @@ template <typename Src>
 int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t batch, int64_t height, int64_t width,
                 int n_levels, double calibration, void* workspace, size_t workspace_bytes_, float* thb, float* so2,
                 float* hbo, float* hb, float* offset, int32_t* fits, uint32_t* flags, void* stream,
-                void* const* ev) {
+                void* const* ev, void* stream_px = nullptr, int reserve = 0) {
   LevelDims d;
   int64_t nll;
   Workspace w;
@@ -649,8 +650,16 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   zero_u32<<<1, 1, 0, s>>>(w.fb_count);
   if ((st = launch_ll(ctx->ops, src, batch, d, w.ybar, nll, flags, w.xinit, s))) return st;
   mark(ev, 1, s);
-  if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
+  if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s, reserve))) return st;
   mark(ev, 2, s);
+  if (stream_px) {  // split launch: the per-pixel stage runs on its own stream after the EM
+    cudaEvent_t em_done;
+    cudaEventCreateWithFlags(&em_done, cudaEventDisableTiming);
+    cudaEventRecord(em_done, s);
+    s = as_stream(stream_px);
+    cudaStreamWaitEvent(s, em_done, 0);
+    cudaEventDestroy(em_done);  // released once it has completed
+  }
   PxGeom g{height, width, d.h[n_levels], d.w[n_levels], nll, n_levels, calibration};
   if (ctx->ops.L == 26)
     st = launch_px_f32<26>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s);
@@ -669,6 +678,17 @@ extern "C" int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int6
                                    void* const* ev) {
   return hybrid_maps(ctx, frames, PlainSrc<float>{frames}, batch, height, width, n_levels, calibration, workspace,
                      workspace_bytes_, thb, so2, hbo, hb, offset, fits, flags, stream, ev);
+}
+
+extern "C" int oxm_hybrid_maps_f32_split(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,
+                                         int64_t width, int n_levels, double calibration, void* workspace,
+                                         size_t workspace_bytes_, float* thb, float* so2, float* hbo, float* hb,
+                                         float* offset, int32_t* fits, uint32_t* flags, void* stream_em,
+                                         void* stream_px, int em_reserve) {
+  if (!stream_px) return OXM_ERR_ARGUMENT;
+  return hybrid_maps(ctx, frames, PlainSrc<float>{frames}, batch, height, width, n_levels, calibration, workspace,
+                     workspace_bytes_, thb, so2, hbo, hb, offset, fits, flags, stream_em, nullptr, stream_px,
+                     em_reserve);
 }
 
 extern "C" int oxm_hybrid_maps_u16(const oxm_ctx* ctx, const uint16_t* frames, int big_endian, double scale,

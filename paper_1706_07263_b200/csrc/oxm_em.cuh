@@ -89,6 +89,7 @@ struct EmIO {
   int32_t* fits;       // (n) fit counts (required)
   int64_t per_warp;    // slice length
   int xinit_ready;     // x_init already computed (fused into the low-pass kernel)
+  int em_reserve;      // CTA slots per SM left free for a concurrent kernel
 };
 
 constexpr int kEmThreads = 128;
@@ -333,6 +334,9 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEmThreads, smem);
   if (sms < 1) sms = 1;
+  // leave `em_reserve` CTA slots per SM free so a concurrent per-pixel kernel
+  // (split launch, other stream) can co-reside with the persistent EM
+  per_sm -= io.em_reserve;
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)sms * per_sm;
   const int64_t need = ceil_div(io.n, kEmThreads);

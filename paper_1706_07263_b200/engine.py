@@ -128,6 +128,51 @@ class HybridMapEngine:
             st = self._lib.oxm_hybrid_maps_u16(self.ctx.handle, ptr(frames), int(big_endian), float(scale), *tail)
         _native.check(st, "hybrid_maps")
 
+    def launch_overlapped(self, frames: torch.Tensor, out: MapBatch, *, parts: int = 4, em_reserve: int = 1,
+                          _state: dict | None = None) -> None:
+        """Device-resident path with sub-batch pipelining: the per-pixel stage
+        of part k (MUFU/FMA) runs on a second stream concurrently with the EM of
+        part k+1 (fp64).  Two workspaces alternate between parts.  Ends with
+        the current stream waiting for both streams (no host sync)."""
+        if frames.dtype != torch.float32 or frames.dim() != 4 or not frames.is_cuda or not frames.is_contiguous():
+            raise ArgumentError("frames must be a contiguous CUDA float32 (B, H, W, 3) tensor")
+        B, H, W, _ = frames.shape
+        n = self.cfg.n_levels
+        if H < 2**n or W < 2**n:
+            raise ArgumentError(f"frame {H}x{W} is smaller than 2^{n} in one dimension")
+        st = _state if _state is not None else {}
+        per = -(-B // parts)
+        nbytes = self.workspace_bytes(per, H, W)
+        if st.get("key") != (per, H, W):
+            st.clear()
+            st["key"] = (per, H, W)
+            st["ws"] = [torch.empty(nbytes, dtype=torch.uint8, device=self.device) for _ in range(2)]
+            st["s_em"] = torch.cuda.Stream(device=self.device)
+            st["s_px"] = torch.cuda.Stream(device=self.device)
+        s_em, s_px, ws = st["s_em"], st["s_px"], st["ws"]
+        cur = torch.cuda.current_stream()
+        s_em.wait_stream(cur)
+        s_px.wait_stream(cur)
+        px_done: list = []
+        for i, b0 in enumerate(range(0, B, per)):
+            nb = min(per, B - b0)
+            if i >= 2:
+                s_em.wait_event(px_done[i - 2])  # workspace i % 2 is free again
+            sl = slice(b0, b0 + nb)
+            planes = out.hbo is not None
+            rc = self._lib.oxm_hybrid_maps_f32_split(
+                self.ctx.handle, ptr(frames[sl]), nb, H, W, n, float(self.cfg.calibration_scale), ptr(ws[i & 1]), nbytes,
+                ptr(out.thb[sl]), ptr(out.so2[sl]), ptr(out.hbo[sl]) if planes else None,
+                ptr(out.hb[sl]) if planes else None, ptr(out.offset[sl]) if planes else None,
+                ptr(out.fits[sl]) if out.fits is not None else None, ptr(out.flags), s_em.cuda_stream,
+                s_px.cuda_stream, int(em_reserve))
+            _native.check(rc, "hybrid_maps_f32_split")
+            ev = torch.cuda.Event()
+            ev.record(s_px)
+            px_done.append(ev)
+        cur.wait_stream(s_em)
+        cur.wait_stream(s_px)
+
     def check_flags(self, out: MapBatch) -> None:
         f = int(out.flags.item())
         if f & _native.FLAG_NONFINITE:
