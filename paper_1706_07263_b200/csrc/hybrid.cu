@@ -430,7 +430,7 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
 //   ybar  3 x nll  double
 //   spectra  fp64 SoA S[l][i] (fp64 path), or fp32 Shi[i][Lp] then Slo[i][Lp]
 //            (fp32 path; Lp = L rounded up to 4 for 16-byte row loads)
-//   x_prev, x_init   3 x nll double each,  fit counts  nll int32   (EM bookkeeping)
+//   x_init   3 x nll double (fit #1),  fit counts  nll int32   (EM bookkeeping)
 //   fallback counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
 struct Workspace {
   double* ybar;
@@ -438,7 +438,6 @@ struct Workspace {
   float* Shi;
   float* Slo;
   int Lp;
-  double* xprev;
   double* xinit;
   int32_t* fits;
   uint32_t* fb_count;
@@ -452,7 +451,7 @@ inline int padded_bands(int L) { return (L + 3) & ~3; }
 size_t workspace_bytes(int L, int64_t nll, int64_t npx) {
   return 256 + align256(sizeof(double) * 3 * (size_t)nll) +
          align256(sizeof(double) * (size_t)padded_bands(L) * (size_t)nll) +
-         2 * align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) + 256 +
+         align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) + 256 +
          align256(sizeof(uint32_t) * (size_t)npx);
 }
 
@@ -466,8 +465,6 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.Shi = reinterpret_cast<float*>(p);
   w.Slo = w.Shi + (size_t)w.Lp * (size_t)nll;
   p += align256(sizeof(double) * (size_t)w.Lp * (size_t)nll);
-  w.xprev = reinterpret_cast<double*>(p);
-  p += align256(sizeof(double) * 3 * (size_t)nll);
   w.xinit = reinterpret_cast<double*>(p);
   p += align256(sizeof(double) * 3 * (size_t)nll);
   w.fits = reinterpret_cast<int32_t*>(p);

@@ -194,3 +194,37 @@ class TestValidation:
                              offset=np.zeros((1, 3)))
         assert np.array_equal(m.thb, [[2.0, 2.0, 0.0]])
         assert np.array_equal(m.sat_o2, [[0.5, 0.0, np.nan]], equal_nan=True)
+
+
+class TestPpmHeader:
+    """read_ppm_raw follows the reference header grammar (io.py:112-162)."""
+
+    def _write(self, tmp_path, header: bytes, raster: bytes):
+        p = tmp_path / "f.ppm"
+        p.write_bytes(header + raster)
+        return p
+
+    def test_roundtrip_and_scale(self, tmp_path):
+        from paper_1706_07263_b200.io import read_ppm_raw
+
+        counts = np.arange(2 * 3 * 3, dtype=">u2").reshape(2, 3, 3)
+        p = self._write(tmp_path, b"P6\n# scale 0.5\n3 2\n65535\n", counts.tobytes())
+        raw, scale = read_ppm_raw(p)
+        assert scale == 0.5
+        assert np.array_equal(raw.view(">u2"), counts)  # file byte order, decoded on device
+        p2 = self._write(tmp_path, b"P6 3 2 65535\n", counts.tobytes())
+        assert read_ppm_raw(p2)[1] == 1.0
+
+    @pytest.mark.parametrize("header,raster", [
+        (b"P5\n3 2\n65535\n", b"\0" * 36),
+        (b"P6\n3 2\n255\n", b"\0" * 36),
+        (b"P6\n3 2\n65535\n", b"\0" * 35),
+        (b"P6\n# scale nope\n3 2\n65535\n", b"\0" * 36),
+        (b"P6\n3", b""),
+    ])
+    def test_malformed(self, tmp_path, header, raster):
+        from paper_1706_07263_b200 import DataError
+        from paper_1706_07263_b200.io import read_ppm_raw
+
+        with pytest.raises(DataError):
+            read_ppm_raw(self._write(tmp_path, header, raster))
