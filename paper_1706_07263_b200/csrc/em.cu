@@ -49,9 +49,10 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   DeviceGuard dg(ctx->device);
   if (!spectra) return OXM_ERR_ARGUMENT;
   cudaStream_t s = as_stream(stream);
-  // scratch: x_init [3][n] (+ fit counts when the caller does not want them)
   void* scratch = nullptr;
-  const size_t bytes = sizeof(double) * 3 * (size_t)n + (fits ? 0 : sizeof(int32_t) * (size_t)n);
+  // scratch: EM chunk counter (zeroed by em_init_kernel), x_init [3][n]
+  // (+ fit counts when the caller does not want them)
+  const size_t bytes = 256 + sizeof(double) * 3 * (size_t)n + (fits ? 0 : sizeof(int32_t) * (size_t)n);
   cudaError_t err = cudaMallocAsync(&scratch, bytes, s);
   if (err != cudaSuccess) {
     set_last_error("em_lowpass scratch", err);
@@ -64,7 +65,8 @@ extern "C" int oxm_em_lowpass(const oxm_ctx* ctx, const double* y, const double*
   io.n = n;
   io.S = spectra;
   io.x = x;
-  io.xinit = static_cast<double*>(scratch);
+  io.work = static_cast<unsigned long long*>(scratch);
+  io.xinit = reinterpret_cast<double*>(static_cast<unsigned char*>(scratch) + 256);
   io.fits = fits ? fits : reinterpret_cast<int32_t*>(io.xinit + 3 * n);
   const int st = ctx->ops.L == 26 ? launch_em<26, SpecOut::kAosF64>(ctx->ops, io, s)
                                   : launch_em<0, SpecOut::kAosF64>(ctx->ops, io, s);

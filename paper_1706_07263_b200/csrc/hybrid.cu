@@ -431,7 +431,7 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
 //   spectra  fp64 SoA S[l][i] (fp64 path), or fp32 Shi[i][Lp] then Slo[i][Lp]
 //            (fp32 path; Lp = L rounded up to 4 for 16-byte row loads)
 //   x_init   3 x nll double (fit #1),  fit counts  nll int32   (EM bookkeeping)
-//   fallback counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
+//   fallback counter + EM chunk counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
 struct Workspace {
   double* ybar;
   double* S;
@@ -441,6 +441,7 @@ struct Workspace {
   double* xinit;
   int32_t* fits;
   uint32_t* fb_count;
+  unsigned long long* em_work;  // EM chunk counter (same 256-byte block as fb_count)
   uint32_t* fb_list;
 };
 
@@ -470,6 +471,7 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.fits = reinterpret_cast<int32_t*>(p);
   p += align256(sizeof(int32_t) * (size_t)nll);
   w.fb_count = reinterpret_cast<uint32_t*>(p);
+  w.em_work = reinterpret_cast<unsigned long long*>(p + 128);
   w.fb_list = reinterpret_cast<uint32_t*>(p + 256);
   return w;
 }
@@ -553,6 +555,7 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   io.xinit = w.xinit;
   io.xinit_ready = 1;  // computed by the low-pass kernel
   io.fits = fits ? fits : w.fits;
+  io.work = w.em_work;  // zeroed by zero_counters
   constexpr SpecOut out = F32OUT ? SpecOut::kAosF32HiLo : SpecOut::kSoaF64;
   if (ops.L == 26) return launch_em<26, out>(ops, io, s);
   return launch_em<0, out>(ops, io, s);
@@ -611,8 +614,11 @@ int hybrid_prologue(const oxm_ctx* ctx, const void* frames, int64_t batch, int64
   return OXM_OK;
 }
 
-// fallback counter reset, ordered before the per-pixel kernel
-__global__ void zero_u32(uint32_t* p) { *p = 0u; }
+// fallback + EM chunk counter reset, ordered before the low-pass kernel
+__global__ void zero_counters(uint32_t* fb, unsigned long long* em) {
+  *fb = 0u;
+  *em = 0ull;
+}
 
 }  // namespace
 }  // namespace oxm
@@ -644,7 +650,7 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  zero_u32<<<1, 1, 0, s>>>(w.fb_count);
+  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work);
   if ((st = launch_ll(ctx->ops, src, batch, d, w.ybar, nll, flags, w.xinit, s))) return st;
   mark(ev, 1, s);
   if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s, reserve))) return st;
@@ -711,6 +717,7 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
+  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work);
   if ((st = launch_ll(ctx->ops, PlainSrc<double>{frames}, batch, d, w.ybar, nll, flags, w.xinit, s))) return st;
   mark(ev, 1, s);
   if ((st = launch_em_soa<false>(ctx->ops, w.ybar, nll, w, fits, s))) return st;

@@ -58,9 +58,13 @@ __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
 //
 // A one-thread-per-coefficient loop would leave a warp running until its
 // slowest lane converges (fit counts vary 11..15 per coefficient) and a CTA
-// until its slowest warp.  Here every warp owns a contiguous slice of the
-// coefficients and advances all its lanes one *fit* per step; a lane whose
-// coefficient has converged records it and immediately takes the next one.
+// until its slowest warp.  Here every warp advances all its lanes one *fit*
+// per step; a lane whose coefficient has converged records it and immediately
+// takes the next one from the warp's current chunk of kEmChunk consecutive
+// coefficients.  Chunks are handed out by one global counter (one atomic per
+// chunk, issued by lane 0): fit counts are spatially correlated (smooth
+// regions converge in fewer fits), so static per-warp slices left the SMs
+// unevenly loaded at the end of a launch.
 //
 // Fit #1 (the Tikhonov start) runs beforehand in em_init_kernel, so every
 // persistent step is the same exp/prior/log/fit step and control flow is
@@ -87,7 +91,7 @@ struct EmIO {
   double* x;           // (n, 3) final concentrations, or null
   double* xinit;       // [3][n] fit #1 of the start spectrum (em_init_kernel output, required)
   int32_t* fits;       // (n) fit counts (required)
-  int64_t per_warp;    // slice length
+  unsigned long long* work;  // chunk counter, zero at launch (zeroed by em_init_kernel when it runs)
   int xinit_ready;     // x_init already computed (fused into the low-pass kernel)
   int em_reserve;      // CTA slots per SM left free for a concurrent kernel
 };
@@ -95,6 +99,7 @@ struct EmIO {
 constexpr int kEmThreads = 128;
 constexpr int kEmUnroll = OXM_EM_UNROLL;
 constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
+constexpr int kEmChunk = 64;  // coefficients per dynamically assigned chunk (>= 32)
 
 // Fit #1 of one coefficient (bayes.py:241-250, 193): x = -F log(max(start, eps))
 // with start = solve y (or ini[0..L) when given).
@@ -124,6 +129,7 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
   load_math_tables(mt);
   __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
+  if (i == 0 && io.work) *io.work = 0ull;
   if (i >= io.n) return;
   const int L = BandCount<KL>::get(ops);
   double y0, y1, y2;
@@ -213,13 +219,17 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t warp = ((int64_t)blockIdx.x * kEmThreads + threadIdx.x) >> 5;
-  int64_t next = warp * io.per_warp;  // next unassigned coefficient of the slice
-  const int64_t stop = min64(next + io.per_warp, io.n);
+  // first 32 coefficients statically per warp, then kEmChunk-sized chunks
+  // from io.work, numbered from dyn0
+  const int64_t dyn0 = (int64_t)gridDim.x * kEmThreads;
+  int64_t next = warp * 32;                // next unassigned coefficient of the current chunk
+  int64_t stop = min64(next + 32, io.n);   // end of the current chunk
+  bool exhausted = false;
 
   if (ops.max_iters <= 1) return;  // fit #1 is the answer: written by em_init_kernel
 
   int64_t idx = next + lane < stop ? next + lane : -1;
-  next = min64(next + 32, stop);
+  next = stop;
   int nfit = 1;
   double y0 = 0.0, y1 = 0.0, y2 = 0.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
   auto load = [&](int64_t i) {
@@ -308,23 +318,41 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     if (m) {
       // ---- the whole warp streams the finished lanes' spectra (smem columns) out
       write_spectra<OUT>(io, e - lane, es, L, m, idx, lane);
-      // ---- refill finished lanes from the warp's slice (no atomics)
+      // ---- refill finished lanes: rest of the current chunk, then a new one
+      const int need = __popc(m);
+      const int64_t avail = stop - next;  // warp-uniform
+      int64_t fresh = io.n, fresh_end = io.n;
+      if (avail < need && !exhausted) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(io.work, (unsigned long long)kEmChunk);
+        fresh = dyn0 + (int64_t)__shfl_sync(0xffffffffu, b, 0);
+        fresh_end = min64(fresh + kEmChunk, io.n);
+        exhausted = fresh >= io.n;
+      }
       if (done) {
-        const int64_t mine = next + __popc(m & lt_mask);
-        idx = mine < stop ? mine : -1;
+        const int r = __popc(m & lt_mask);
+        const int64_t mine = r < avail ? next + r : fresh + (r - avail);
+        idx = mine < (r < avail ? stop : fresh_end) ? mine : -1;
         nfit = 1;
         if (idx >= 0) load(idx);
       }
-      next = min64(next + __popc(m), stop);
+      if (avail < need) {
+        next = fresh_end > fresh ? min64(fresh + (need - avail), fresh_end) : fresh_end;
+        stop = fresh_end;
+      } else {
+        next += need;
+      }
     }
   }
 }
 
-// Persistent EM launch (enough CTAs to fill every SM once) + spectra kernel.
+// Persistent EM launch (enough CTAs to fill every SM once).  io.work must be
+// zero when the persistent kernel starts: em_init_kernel zeroes it when it
+// runs, otherwise (x_init fused upstream) the caller does.
 template <int KL, SpecOut OUT>
 inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (io.n <= 0) return OXM_OK;
-  if (!io.fits || !io.xinit) return OXM_ERR_ARGUMENT;
+  if (!io.fits || !io.xinit || !io.work) return OXM_ERR_ARGUMENT;
   io.fmt = OUT;
   const size_t smem = em_smem_bytes(ops.L, kEmThreads);
   auto kern = em_persistent_kernel<KL, OUT>;
@@ -341,8 +369,6 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   int64_t blocks = (int64_t)sms * per_sm;
   const int64_t need = ceil_div(io.n, kEmThreads);
   if (blocks > need) blocks = need;
-  const int64_t warps = blocks * (kEmThreads / 32);
-  io.per_warp = ceil_div(io.n, warps);
   if (!io.xinit_ready || ops.max_iters <= 1) {
     em_init_kernel<KL><<<(unsigned)need, kEmThreads, 0, s>>>(ops, io);
     int st0 = check_launch("em_init");
