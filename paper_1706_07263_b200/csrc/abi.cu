@@ -6,6 +6,7 @@
 #include <new>
 
 #include "oxm_common.cuh"
+#include "oxm_tables.h"
 
 namespace oxm {
 
@@ -80,14 +81,8 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
     }
   }
   for (int l = 0; l < L; ++l) {
-    d.em_a[l][0] = d.xi[l][0];
-    d.em_a[l][1] = d.xi[l][1];
-    for (int k = 0; k < 3; ++k) {
-      d.em_a[l][2 + k] = d.sens[k][l];
-      d.em_b[l][k] = d.gain[l][k];
-      d.em_b[l][3 + k] = d.fitm[k][l];
-    }
-    d.em_a[l][5] = 0.0;
+    d.xis[l][0] = d.xi[l][0] * kExpScale;
+    d.xis[l][1] = d.xi[l][1] * kExpScale;
   }
   // the EM kernels use xi[:, 2] == 1 (ChromophoreBasis contract, core.py:152-153)
   for (int l = 0; l < L; ++l)

@@ -103,11 +103,6 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
                                                         int64_t batch, LevelDims d, double* __restrict__ out,
                                                         int64_t nll, int scale_exp, uint32_t* flags,
                                                         double* __restrict__ xinit) {
-  __shared__ MathSmem mt;
-  if (OUT_YBAR && xinit) {
-    load_math_tables(mt);
-    __syncthreads();
-  }
   const int64_t idx = (int64_t)blockIdx.x * kLlThreads + threadIdx.x;
   if (idx >= nll) return;
   const int64_t hL = d.h[NLV], wL = d.w[NLV];
@@ -138,9 +133,9 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
     if (xinit) {
       double x0, x1, x2;
       if (ops.L == 26)
-        start_fit<26>(ops, mt, yv[0], yv[1], yv[2], nullptr, x0, x1, x2);
+        start_fit<26>(ops, log_table_global(), yv[0], yv[1], yv[2], nullptr, x0, x1, x2);
       else
-        start_fit<0>(ops, mt, yv[0], yv[1], yv[2], nullptr, x0, x1, x2);
+        start_fit<0>(ops, log_table_global(), yv[0], yv[1], yv[2], nullptr, x0, x1, x2);
       xinit[idx] = x0;
       xinit[nll + idx] = x1;
       xinit[2 * nll + idx] = x2;

@@ -30,10 +30,7 @@ struct DevOps {
   double xi[kMaxBands][3];     // chromophore basis, core.py:134-158
   double sens[3][kMaxBands];   // camera matrix C, core.py:112-131
   double gain[kMaxBands][3];   // N^-1 C^T, N = C^T C + beta D2^T D2 (bayes.py:117-129)
-  // the same entries packed per band for the EM loop (16-byte aligned rows,
-  // so each band's constants arrive in three 128-bit uniform loads):
-  double em_a[kMaxBands][6];   // xi0, xi1, C0, C1, C2, 0   (phase A: exp, C e)
-  double em_b[kMaxBands][6];   // G0, G1, G2, F0, F1, F2    (phase B: prior, fit)
+  double xis[kMaxBands][2];    // xi[:, 0:2] * 256/ln2: EM exp arguments pre-scaled (oxm_math.cuh)
 };
 
 struct oxm_ctx_impl {

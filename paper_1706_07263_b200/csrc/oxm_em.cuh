@@ -99,19 +99,23 @@ struct EmIO {
 constexpr int kEmThreads = 128;
 constexpr int kEmUnroll = OXM_EM_UNROLL;
 constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
-constexpr int kEmChunk = 64;  // coefficients per dynamically assigned chunk (>= 32)
+#ifndef OXM_EM_CHUNK
+#define OXM_EM_CHUNK 64
+#endif
+constexpr int kEmChunk = OXM_EM_CHUNK;  // coefficients per dynamically assigned chunk (>= 32)
+static_assert(kEmChunk >= 32, "a refill may need up to 32 fresh coefficients");
 
 // Fit #1 of one coefficient (bayes.py:241-250, 193): x = -F log(max(start, eps))
 // with start = solve y (or ini[0..L) when given).
 template <int KL>
-__device__ __forceinline__ void start_fit(const DevOps& ops, const MathSmem& mt, double y0, double y1, double y2,
+__device__ __forceinline__ void start_fit(const DevOps& ops, const double2* logt, double y0, double y1, double y2,
                                           const double* ini, double& x0, double& x1, double& x2) {
   const int L = BandCount<KL>::get(ops);
   double n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll(KL > 0 ? KL : 2)
   for (int l = 0; l < L; ++l) {
     const double st = ini ? ini[l] : fma(ops.solve[l][2], y2, fma(ops.solve[l][1], y1, ops.solve[l][0] * y0));
-    const double lg = log_tab(clamp_eps(st, ops.eps), mt);
+    const double lg = log_tab(clamp_eps(st, ops.eps), logt);
     n0 = fma(ops.fitm[0][l], lg, n0);
     n1 = fma(ops.fitm[1][l], lg, n1);
     n2 = fma(ops.fitm[2][l], lg, n2);
@@ -125,9 +129,6 @@ __device__ __forceinline__ void start_fit(const DevOps& ops, const MathSmem& mt,
 // (the fused video path does this inside its low-pass kernel instead).
 template <int KL>
 __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_constant__ DevOps ops, EmIO io) {
-  __shared__ MathSmem mt;
-  load_math_tables(mt);
-  __syncthreads();
   const int64_t i = (int64_t)blockIdx.x * kEmThreads + threadIdx.x;
   if (i == 0 && io.work) *io.work = 0ull;
   if (i >= io.n) return;
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
   }
   const double* ini = io.init ? io.init + i * L : nullptr;
   double n0, n1, n2;
-  start_fit<KL>(ops, mt, y0, y1, y2, ini, n0, n1, n2);
+  start_fit<KL>(ops, log_table_global(), y0, y1, y2, ini, n0, n1, n2);
   n0 = -n0;
   n1 = -n1;
   n2 = -n2;
@@ -251,45 +252,26 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   while (__any_sync(0xffffffffu, idx >= 0)) {
     // ---- phase A: expected spectrum e = exp(-xi x) and residual r = y - C e
     double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    const double x2s = x2 * kExpScale;  // xi[:, 2] == 1 (core.py:152-153); xis = xi[:, 0:2] * kExpScale
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
-      // xi[:, 2] == 1 by the ChromophoreBasis contract (core.py:152-153)
-#ifdef OXM_EM_PACKED
-      const double* ka = ops.em_a[l];
-      const double el = exp_tab(-fma(ka[0], x0, fma(ka[1], x1, x2)), mt);
-      e[l * es] = el;
-      c0 = fma(ka[2], el, c0);
-      c1 = fma(ka[3], el, c1);
-      c2 = fma(ka[4], el, c2);
-#else
-      const double el = exp_tab(-fma(ops.xi[l][0], x0, fma(ops.xi[l][1], x1, x2)), mt);
+      const double el = exp_scaled(-fma(ops.xis[l][0], x0, fma(ops.xis[l][1], x1, x2s)), mt);
       e[l * es] = el;
       c0 = fma(ops.sens[0][l], el, c0);
       c1 = fma(ops.sens[1][l], el, c1);
       c2 = fma(ops.sens[2][l], el, c2);
-#endif
     }
     const double r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll(KL > 0 ? kEmUnrollB : 2)
     for (int l = 0; l < L; ++l) {
-#ifdef OXM_EM_PACKED
-      const double* kb = ops.em_b[l];
-      const double s = clamp_eps(fma(kb[2], r2, fma(kb[1], r1, fma(kb[0], r0, e[l * es]))), eps);
-      e[l * es] = s;  // this step's spectrum, written out below if the lane finishes
-      const double lg = log_tab(s, mt);
-      n0 = fma(kb[3], lg, n0);
-      n1 = fma(kb[4], lg, n1);
-      n2 = fma(kb[5], lg, n2);
-#else
       const double s = clamp_eps(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps);
       e[l * es] = s;  // this step's spectrum, written out below if the lane finishes
-      const double lg = log_tab(s, mt);
+      const double lg = log_tab(s, mt.logt);
       n0 = fma(ops.fitm[0][l], lg, n0);
       n1 = fma(ops.fitm[1][l], lg, n1);
       n2 = fma(ops.fitm[2][l], lg, n2);
-#endif
     }
     n0 = -n0;
     n1 = -n1;
