@@ -100,7 +100,7 @@ constexpr int kEmThreads = 128;
 constexpr int kEmUnroll = OXM_EM_UNROLL;
 constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 #ifndef OXM_EM_CHUNK
-#define OXM_EM_CHUNK 64
+#define OXM_EM_CHUNK 32
 #endif
 constexpr int kEmChunk = OXM_EM_CHUNK;  // coefficients per dynamically assigned chunk (>= 32)
 static_assert(kEmChunk >= 32, "a refill may need up to 32 fresh coefficients");
