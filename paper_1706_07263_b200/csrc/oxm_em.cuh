@@ -176,20 +176,20 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
 
 // Copy the spectra of the lanes in `done_mask` from their shared-memory
 // columns (column j holds lane j's s_l at ecol0[l * es + j]) to global memory.
-// All 32 lanes take part; consecutive lanes handle consecutive bands of a
-// row, so row-major outputs are written with coalesced stores.
-template <SpecOut OUT>
+// One finished lane at a time (warp-uniform loop, ~2.4 lanes finish per
+// step); all lanes take part, lane l writing band l, so every row is stored
+// with coalesced 4- or 8-byte accesses.
+template <int KL, SpecOut OUT>
 __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol0, int es, int L, unsigned done_mask,
                                               int64_t idx, int lane) {
-  const int k = __popc(done_mask);
-  const int items = k * L;
-  for (int base = 0; base < items; base += 32) {  // uniform trip count
-    const int q = base + lane;
-    const int j = q < items ? q / L : 0;
-    const int l = q - j * L;
-    const int owner = __fns(done_mask, 0, j + 1);  // lane of the (j+1)-th finished lane
-    const int64_t oidx = __shfl_sync(0xffffffffu, idx, owner < 32 ? owner : 0);
-    if (q < items) {
+  while (done_mask) {
+    const int owner = __ffs(done_mask) - 1;
+    done_mask &= done_mask - 1;
+    const int64_t oidx = __shfl_sync(0xffffffffu, idx, owner);
+#pragma unroll
+    for (int l = lane; l < BandCount<KL>::kMax; l += 32) {
+      if (KL == 0 && l >= L) break;
+      if (KL > 0 && l >= KL) break;
       const double s = ecol0[l * es + owner];
       if constexpr (OUT == SpecOut::kSoaF64) {
         io.S[(int64_t)l * io.n + oidx] = s;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if (m) {
       // ---- the whole warp streams the finished lanes' spectra (smem columns) out
-      write_spectra<OUT>(io, e - lane, es, L, m, idx, lane);
+      write_spectra<KL, OUT>(io, e - lane, es, L, m, idx, lane);
       // ---- refill finished lanes: rest of the current chunk, then a new one
       const int need = __popc(m);
       const int64_t avail = stop - next;  // warp-uniform
