@@ -31,7 +31,7 @@
 #define OXM_EM_UNROLL 26
 #endif
 #ifndef OXM_EM_UNROLL_B
-#define OXM_EM_UNROLL_B 6
+#define OXM_EM_UNROLL_B 26
 #endif
 #ifndef OXM_EM_MIN_BLOCKS
 #define OXM_EM_MIN_BLOCKS 6
@@ -48,9 +48,9 @@ struct BandCount {
   __device__ __forceinline__ static int get(const DevOps& ops) { return KL > 0 ? KL : ops.L; }
 };
 
-// Dynamic shared memory of an EM kernel: tables + one e column per thread.
+// Dynamic shared memory of an EM kernel: tables + G + one e column per thread.
 __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
-  return sizeof(MathSmem) + sizeof(double) * (size_t)L * (size_t)threads;
+  return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands + sizeof(double) * (size_t)L * (size_t)threads;
 }
 
 // ---------------------------------------------------------------------------
@@ -73,9 +73,9 @@ __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
 // per-thread indexed LDCs feeding every DFMA.
 //
 // The final spectrum is not written by its own lane (a 26-store divergent
-// branch in almost every step): phase B leaves s = max(e + G r, eps) in the
-// lane's shared-memory column, and when lanes finish the whole warp copies
-// their rows out together (write_spectra: coalesced, ~2 rounds per step).
+// branch in almost every step): e stays in the lane's shared-memory column,
+// and when lanes finish the whole warp re-forms their s = max(e + G r, eps)
+// rows and writes them out together (write_spectra: coalesced).
 enum class SpecOut { kSoaF64, kAosF32HiLo, kAosF64 };
 
 struct EmIO {
@@ -174,23 +174,28 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
   }
 }
 
-// Copy the spectra of the lanes in `done_mask` from their shared-memory
-// columns (column j holds lane j's s_l at ecol0[l * es + j]) to global memory.
-// One finished lane at a time (warp-uniform loop, ~2.4 lanes finish per
-// step); all lanes take part, lane l writing band l, so every row is stored
-// with coalesced 4- or 8-byte accesses.
+// Write the spectra s = max(e + G r, eps) of the lanes in `done_mask` to
+// global memory.  Phase B does not store s (it only needs log s), so it is
+// re-formed here from the lane's e column in shared memory (column j holds
+// lane j's e_l at ecol0[l * es + j]), its residual r and a shared-memory copy
+// of G -- the same FMAs in the same order, so the same bits.  One finished
+// lane at a time (warp-uniform loop, ~2.4 lanes finish per step); lane l
+// handles band l, so every row is stored with coalesced accesses.
 template <int KL, SpecOut OUT>
 __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol0, int es, int L, unsigned done_mask,
-                                              int64_t idx, int lane) {
+                                              int64_t idx, int lane, double r0, double r1, double r2,
+                                              const double (*gsm)[3], double eps) {
   while (done_mask) {
     const int owner = __ffs(done_mask) - 1;
     done_mask &= done_mask - 1;
     const int64_t oidx = __shfl_sync(0xffffffffu, idx, owner);
+    const double q0 = __shfl_sync(0xffffffffu, r0, owner);
+    const double q1 = __shfl_sync(0xffffffffu, r1, owner);
+    const double q2 = __shfl_sync(0xffffffffu, r2, owner);
 #pragma unroll
     for (int l = lane; l < BandCount<KL>::kMax; l += 32) {
       if (KL == 0 && l >= L) break;
-      if (KL > 0 && l >= KL) break;
-      const double s = ecol0[l * es + owner];
+      const double s = clamp_eps(fma(gsm[l][2], q2, fma(gsm[l][1], q1, fma(gsm[l][0], q0, ecol0[l * es + owner]))), eps);
       if constexpr (OUT == SpecOut::kSoaF64) {
         io.S[(int64_t)l * io.n + oidx] = s;
       } else if constexpr (OUT == SpecOut::kAosF64) {
@@ -209,9 +214,11 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
                                                                                         EmIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
-  double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;
+  double(*gsm)[3] = reinterpret_cast<double(*)[3]>(smem_raw + sizeof(MathSmem));  // G, for write_spectra
+  double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem) + sizeof(ops.gain)) + threadIdx.x;
   constexpr int es = kEmThreads;
   load_math_tables(mt);
+  for (int i = threadIdx.x; i < kMaxBands * 3; i += kEmThreads) gsm[i / 3][i % 3] = ops.gain[i / 3][i % 3];
   __syncthreads();
 
   const int L = BandCount<KL>::get(ops);
@@ -263,11 +270,11 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     }
     const double r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
+    // (s itself is not stored: write_spectra re-forms it for finished lanes)
     double n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll(KL > 0 ? kEmUnrollB : 2)
     for (int l = 0; l < L; ++l) {
       const double s = clamp_eps(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps);
-      e[l * es] = s;  // this step's spectrum, written out below if the lane finishes
       const double lg = log_tab(s, mt.logt);
       n0 = fma(ops.fitm[0][l], lg, n0);
       n1 = fma(ops.fitm[1][l], lg, n1);
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     const unsigned m = __ballot_sync(0xffffffffu, done);
     if (m) {
       // ---- the whole warp streams the finished lanes' spectra (smem columns) out
-      write_spectra<KL, OUT>(io, e - lane, es, L, m, idx, lane);
+      write_spectra<KL, OUT>(io, e - lane, es, L, m, idx, lane, r0, r1, r2, gsm, eps);
       // ---- refill finished lanes: rest of the current chunk, then a new one
       const int need = __popc(m);
       const int64_t avail = stop - next;  // warp-uniform

@@ -16,13 +16,8 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {
     "base": (),
-    "b4": ("OXM_EM_UNROLL_B=4",),
     "b13": ("OXM_EM_UNROLL_B=13",),
-    "a13": ("OXM_EM_UNROLL=13",),
-    "m7": ("OXM_EM_MIN_BLOCKS=7",),
-    "m5": ("OXM_EM_MIN_BLOCKS=5",),
-    "chunk32": ("OXM_EM_CHUNK=32",),
-    "chunk256": ("OXM_EM_CHUNK=256",),
+    "b26": ("OXM_EM_UNROLL_B=26",),
 }
 
 
