@@ -78,6 +78,8 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
       d.sens[k][l] = o->sens[k * L + l];
       d.solve_f[l][k] = static_cast<float>(d.solve[l][k]);
       d.fitl2_f[k][l] = static_cast<float>(-ln2 * d.fitm[k][l]);
+      d.solve_f2[l][k] = make_float2(d.solve_f[l][k], d.solve_f[l][k]);
+      d.fitl2_f2[k][l] = make_float2(d.fitl2_f[k][l], d.fitl2_f[k][l]);
     }
   }
   for (int l = 0; l < L; ++l) {

@@ -183,7 +183,8 @@ __device__ __forceinline__ float lg2_approx(float v) {
 // once, updating its R pixels per band (R independent MUFU/FMA chains).
 // Per band and pixel: 3 FFMA (solve d, started from the block spectrum), one
 // 3-input min per band pair (fallback detection), MUFU lg2, 2 FFMA (hbo, hb;
-// +1 for the offset plane when requested).  No eps clamp: any pixel with a
+// +1 for the offset plane when requested); the FFMAs of two rows issue as one
+// packed FFMA2.  No eps clamp: any pixel with a
 // band below fallback_below (>= eps) is recomputed in fp64 by the fixup
 // kernel, which applies the reference's clamp.  The block spectrum row
 // Shi[coef][Lp] is read with 16-byte loads (Lp = L rounded up to 4), shared
@@ -216,48 +217,59 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
     yh[k] = __double2float_rn(yb[k]);
     yl[k] = __double2float_rn(yb[k] - (double)yh[k]);
   }
-  float d[R][3], a0[R], a1[R], a2[R], vmin[R];
+  // rows are processed in pairs with packed FFMA2 (two fp32 FMAs per
+  // instruction; the per-band constants are pre-duplicated float2s in DevOps)
+  constexpr int P = R / 2;
+  float2 d[P][3], a0[P], a1[P], a2[P];
+  float vmin[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + min(r, nrow - 1)) * g.W + col;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
+      float v;
       if constexpr (Src::kF32)
-        d[r][k] = (frames.atf(3 * p + k) - yh[k]) - yl[k];  // exact-ish: rgb is an fp32 value
+        v = (frames.atf(3 * p + k) - yh[k]) - yl[k];  // exact-ish: rgb is an fp32 value
       else
-        d[r][k] = __double2float_rn(frames.at(3 * p + k) - yb[k]);  // decoded sample in fp64
+        v = __double2float_rn(frames.at(3 * p + k) - yb[k]);  // decoded sample in fp64
+      if (r & 1)
+        d[r >> 1][k].y = v;
+      else
+        d[r >> 1][k].x = v;
     }
-    a0[r] = a1[r] = a2[r] = 0.f;
     vmin[r] = 3.0e38f;
   }
-  auto spec = [&](int l, float sh, float& s_out, int r) {
-    s_out = fmaf(ops.solve_f[l][2], d[r][2], fmaf(ops.solve_f[l][1], d[r][1], fmaf(ops.solve_f[l][0], d[r][0], sh)));
+#pragma unroll
+  for (int q = 0; q < P; ++q) a0[q] = a1[q] = a2[q] = make_float2(0.f, 0.f);
+  auto spec = [&](int l, float sh, int q) {
+    return __ffma2_rn(ops.solve_f2[l][2], d[q][2],
+                      __ffma2_rn(ops.solve_f2[l][1], d[q][1], __ffma2_rn(ops.solve_f2[l][0], d[q][0], make_float2(sh, sh))));
   };
-  auto fit = [&](int l, float s, int r) {
-    const float lg = lg2_approx(s);
-    a0[r] = fmaf(ops.fitl2_f[0][l], lg, a0[r]);
-    a1[r] = fmaf(ops.fitl2_f[1][l], lg, a1[r]);
-    if constexpr (PLANES) a2[r] = fmaf(ops.fitl2_f[2][l], lg, a2[r]);
+  auto fit = [&](int l, float2 s, int q) {
+    const float2 lg = make_float2(lg2_approx(s.x), lg2_approx(s.y));
+    a0[q] = __ffma2_rn(ops.fitl2_f2[0][l], lg, a0[q]);
+    a1[q] = __ffma2_rn(ops.fitl2_f2[1][l], lg, a1[q]);
+    if constexpr (PLANES) a2[q] = __ffma2_rn(ops.fitl2_f2[2][l], lg, a2[q]);
   };
   const float* sp = Shi + bidx * Lp;
   if constexpr (KL > 0 && KL % 2 == 0) {
     const float4* sp4 = reinterpret_cast<const float4*>(sp);
 #pragma unroll
-    for (int q = 0; q < (KL + 3) / 4; ++q) {
-      const float4 v = ldg(sp4 + q);
+    for (int qq = 0; qq < (KL + 3) / 4; ++qq) {
+      const float4 v = ldg(sp4 + qq);
       const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
       for (int h = 0; h < 4; h += 2) {
-        const int l = 4 * q + h;
+        const int l = 4 * qq + h;
         if (l < KL) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            float s0, s1;
-            spec(l, vv[h], s0, r);
-            spec(l + 1, vv[h + 1], s1, r);
-            vmin[r] = fminf(vmin[r], fminf(s0, s1));
-            fit(l, s0, r);
-            fit(l + 1, s1, r);
+          for (int q = 0; q < P; ++q) {
+            const float2 s0 = spec(l, vv[h], q);
+            const float2 s1 = spec(l + 1, vv[h + 1], q);
+            vmin[2 * q] = fminf(vmin[2 * q], fminf(s0.x, s1.x));
+            vmin[2 * q + 1] = fminf(vmin[2 * q + 1], fminf(s0.y, s1.y));
+            fit(l, s0, q);
+            fit(l + 1, s1, q);
           }
         }
       }
@@ -268,11 +280,11 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
       if (KL == 0 && l >= L) break;
       const float sh = ldg(sp + l);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        float s0;
-        spec(l, sh, s0, r);
-        vmin[r] = fminf(vmin[r], s0);
-        fit(l, s0, r);
+      for (int q = 0; q < P; ++q) {
+        const float2 s0 = spec(l, sh, q);
+        vmin[2 * q] = fminf(vmin[2 * q], s0.x);
+        vmin[2 * q + 1] = fminf(vmin[2 * q + 1], s0.y);
+        fit(l, s0, q);
       }
     }
   }
@@ -283,7 +295,9 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + r) * g.W + col;
     if (r < nrow) {
-      const float xo = a0[r] * cal, xd = a1[r] * cal;
+      const float A0 = (r & 1) ? a0[r >> 1].y : a0[r >> 1].x;
+      const float A1 = (r & 1) ? a1[r >> 1].y : a1[r >> 1].x;
+      const float xo = A0 * cal, xd = A1 * cal;
       const float co = fmaxf(xo, 0.f);
       const float t = co + fmaxf(xd, 0.f);
       thb[p] = t;
@@ -291,7 +305,7 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
       if constexpr (PLANES) {
         hbo[p] = xo;
         hb[p] = xd;
-        off[p] = a2[r];
+        off[p] = (r & 1) ? a2[r >> 1].y : a2[r >> 1].x;
       }
       any_fb |= !(vmin[r] >= thr);  // also catches NaN
     }

@@ -19,6 +19,8 @@ struct DevOps {
   // fp32 copies first: low parameter-bank offsets encode directly in FFMA
   float solve_f[kMaxBands][3];
   float fitl2_f[3][kMaxBands];  // -ln(2) * fit_mat: x = sum_l fitl2 * log2(s)
+  float2 solve_f2[kMaxBands][3];   // the same, duplicated into both halves for FFMA2
+  float2 fitl2_f2[3][kMaxBands];
   float eps_f;
   int L;
   int max_iters;
