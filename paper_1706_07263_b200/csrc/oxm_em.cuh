@@ -33,8 +33,11 @@
 #ifndef OXM_EM_UNROLL_B
 #define OXM_EM_UNROLL_B 26
 #endif
+#ifndef OXM_EM_SLOTS
+#define OXM_EM_SLOTS 1
+#endif
 #ifndef OXM_EM_MIN_BLOCKS
-#define OXM_EM_MIN_BLOCKS 6
+#define OXM_EM_MIN_BLOCKS 5
 #endif
 
 namespace oxm {
@@ -50,7 +53,7 @@ struct BandCount {
 
 // Dynamic shared memory of an EM kernel: tables + G + one e column per thread.
 __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
-  return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands + sizeof(double) * (size_t)L * (size_t)threads;
+  return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands + sizeof(double) * (size_t)L * (size_t)threads * OXM_EM_SLOTS;
 }
 
 // ---------------------------------------------------------------------------
@@ -103,6 +106,7 @@ constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 #define OXM_EM_CHUNK 32
 #endif
 constexpr int kEmChunk = OXM_EM_CHUNK;  // coefficients per dynamically assigned chunk (>= 32)
+constexpr int kEmSlots = OXM_EM_SLOTS;  // coefficients in flight per thread
 static_assert(kEmChunk >= 32, "a refill may need up to 32 fresh coefficients");
 
 // Fit #1 of one coefficient (bayes.py:241-250, 193): x = -F log(max(start, eps))
@@ -212,9 +216,11 @@ __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol
 template <int KL, SpecOut OUT>
 __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_kernel(const __grid_constant__ DevOps ops,
                                                                                         EmIO io) {
+  constexpr int NS = kEmSlots;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
   double(*gsm)[3] = reinterpret_cast<double(*)[3]>(smem_raw + sizeof(MathSmem));  // G, for write_spectra
+  // e of slot s, band l at e[(s * L + l) * es]: one column per thread and slot
   double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem) + sizeof(ops.gain)) + threadIdx.x;
   constexpr int es = kEmThreads;
   load_math_tables(mt);
@@ -227,109 +233,146 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t warp = ((int64_t)blockIdx.x * kEmThreads + threadIdx.x) >> 5;
-  // first 32 coefficients statically per warp, then kEmChunk-sized chunks
-  // from io.work, numbered from dyn0
-  const int64_t dyn0 = (int64_t)gridDim.x * kEmThreads;
-  int64_t next = warp * 32;                // next unassigned coefficient of the current chunk
-  int64_t stop = min64(next + 32, io.n);   // end of the current chunk
+  // first 32 * NS coefficients statically per warp, then kEmChunk-sized
+  // chunks from io.work, numbered from dyn0
+  const int64_t dyn0 = (int64_t)gridDim.x * kEmThreads * NS;
+  int64_t next = warp * 32 * NS;               // next unassigned coefficient of the current chunk
+  int64_t stop = min64(next + 32 * NS, io.n);  // end of the current chunk
   bool exhausted = false;
 
   if (ops.max_iters <= 1) return;  // fit #1 is the answer: written by em_init_kernel
 
-  int64_t idx = next + lane < stop ? next + lane : -1;
-  next = stop;
-  int nfit = 1;
-  double y0 = 0.0, y1 = 0.0, y2 = 0.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
-  auto load = [&](int64_t i) {
-    if (io.y_soa) {
-      y0 = io.y[i];
-      y1 = io.y[io.n + i];
-      y2 = io.y[2 * io.n + i];
-    } else {
-      y0 = io.y[3 * i];
-      y1 = io.y[3 * i + 1];
-      y2 = io.y[3 * i + 2];
+  // y layout is fixed per output format (hybrid path: SoA; estimate_lowpass
+  // API: AoS), so the refill has no runtime branch for it
+  constexpr bool kYSoa = OUT != SpecOut::kAosF64;
+  int64_t idx[NS];
+  int nfit[NS];
+  double y[NS][3], x[NS][3];
+  auto load = [&](int sl, int64_t i) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      y[sl][k] = kYSoa ? io.y[k * io.n + i] : io.y[3 * i + k];
+      x[sl][k] = io.xinit[k * io.n + i];
     }
-    x0 = io.xinit[i];
-    x1 = io.xinit[io.n + i];
-    x2 = io.xinit[2 * io.n + i];
   };
-  if (idx >= 0) load(idx);
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) {
+    const int64_t i = next + 32 * sl + lane;
+    idx[sl] = i < stop ? i : -1;
+    nfit[sl] = 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) y[sl][k] = x[sl][k] = 0.0;
+    if (idx[sl] >= 0) load(sl, idx[sl]);
+  }
+  next = stop;
 
-  while (__any_sync(0xffffffffu, idx >= 0)) {
+  // refill the finished lanes (mask m) of slot sl: rest of the current chunk,
+  // then a new one
+  auto refill = [&](int sl, unsigned m, bool done) {
+    const int need = __popc(m);
+    const int64_t avail = stop - next;  // warp-uniform
+    int64_t fresh = io.n, fresh_end = io.n;
+    if (avail < need && !exhausted) {
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(io.work, (unsigned long long)kEmChunk);
+      fresh = dyn0 + (int64_t)__shfl_sync(0xffffffffu, b, 0);
+      fresh_end = min64(fresh + kEmChunk, io.n);
+      exhausted = fresh >= io.n;
+    }
+    if (done) {
+      const int r = __popc(m & lt_mask);
+      const int64_t mine = r < avail ? next + r : fresh + (r - avail);
+      idx[sl] = mine < (r < avail ? stop : fresh_end) ? mine : -1;
+      nfit[sl] = 1;
+      if (idx[sl] >= 0) load(sl, idx[sl]);
+    }
+    if (avail < need) {
+      next = fresh_end > fresh ? min64(fresh + (need - avail), fresh_end) : fresh_end;
+      stop = fresh_end;
+    } else {
+      next += need;
+    }
+  };
+
+  auto any_active = [&]() {
+    bool a = false;
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) a |= idx[sl] >= 0;
+    return __any_sync(0xffffffffu, a);
+  };
+
+  while (any_active()) {
     // ---- phase A: expected spectrum e = exp(-xi x) and residual r = y - C e
-    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-    const double x2s = x2 * kExpScale;  // xi[:, 2] == 1 (core.py:152-153); xis = xi[:, 0:2] * kExpScale
+    double c[NS][3], x2s[NS];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      c[sl][0] = c[sl][1] = c[sl][2] = 0.0;
+      x2s[sl] = x[sl][2] * kExpScale;  // xi[:, 2] == 1 (core.py:152-153); xis = xi[:, 0:2] * kExpScale
+    }
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
-      const double el = exp_scaled(-fma(ops.xis[l][0], x0, fma(ops.xis[l][1], x1, x2s)), mt);
-      e[l * es] = el;
-      c0 = fma(ops.sens[0][l], el, c0);
-      c1 = fma(ops.sens[1][l], el, c1);
-      c2 = fma(ops.sens[2][l], el, c2);
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const double el = exp_scaled(-fma(ops.xis[l][0], x[sl][0], fma(ops.xis[l][1], x[sl][1], x2s[sl])), mt);
+        e[(sl * L + l) * es] = el;
+        c[sl][0] = fma(ops.sens[0][l], el, c[sl][0]);
+        c[sl][1] = fma(ops.sens[1][l], el, c[sl][1]);
+        c[sl][2] = fma(ops.sens[2][l], el, c[sl][2]);
+      }
     }
-    const double r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
+    double r[NS][3], nn[NS][3];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        r[sl][k] = y[sl][k] - c[sl][k];
+        nn[sl][k] = 0.0;
+      }
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     // (s itself is not stored: write_spectra re-forms it for finished lanes)
-    double n0 = 0.0, n1 = 0.0, n2 = 0.0;
 #pragma unroll(KL > 0 ? kEmUnrollB : 2)
     for (int l = 0; l < L; ++l) {
-      const double s = clamp_eps(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, e[l * es]))), eps);
-      const double lg = log_tab(s, mt.logt);
-      n0 = fma(ops.fitm[0][l], lg, n0);
-      n1 = fma(ops.fitm[1][l], lg, n1);
-      n2 = fma(ops.fitm[2][l], lg, n2);
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const double sv = clamp_eps(
+            fma(ops.gain[l][2], r[sl][2], fma(ops.gain[l][1], r[sl][1], fma(ops.gain[l][0], r[sl][0], e[(sl * L + l) * es]))),
+            eps);
+        const double lg = log_tab(sv, mt.logt);
+        nn[sl][0] = fma(ops.fitm[0][l], lg, nn[sl][0]);
+        nn[sl][1] = fma(ops.fitm[1][l], lg, nn[sl][1]);
+        nn[sl][2] = fma(ops.fitm[2][l], lg, nn[sl][2]);
+      }
     }
-    n0 = -n0;
-    n1 = -n1;
-    n2 = -n2;
-    // ---- bookkeeping: stopping rule of bayes.py:195-205
-    bool done = false;
-    if (idx >= 0) {
-      ++nfit;
-      const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
-      const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
-      const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
-      done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters;
-      if (done) {
-        io.fits[idx] = nfit;
-        if (io.x) {
-          io.x[3 * idx] = n0;
-          io.x[3 * idx + 1] = n1;
-          io.x[3 * idx + 2] = n2;
+    // ---- bookkeeping: stopping rule of bayes.py:195-205, then write-out and refill
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const double n0 = -nn[sl][0], n1 = -nn[sl][1], n2 = -nn[sl][2];
+      bool done = false;
+      if (idx[sl] >= 0) {
+        ++nfit[sl];
+        const double d0 = n0 - x[sl][0], d1 = n1 - x[sl][1], d2 = n2 - x[sl][2];
+        const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+        const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x[sl][0], x[sl][0]), __dmul_rn(x[sl][1], x[sl][1])),
+                                     __dmul_rn(x[sl][2], x[sl][2]));
+        done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit[sl] >= ops.max_iters;
+        if (done) {
+          io.fits[idx[sl]] = nfit[sl];
+          if (io.x) {
+            io.x[3 * idx[sl]] = n0;
+            io.x[3 * idx[sl] + 1] = n1;
+            io.x[3 * idx[sl] + 2] = n2;
+          }
         }
       }
-    }
-    x0 = n0;
-    x1 = n1;
-    x2 = n2;
-    const unsigned m = __ballot_sync(0xffffffffu, done);
-    if (m) {
-      // ---- the whole warp streams the finished lanes' spectra (smem columns) out
-      write_spectra<KL, OUT>(io, e - lane, es, L, m, idx, lane, r0, r1, r2, gsm, eps);
-      // ---- refill finished lanes: rest of the current chunk, then a new one
-      const int need = __popc(m);
-      const int64_t avail = stop - next;  // warp-uniform
-      int64_t fresh = io.n, fresh_end = io.n;
-      if (avail < need && !exhausted) {
-        unsigned long long b = 0;
-        if (lane == 0) b = atomicAdd(io.work, (unsigned long long)kEmChunk);
-        fresh = dyn0 + (int64_t)__shfl_sync(0xffffffffu, b, 0);
-        fresh_end = min64(fresh + kEmChunk, io.n);
-        exhausted = fresh >= io.n;
-      }
-      if (done) {
-        const int r = __popc(m & lt_mask);
-        const int64_t mine = r < avail ? next + r : fresh + (r - avail);
-        idx = mine < (r < avail ? stop : fresh_end) ? mine : -1;
-        nfit = 1;
-        if (idx >= 0) load(idx);
-      }
-      if (avail < need) {
-        next = fresh_end > fresh ? min64(fresh + (need - avail), fresh_end) : fresh_end;
-        stop = fresh_end;
-      } else {
-        next += need;
+      x[sl][0] = n0;
+      x[sl][1] = n1;
+      x[sl][2] = n2;
+      const unsigned m = __ballot_sync(0xffffffffu, done);
+      if (m) {
+        // the whole warp streams the finished lanes' spectra out, then refills them
+        write_spectra<KL, OUT>(io, e - lane + sl * L * es, es, L, m, idx[sl], lane, r[sl][0], r[sl][1], r[sl][2], gsm,
+                               eps);
+        refill(sl, m, done);
       }
     }
   }
@@ -342,6 +385,7 @@ template <int KL, SpecOut OUT>
 inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (io.n <= 0) return OXM_OK;
   if (!io.fits || !io.xinit || !io.work) return OXM_ERR_ARGUMENT;
+  if ((io.y_soa != 0) != (OUT != SpecOut::kAosF64)) return OXM_ERR_ARGUMENT;  // see em_persistent_kernel
   io.fmt = OUT;
   const size_t smem = em_smem_bytes(ops.L, kEmThreads);
   auto kern = em_persistent_kernel<KL, OUT>;
@@ -357,7 +401,7 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (per_sm < 1) per_sm = 1;
   int64_t blocks = (int64_t)sms * per_sm;
   const int64_t need = ceil_div(io.n, kEmThreads);
-  if (blocks > need) blocks = need;
+  if (blocks > ceil_div(need, kEmSlots)) blocks = ceil_div(need, kEmSlots);
   if (!io.xinit_ready || ops.max_iters <= 1) {
     em_init_kernel<KL><<<(unsigned)need, kEmThreads, 0, s>>>(ops, io);
     int st0 = check_launch("em_init");
