@@ -329,10 +329,14 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   }
 }
 
-// fp64 recompute of the queued pixels: one warp per pixel, one band per lane
-// (the 26 band loads and logs of a pixel proceed in parallel), operators
-// staged in shared memory so the per-lane band index does not serialise
-// constant-bank reads; the three fit sums are warp-reduced.
+// fp64 recompute of the queued pixels (~0.4% of them): kFbLanes threads per
+// pixel, each taking every kFbLanes-th band, partial fit sums reduced with
+// two shuffles; grid-stride over the device-side count.  Each thread issues
+// its loads (rgb, ybar, its part of the hi/lo spectrum row) together and uses
+// the table log (~1 ulp; the argument is clamped at eps > 0 first, as the
+// reference does).  Operators are staged in shared memory by CTAs that have
+// work (the per-lane band index would serialise constant-bank reads).
+constexpr int kFbLanes = 4;
 template <typename Src>
 __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
                                                                  const Src frames, PxGeom g,
@@ -345,49 +349,60 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
                                                                  float* __restrict__ hbo, float* __restrict__ hb,
                                                                  float* __restrict__ off) {
   __shared__ double T[kMaxBands][3], F[3][kMaxBands];
+  constexpr int kPerCta = kFbThreads / kFbLanes;
+  const uint32_t cnt = *fb_count;
+  if ((int64_t)blockIdx.x * kPerCta >= cnt) return;  // whole CTA idle: skip the staging
   const int L = ops.L;
   for (int q = threadIdx.x; q < 3 * L; q += kFbThreads) {
     T[q / 3][q % 3] = ops.solve[q / 3][q % 3];
     F[q / L][q % L] = ops.fitm[q / L][q % L];
   }
   __syncthreads();
-  const uint32_t cnt = *fb_count;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = ((int64_t)gridDim.x * kFbThreads) >> 5;
-  const int64_t plane = g.H * g.W;
-  for (int64_t i = ((int64_t)blockIdx.x * kFbThreads + threadIdx.x) >> 5; i < cnt; i += warps) {
-    const int64_t p = fb_list[i];
-    const int64_t f = p / plane;
-    const int64_t rem = p - f * plane;
-    const int64_t row = rem / g.W, col = rem - row * g.W;
-    const int64_t bidx = (f * g.hL + (row >> g.n)) * g.wL + (col >> g.n);
-    const double D0 = frames.at(3 * p) - ybar[bidx];
-    const double D1 = frames.at(3 * p + 1) - ybar[g.nll + bidx];
-    const double D2 = frames.at(3 * p + 2) - ybar[2 * g.nll + bidx];
+  const int sub = threadIdx.x & (kFbLanes - 1);
+  // pixel indices are < 2^32 (checked at launch): 32-bit index arithmetic
+  const uint32_t plane = (uint32_t)(g.H * g.W), W = (uint32_t)g.W;
+  const double2* logt = log_table_global();
+  const int64_t stride = (int64_t)gridDim.x * kPerCta;
+  // the loop bound is uniform over each group of kFbLanes lanes (shuffles below)
+  for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride) {
+    const uint32_t p = fb_list[i];
+    const uint32_t f = p / plane;
+    const uint32_t rem = p - f * plane;
+    const uint32_t row = rem / W, col = rem - row * W;
+    const int64_t bidx = ((int64_t)f * g.hL + (row >> g.n)) * g.wL + (col >> g.n);
+    const double D0 = frames.at(3 * (int64_t)p) - ybar[bidx];
+    const double D1 = frames.at(3 * (int64_t)p + 1) - ybar[g.nll + bidx];
+    const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + bidx];
+    const float* hi = Shi + bidx * Lp;
+    const float* lo = Slo + bidx * Lp;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int l = lane; l < L; l += 32) {
-      const double S = (double)Shi[bidx * Lp + l] + (double)Slo[bidx * Lp + l];
+#pragma unroll 4
+    for (int l = sub; l < L; l += kFbLanes) {
+      const double S = (double)ldg(hi + l) + (double)ldg(lo + l);
       const double sp = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
-      const double lg = log(fmax(sp, ops.eps));
+      const double lg = log_tab(fmax(sp, ops.eps), logt);
       a0 = fma(F[0][l], lg, a0);
       a1 = fma(F[1][l], lg, a1);
       a2 = fma(F[2][l], lg, a2);
     }
+    const unsigned grp = __activemask();
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    for (int o = 1; o < kFbLanes; o <<= 1) {
+      a0 += __shfl_xor_sync(grp, a0, o);
+      a1 += __shfl_xor_sync(grp, a1, o);
+      a2 += __shfl_xor_sync(grp, a2, o);
     }
-    if (lane == 0) {
+    if (sub == 0) {
       const float xo = (float)(-a0 * g.cal), xd = (float)(-a1 * g.cal);
       const float co = fmaxf(xo, 0.f);
       const float t = co + fmaxf(xd, 0.f);
-      if (thb) thb[p] = t;
-      if (so2) so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
-      if (hbo) hbo[p] = xo;
-      if (hb) hb[p] = xd;
-      if (off) off[p] = (float)(-a2);
+      thb[p] = t;
+      so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
+      if (hbo) {
+        hbo[p] = xo;
+        hb[p] = xd;
+        off[p] = (float)(-a2);
+      }
     }
   }
 }
@@ -440,7 +455,7 @@ int level_dims(int64_t H, int64_t W, int n, LevelDims& d) {
 //   spectra  fp64 SoA S[l][i] (fp64 path), or fp32 Shi[i][Lp] then Slo[i][Lp]
 //            (fp32 path; Lp = L rounded up to 4 for 16-byte row loads)
 //   x_init   3 x nll double (fit #1),  fit counts  nll int32   (EM bookkeeping)
-//   fallback counter + EM chunk counter (256 B) + fallback list (batch*H*W uint32)   [fp32 path]
+//   fallback counter + EM chunk counter (256 B), fallback list (batch*H*W uint32)   [fp32 path]
 struct Workspace {
   double* ybar;
   double* S;
@@ -599,7 +614,7 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
   px_fallback_kernel<Src><<<148 * 32, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
-                                                     w.fb_list, thb, so2, hbo, hb, off);
+                                                        w.fb_list, thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
 }
 
