@@ -52,8 +52,12 @@ struct BandCount {
 };
 
 // Dynamic shared memory of an EM kernel: tables + G + one e column per thread.
+// The e columns are strided by threads + 1 doubles per band: rows (one band,
+// consecutive threads) stay contiguous, and a column (one thread, consecutive
+// bands -- write_spectra) walks the banks instead of hitting one bank 26 times.
 __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
-  return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands + sizeof(double) * (size_t)L * (size_t)threads * OXM_EM_SLOTS;
+  return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands +
+         sizeof(double) * (size_t)L * (size_t)(threads + 1) * OXM_EM_SLOTS;
 }
 
 // ---------------------------------------------------------------------------
@@ -222,7 +226,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   double(*gsm)[3] = reinterpret_cast<double(*)[3]>(smem_raw + sizeof(MathSmem));  // G, for write_spectra
   // e of slot s, band l at e[(s * L + l) * es]: one column per thread and slot
   double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem) + sizeof(ops.gain)) + threadIdx.x;
-  constexpr int es = kEmThreads;
+  constexpr int es = kEmThreads + 1;  // band stride of the e columns (see em_smem_bytes)
   load_math_tables(mt);
   for (int i = threadIdx.x; i < kMaxBands * 3; i += kEmThreads) gsm[i / 3][i % 3] = ops.gain[i / 3][i % 3];
   __syncthreads();
