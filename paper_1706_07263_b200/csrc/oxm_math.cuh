@@ -79,9 +79,15 @@ __device__ __forceinline__ double log_tab(const double x, const double2* __restr
   double q = fma(r, kLogB5, kLogB4);
   q = fma(q, r, kLogB3);
   q = fma(q, r, -0.5);  // log1p(r) - r = r^2 q
+#ifdef OXM_LOG_SPLIT_LN2
   const double ed = (double)e;
   const double h = fma(ed, kLn2I, cj.y);  // ed * kLn2I exact (20 x 11 bits)
   return h + (r + fma(q, r * r, ed * kLn2Lo20));
+#else
+  // e ln2 - ln c_j rounded once (<= 0.5 ulp of |log x| <= ~15), then + log1p(r)
+  const double h = fma((double)e, kLn2Hi, cj.y);
+  return h + fma(q, r * r, r);
+#endif
 }
 
 }  // namespace oxm
