@@ -51,10 +51,10 @@ __device__ __forceinline__ const double2* log_table_global() { return reinterpre
 
 // exp(zs * ln2/256) for a pre-scaled argument zs
 __device__ __forceinline__ double exp_scaled(const double zs, const MathSmem& t) {
-  const double magic = 6755399441055744.0;  // 1.5 * 2^52: round-to-nearest integer trick
-  const double km = zs + magic;
-  const int k = __double2loint(km);
-  const double rs = zs - (km - magic);  // exact
+  // round-to-nearest via F2I/I2F: conversions run on the XU pipe, which the
+  // EM leaves mostly idle, instead of two fp64 adds with a 1.5*2^52 shifter
+  const int k = __double2int_rn(zs);
+  const double rs = zs - (double)k;  // exact
   double q = fma(rs, kExpA4, kExpA3);
   q = fma(q, rs, kExpA2);
   q = fma(q, rs, kExpA1);
