@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kMaxLevels = 24;
 constexpr int kLlThreads = 128;
-constexpr int kPxCols = 128;  // pixel columns per CTA in the fp32 map kernel
+constexpr int kPxThreads = 128;  // threads per CTA in the fp32 map kernel (2 pixel columns each)
 constexpr int kFbThreads = 128;
 
 struct LevelDims {
@@ -178,34 +178,36 @@ __device__ __forceinline__ float lg2_approx(float v) {
   return r;
 }
 
-// fp32 map kernel.  CTA = kPxCols columns x R rows of one low-pass block row
-// of one frame; each thread owns one column and R rows and walks the bands
-// once, updating its R pixels per band (R independent MUFU/FMA chains).
-// Per band and pixel: 3 FFMA (solve d, started from the block spectrum), one
-// 3-input min per band pair (fallback detection), MUFU lg2, 2 FFMA (hbo, hb;
-// +1 for the offset plane when requested); the FFMAs of two rows issue as one
-// packed FFMA2.  No eps clamp: any pixel with a
+// fp32 map kernel.  CTA = kPxThreads threads x R rows of one low-pass block
+// row of one frame; each thread owns two adjacent columns (always in the same
+// low-pass block: n >= 1 and the first column is even) and R rows, and walks
+// the bands once, updating its 2R pixels per band.  The two columns of a row
+// form one float2 lane pair, so every FMA issues as a packed FFMA2.
+// Per band and pixel: 3 FMA (solve d, started from the block spectrum), one
+// 3-input min per band pair (fallback detection), MUFU lg2, 2 FMA (hbo, hb;
+// +1 for the offset plane when requested).  No eps clamp: any pixel with a
 // band below fallback_below (>= eps) is recomputed in fp64 by the fixup
 // kernel, which applies the reference's clamp.  The block spectrum row
 // Shi[coef][Lp] is read with 16-byte loads (Lp = L rounded up to 4), shared
-// through L1 by the 2^n threads of a block column.
+// through L1 by the threads of a block.
 template <int KL, int R, bool PLANES, typename Src>
-__global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__ DevOps ops,
-                                                         const Src frames, PxGeom g,
-                                                         const float* __restrict__ Shi, int Lp,
-                                                         const double* __restrict__ ybar, float* __restrict__ thb,
-                                                         float* __restrict__ so2, float* __restrict__ hbo,
-                                                         float* __restrict__ hb, float* __restrict__ off,
-                                                         uint32_t* __restrict__ fb_count, uint32_t* __restrict__ fb_list) {
+__global__ void __launch_bounds__(kPxThreads) px_f32_kernel(const __grid_constant__ DevOps ops,
+                                                            const Src frames, PxGeom g,
+                                                            const float* __restrict__ Shi, int Lp,
+                                                            const double* __restrict__ ybar, float* __restrict__ thb,
+                                                            float* __restrict__ so2, float* __restrict__ hbo,
+                                                            float* __restrict__ hb, float* __restrict__ off,
+                                                            uint32_t* __restrict__ fb_count, uint32_t* __restrict__ fb_list) {
   constexpr int LM = BandCount<KL>::kMax;
   const int L = BandCount<KL>::get(ops);
   const int64_t f = blockIdx.z;
-  const int64_t col = (int64_t)blockIdx.x * kPxCols + threadIdx.x;
-  const int bs = 1 << g.n;                    // rows per low-pass block
-  const int cpb = bs > R ? bs / R : 1;        // row chunks per block row
-  const int64_t by = blockIdx.y / cpb;
-  const int64_t row0 = by * bs + (int64_t)(blockIdx.y - by * cpb) * R;
+  const int64_t col = 2 * ((int64_t)blockIdx.x * kPxThreads + threadIdx.x);  // first of the two columns
+  const int bs = 1 << g.n;               // rows per low-pass block
+  const int cpb = bs > R ? bs / R : 1;   // row chunks per block row (a power of two)
+  const int64_t by = blockIdx.y >> (__ffs(cpb) - 1);
+  const int64_t row0 = by * bs + (int64_t)(blockIdx.y & (cpb - 1)) * R;
   if (col >= g.W) return;
+  const bool two = col + 1 < g.W;
   const int nrow = (int)min64(min64(R, g.H - row0), (int64_t)bs);
   const int64_t bidx = (f * g.hL + by) * g.wL + (col >> g.n);
 
@@ -217,39 +219,35 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
     yh[k] = __double2float_rn(yb[k]);
     yl[k] = __double2float_rn(yb[k] - (double)yh[k]);
   }
-  // rows are processed in pairs with packed FFMA2 (two fp32 FMAs per
-  // instruction; the per-band constants are pre-duplicated float2s in DevOps)
-  constexpr int P = R / 2;
-  float2 d[P][3], a0[P], a1[P], a2[P];
-  float vmin[R];
+  float2 d[R][3], a0[R], a1[R], a2[R];
+  float vmin[R][2];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + min(r, nrow - 1)) * g.W + col;
+    const int64_t p1 = two ? p + 1 : p;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      float v;
-      if constexpr (Src::kF32)
-        v = (frames.atf(3 * p + k) - yh[k]) - yl[k];  // exact-ish: rgb is an fp32 value
-      else
-        v = __double2float_rn(frames.at(3 * p + k) - yb[k]);  // decoded sample in fp64
-      if (r & 1)
-        d[r >> 1][k].y = v;
-      else
-        d[r >> 1][k].x = v;
+      if constexpr (Src::kF32) {
+        d[r][k].x = (frames.atf(3 * p + k) - yh[k]) - yl[k];  // exact-ish: rgb is an fp32 value
+        d[r][k].y = (frames.atf(3 * p1 + k) - yh[k]) - yl[k];
+      } else {
+        d[r][k].x = __double2float_rn(frames.at(3 * p + k) - yb[k]);  // decoded sample in fp64
+        d[r][k].y = __double2float_rn(frames.at(3 * p1 + k) - yb[k]);
+      }
     }
-    vmin[r] = 3.0e38f;
+    a0[r] = a1[r] = a2[r] = make_float2(0.f, 0.f);
+    vmin[r][0] = vmin[r][1] = 3.0e38f;
   }
-#pragma unroll
-  for (int q = 0; q < P; ++q) a0[q] = a1[q] = a2[q] = make_float2(0.f, 0.f);
-  auto spec = [&](int l, float sh, int q) {
-    return __ffma2_rn(ops.solve_f2[l][2], d[q][2],
-                      __ffma2_rn(ops.solve_f2[l][1], d[q][1], __ffma2_rn(ops.solve_f2[l][0], d[q][0], make_float2(sh, sh))));
+  // the per-band constants are pre-duplicated float2s in DevOps (FFMA2 operands)
+  auto spec = [&](int l, float sh, int r) {
+    return __ffma2_rn(ops.solve_f2[l][2], d[r][2],
+                      __ffma2_rn(ops.solve_f2[l][1], d[r][1], __ffma2_rn(ops.solve_f2[l][0], d[r][0], make_float2(sh, sh))));
   };
-  auto fit = [&](int l, float2 s, int q) {
+  auto fit = [&](int l, float2 s, int r) {
     const float2 lg = make_float2(lg2_approx(s.x), lg2_approx(s.y));
-    a0[q] = __ffma2_rn(ops.fitl2_f2[0][l], lg, a0[q]);
-    a1[q] = __ffma2_rn(ops.fitl2_f2[1][l], lg, a1[q]);
-    if constexpr (PLANES) a2[q] = __ffma2_rn(ops.fitl2_f2[2][l], lg, a2[q]);
+    a0[r] = __ffma2_rn(ops.fitl2_f2[0][l], lg, a0[r]);
+    a1[r] = __ffma2_rn(ops.fitl2_f2[1][l], lg, a1[r]);
+    if constexpr (PLANES) a2[r] = __ffma2_rn(ops.fitl2_f2[2][l], lg, a2[r]);
   };
   const float* sp = Shi + bidx * Lp;
   if constexpr (KL > 0 && KL % 2 == 0) {
@@ -263,13 +261,13 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
         const int l = 4 * qq + h;
         if (l < KL) {
 #pragma unroll
-          for (int q = 0; q < P; ++q) {
-            const float2 s0 = spec(l, vv[h], q);
-            const float2 s1 = spec(l + 1, vv[h + 1], q);
-            vmin[2 * q] = fminf(vmin[2 * q], fminf(s0.x, s1.x));
-            vmin[2 * q + 1] = fminf(vmin[2 * q + 1], fminf(s0.y, s1.y));
-            fit(l, s0, q);
-            fit(l + 1, s1, q);
+          for (int r = 0; r < R; ++r) {
+            const float2 s0 = spec(l, vv[h], r);
+            const float2 s1 = spec(l + 1, vv[h + 1], r);
+            vmin[r][0] = fminf(vmin[r][0], fminf(s0.x, s1.x));
+            vmin[r][1] = fminf(vmin[r][1], fminf(s0.y, s1.y));
+            fit(l, s0, r);
+            fit(l + 1, s1, r);
           }
         }
       }
@@ -280,11 +278,11 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
       if (KL == 0 && l >= L) break;
       const float sh = ldg(sp + l);
 #pragma unroll
-      for (int q = 0; q < P; ++q) {
-        const float2 s0 = spec(l, sh, q);
-        vmin[2 * q] = fminf(vmin[2 * q], s0.x);
-        vmin[2 * q + 1] = fminf(vmin[2 * q + 1], s0.y);
-        fit(l, s0, q);
+      for (int r = 0; r < R; ++r) {
+        const float2 s0 = spec(l, sh, r);
+        vmin[r][0] = fminf(vmin[r][0], s0.x);
+        vmin[r][1] = fminf(vmin[r][1], s0.y);
+        fit(l, s0, r);
       }
     }
   }
@@ -295,19 +293,32 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + r) * g.W + col;
     if (r < nrow) {
-      const float A0 = (r & 1) ? a0[r >> 1].y : a0[r >> 1].x;
-      const float A1 = (r & 1) ? a1[r >> 1].y : a1[r >> 1].x;
-      const float xo = A0 * cal, xd = A1 * cal;
-      const float co = fmaxf(xo, 0.f);
-      const float t = co + fmaxf(xd, 0.f);
-      thb[p] = t;
-      so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
-      if constexpr (PLANES) {
-        hbo[p] = xo;
-        hb[p] = xd;
-        off[p] = (r & 1) ? a2[r >> 1].y : a2[r >> 1].x;
+      const float2 xo = make_float2(a0[r].x * cal, a0[r].y * cal), xd = make_float2(a1[r].x * cal, a1[r].y * cal);
+      const float2 co = make_float2(fmaxf(xo.x, 0.f), fmaxf(xo.y, 0.f));
+      const float2 t = make_float2(co.x + fmaxf(xd.x, 0.f), co.y + fmaxf(xd.y, 0.f));
+      const float2 so = make_float2(t.x > 0.f ? __fdividef(co.x, t.x) : qnan_f(), t.y > 0.f ? __fdividef(co.y, t.y) : qnan_f());
+      if (two && (p & 1) == 0) {  // 8-byte aligned pair
+        *reinterpret_cast<float2*>(thb + p) = t;
+        *reinterpret_cast<float2*>(so2 + p) = so;
+      } else {
+        thb[p] = t.x;
+        so2[p] = so.x;
+        if (two) {
+          thb[p + 1] = t.y;
+          so2[p + 1] = so.y;
+        }
       }
-      any_fb |= !(vmin[r] >= thr);  // also catches NaN
+      if constexpr (PLANES) {
+        hbo[p] = xo.x;
+        hb[p] = xd.x;
+        off[p] = a2[r].x;
+        if (two) {
+          hbo[p + 1] = xo.y;
+          hb[p + 1] = xd.y;
+          off[p + 1] = a2[r].y;
+        }
+      }
+      any_fb |= !(vmin[r][0] >= thr) || (two && !(vmin[r][1] >= thr));  // also catches NaN
     }
   }
   // cancellation guard: queue pixels for the fp64 fixup kernel (rare)
@@ -316,14 +327,18 @@ __global__ void __launch_bounds__(kPxCols) px_f32_kernel(const __grid_constant__
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const bool need = r < nrow && !(vmin[r] >= thr);
-      const unsigned m = __ballot_sync(active, need);
-      if (m) {
-        const int leader = __ffs(m) - 1;
-        uint32_t base = 0;
-        if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
-        base = __shfl_sync(active, base, leader);
-        if (need) fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const bool need = r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr);
+        const unsigned m = __ballot_sync(active, need);
+        if (m) {
+          const int leader = __ffs(m) - 1;
+          uint32_t base = 0;
+          if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
+          base = __shfl_sync(active, base, leader);
+          if (need)
+            fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col + c);
+        }
       }
     }
   }
@@ -588,11 +603,10 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
 template <int KL, bool PLANES, typename Src>
 void launch_px_rows(const DevOps& ops, const Src& frames, const PxGeom& g, dim3 grid, int R, const Workspace& w,
                     float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
-  switch (R) {
-    case 2: px_f32_kernel<KL, 2, PLANES, Src><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    case 4: px_f32_kernel<KL, 4, PLANES, Src><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-    default: px_f32_kernel<KL, 8, PLANES, Src><<<grid, kPxCols, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list); break;
-  }
+  if (R == 2)
+    px_f32_kernel<KL, 2, PLANES, Src><<<grid, kPxThreads, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list);
+  else
+    px_f32_kernel<KL, 4, PLANES, Src><<<grid, kPxThreads, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list);
 }
 
 template <int KL, typename Src>
@@ -603,9 +617,9 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
   const bool planes = hbo || hb || off;
   if (planes && !(hbo && hb && off)) return OXM_ERR_ARGUMENT;
   const int bs = 1 << g.n;
-  const int R = bs >= 8 ? 8 : bs;
+  const int R = bs >= 4 ? 4 : bs;
   const int64_t cpb = bs > R ? bs / R : 1;
-  dim3 grid((unsigned)ceil_div(g.W, kPxCols), (unsigned)(g.hL * cpb), (unsigned)batch);
+  dim3 grid((unsigned)ceil_div(g.W, 2 * kPxThreads), (unsigned)(g.hL * cpb), (unsigned)batch);
   if (g.hL * cpb > 65535 || batch > 65535) return OXM_ERR_ARGUMENT;
   if (planes)
     launch_px_rows<KL, true>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
