@@ -227,6 +227,13 @@ OXM_API int oxm_pack_hwc3_f32(const float* a, const float* b, const float* c, in
 OXM_API int oxm_probe_fp64_fma(int blocks, int iters, double* sink, double* ops_per_launch, void* stream);
 OXM_API int oxm_probe_mufu_lg2(int blocks, int iters, float* sink, double* ops_per_launch, void* stream);
 
+/* Self-test of the EM's table-driven fp64 transcendentals (oxm_math.cuh):
+ * out[i] = exp(in[i] * ln2/256) (which == 0: the EM's pre-scaled argument,
+ * |in| < 2.5e5) or log(in[i]) (which == 1, in > 0 normal), evaluated exactly
+ * as the EM kernels do.  For accuracy tests against a high-precision
+ * reference; not on the hot path. */
+OXM_API int oxm_selftest_math(const double* in, int64_t n, int which, double* out, void* stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -104,6 +104,7 @@ _SIGNATURES = {
     "oxm_pack_hwc3_f32": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "oxm_probe_fp64_fma": (_i32, [_i32, _i32, _vp, _vp, _vp]),
     "oxm_probe_mufu_lg2": (_i32, [_i32, _i32, _vp, _vp, _vp]),
+    "oxm_selftest_math": (_i32, [_vp, _i64, _i32, _vp, _vp]),
 }
 
 _lock = threading.Lock()

@@ -6,6 +6,7 @@
 // chains per thread (enough ILP to cover the pipe latency at full occupancy)
 // so bench.py can report achieved / measured-peak for them.
 #include "oxm_common.cuh"
+#include "oxm_math.cuh"
 
 namespace oxm {
 namespace {
@@ -47,6 +48,16 @@ __global__ void __launch_bounds__(kProbeThreads) mufu_lg2_probe(int iters, float
   if (s == 12345.678f) sink[threadIdx.x] = s;
 }
 
+__global__ void __launch_bounds__(kProbeThreads) math_selftest_kernel(const double* __restrict__ in, int64_t n,
+                                                                        int which, double* __restrict__ out) {
+  __shared__ MathSmem mt;
+  load_math_tables(mt);
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kProbeThreads + threadIdx.x;
+  if (i >= n) return;
+  out[i] = which == 0 ? exp_scaled(in[i], mt) : log_tab(in[i], mt.logt);
+}
+
 }  // namespace
 }  // namespace oxm
 
@@ -64,4 +75,11 @@ extern "C" int oxm_probe_mufu_lg2(int blocks, int iters, float* sink, double* op
   mufu_lg2_probe<<<blocks, kProbeThreads, 0, as_stream(stream)>>>(iters, sink);
   if (ops) *ops = (double)blocks * kProbeThreads * (double)iters * 16.0 * 8.0;
   return check_launch("probe_mufu_lg2");
+}
+
+extern "C" int oxm_selftest_math(const double* in, int64_t n, int which, double* out, void* stream) {
+  if (n < 0 || (which != 0 && which != 1) || (n > 0 && (!in || !out))) return OXM_ERR_ARGUMENT;
+  if (n == 0) return OXM_OK;
+  math_selftest_kernel<<<grid_1d(n, kProbeThreads), kProbeThreads, 0, as_stream(stream)>>>(in, n, which, out);
+  return check_launch("selftest_math");
 }

@@ -262,3 +262,43 @@ def test_fit_fp32_kernel(cuda, rng, basis):
     got = fit_device(torch.from_numpy(cube).to(cuda), ops).cpu().numpy()
     want = O.fit_cube(cube.astype(np.float64)[None], basis.xi)[0]
     assert np.max(np.abs(got[:, :2] - want[:, :2])) <= 1e-4 * np.max(np.abs(want[:, :2]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["exp", "log"])
+def test_table_transcendentals_ulp(which):
+    """The EM's table-driven exp/log (oxm_math.cuh) against a high-precision
+    reference over the EM's argument range: exp of the pre-scaled argument
+    zs (e = exp(zs ln2/256)) within 1.1 ulp; log within 1.5 ulp of max(|log x|, 1)
+    absolute (the fit sums x = -F log s accumulate absolute errors)."""
+    import ctypes
+    from decimal import Decimal, getcontext
+
+    from paper_1706_07263_b200 import _native
+
+    getcontext().prec = 40
+    rng = np.random.default_rng(7)
+    if which == "exp":  # zs = -xi x * 256/ln2 for spectra in [eps, ~1], plus margin
+        x = np.concatenate([rng.uniform(-15000.0, 2000.0, 20000), np.linspace(-3.0, 3.0, 2001)])
+        c = Decimal(2).ln() / 256
+        ref = np.array([float((Decimal(float(v)) * c).exp()) for v in x])
+        ref_hp = [(Decimal(float(v)) * c).exp() for v in x]
+    else:  # clamped spectra s >= eps: [1e-6, 10], log-uniform, plus values near 1
+        x = np.concatenate([np.exp(rng.uniform(np.log(1e-6), np.log(10.0), 20000)), 1.0 + np.linspace(-1e-3, 1e-3, 2001)])
+        ref_hp = [Decimal(float(v)).ln() for v in x]
+        ref = np.array([float(v) for v in ref_hp])
+    dev = torch.device("cuda", 0)
+    xin = torch.from_numpy(x).to(dev)
+    out = torch.empty_like(xin)
+    st = _native.load().oxm_selftest_math(ctypes.c_void_p(xin.data_ptr()), x.size, 0 if which == "exp" else 1,
+                                          ctypes.c_void_p(out.data_ptr()), None)
+    _native.check(st, "selftest_math")
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    err = np.array([float(abs(Decimal(float(g)) - h)) for g, h in zip(got, ref_hp)])
+    if which == "exp":
+        ulps = err / np.spacing(np.abs(ref))
+        assert ulps.max() <= 1.1, (ulps.max(), x[np.argmax(ulps)])
+    else:
+        ulps = err / np.spacing(np.maximum(np.abs(ref), 1.0))
+        assert ulps.max() <= 1.5, (ulps.max(), x[np.argmax(ulps)])
