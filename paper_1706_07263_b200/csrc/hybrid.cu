@@ -191,7 +191,10 @@ __device__ __forceinline__ float lg2_approx(float v) {
 // Shi[coef][Lp] is read with 16-byte loads (Lp = L rounded up to 4), shared
 // through L1 by the threads of a block.
 template <int KL, int R, bool PLANES, typename Src>
-__global__ void __launch_bounds__(kPxThreads) px_f32_kernel(const __grid_constant__ DevOps ops,
+#ifndef OXM_PX_MIN_BLOCKS
+#define OXM_PX_MIN_BLOCKS 7
+#endif
+__global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(const __grid_constant__ DevOps ops,
                                                             const Src frames, PxGeom g,
                                                             const float* __restrict__ Shi, int Lp,
                                                             const double* __restrict__ ybar, float* __restrict__ thb,
