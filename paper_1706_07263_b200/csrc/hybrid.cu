@@ -697,12 +697,16 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s, reserve))) return st;
   mark(ev, 2, s);
   if (stream_px) {  // split launch: the per-pixel stage runs on its own stream after the EM
-    cudaEvent_t em_done;
-    cudaEventCreateWithFlags(&em_done, cudaEventDisableTiming);
-    cudaEventRecord(em_done, s);
+    cudaEvent_t em_done = nullptr;
+    cudaError_t err = cudaEventCreateWithFlags(&em_done, cudaEventDisableTiming);
+    if (err == cudaSuccess) err = cudaEventRecord(em_done, s);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(as_stream(stream_px), em_done, 0);
+    if (em_done) cudaEventDestroy(em_done);  // released once it has completed
+    if (err != cudaSuccess) {
+      set_last_error("split launch event", err);
+      return OXM_ERR_CUDA;
+    }
     s = as_stream(stream_px);
-    cudaStreamWaitEvent(s, em_done, 0);
-    cudaEventDestroy(em_done);  // released once it has completed
   }
   PxGeom g{height, width, d.h[n_levels], d.w[n_levels], nll, n_levels, calibration};
   if (ctx->ops.L == 26)

@@ -393,11 +393,16 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
   io.fmt = OUT;
   const size_t smem = em_smem_bytes(ops.L, kEmThreads);
   auto kern = em_persistent_kernel<KL, OUT>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t err = cudaSuccess;
+  if (smem > 48 * 1024) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEmThreads, smem);
+  if (err == cudaSuccess) err = cudaGetDevice(&dev);
+  if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEmThreads, smem);
+  if (err != cudaSuccess) {
+    set_last_error("em launch configuration", err);
+    return OXM_ERR_CUDA;
+  }
   if (sms < 1) sms = 1;
   // leave `em_reserve` CTA slots per SM free so a concurrent per-pixel kernel
   // (split launch, other stream) can co-reside with the persistent EM
