@@ -1,8 +1,9 @@
 """Batched throughput API for video: THb / SO2 maps for many frames per launch.
 
 ``HybridMapEngine.run`` is the device-resident path benchmarked as ``value``
-(frames already in HBM): three kernels per batch (low-pass chain, EM, fused
-per-pixel map).  ``HybridMapEngine.maps_from_host`` is the end-to-end path
+(frames already in HBM): five launches per batch (counter reset, low-pass chain
+with the EM start fit, persistent EM, fused per-pixel map, fp64 fixup of the
+flagged pixels).  ``HybridMapEngine.maps_from_host`` is the end-to-end path
 (``e2e``): pinned host frames -> H2D -> kernels -> D2H of the maps, chunked
 over three streams so copies in both directions overlap the compute.
 
@@ -55,7 +56,8 @@ class MapBatch:
 class HybridMapEngine:
     """Hybrid estimator for (B, H, W, 3) float32 frame batches on one GPU."""
 
-    KERNELS_PER_RUN = 3  # ll_kernel, em_soa_kernel, px_f32_kernel
+    # zero_counters, ll_kernel (+ EM fit #1), em_persistent_kernel, px_f32_kernel, px_fallback_kernel
+    KERNELS_PER_RUN = 5
 
     def __init__(
         self,
@@ -104,6 +106,10 @@ class HybridMapEngine:
     def launch(self, frames: torch.Tensor, out: MapBatch, *, stream: torch.cuda.Stream | None = None,
                stage_events=None, scale: float = 1.0, big_endian: bool = True) -> None:
         """Enqueue the hybrid kernels on ``stream``; no host synchronisation.
+
+        The engine owns one workspace (intermediates and the EM / fallback
+        counters): launches on different streams must not overlap in time --
+        use one engine per concurrent stream.
 
         ``frames``: CUDA (B, H, W, 3) float32 values, or uint16 PPM counts
         (sample = count * ``scale``; ``big_endian`` as stored in the file)."""
