@@ -440,12 +440,12 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-# fp64 flops per EM fit of this implementation's formulation:
-# per band 62 (exp arg 4, table exp 20, C e 6, e + G r 6, table log 20, fit 6)
-# x 26 bands + 16 per step; the spectra kernel adds 36 per band per coefficient.
+# EM work model, a fixed convention independent of the code's
+# current op counts: per band 22 arithmetic flops (exp arg 4, C e 6, e + G r 6,
+# fit 6) + 20 per fp64 exp and per log, x 26 bands, + 16 per step.
 FLOPS_PER_FIT = 62 * 26 + 16
-FLOPS_INIT = 32 * 26   # fit #1: solve y 6, table log 20, fit 6 per band (fused into ll_kernel)
-# kernels launched per step: zero_u32, ll (+ fit #1), em_persistent, px, fallback
+FLOPS_INIT = 32 * 26   # fit #1: solve y 6, log 20, fit 6 per band (fused into ll_kernel)
+# kernels launched per step: zero_counters, ll (+ fit #1), em_persistent, px, fallback
 HybridMapLaunches = 5
 
 
