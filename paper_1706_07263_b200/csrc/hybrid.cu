@@ -36,7 +36,10 @@ namespace {
 
 constexpr int kMaxLevels = 24;
 constexpr int kLlThreads = 128;
-constexpr int kPxThreads = 128;  // threads per CTA in the fp32 map kernel (2 pixel columns each)
+#ifndef OXM_PX_THREADS
+#define OXM_PX_THREADS 64
+#endif
+constexpr int kPxThreads = OXM_PX_THREADS;  // threads per CTA in the fp32 map kernel (2 pixel columns each)
 constexpr int kFbThreads = 128;
 
 struct LevelDims {
@@ -192,7 +195,7 @@ __device__ __forceinline__ float lg2_approx(float v) {
 // through L1 by the threads of a block.
 template <int KL, int R, bool PLANES, typename Src>
 #ifndef OXM_PX_MIN_BLOCKS
-#define OXM_PX_MIN_BLOCKS 7
+#define OXM_PX_MIN_BLOCKS 14
 #endif
 __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(const __grid_constant__ DevOps ops,
                                                             const Src frames, PxGeom g,
@@ -620,7 +623,10 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
   const bool planes = hbo || hb || off;
   if (planes && !(hbo && hb && off)) return OXM_ERR_ARGUMENT;
   const int bs = 1 << g.n;
-  const int R = bs >= 4 ? 4 : bs;
+#ifndef OXM_PX_ROWS
+#define OXM_PX_ROWS 4
+#endif
+  const int R = bs >= OXM_PX_ROWS ? OXM_PX_ROWS : bs;
   const int64_t cpb = bs > R ? bs / R : 1;
   dim3 grid((unsigned)ceil_div(g.W, 2 * kPxThreads), (unsigned)(g.hL * cpb), (unsigned)batch);
   if (g.hL * cpb > 65535 || batch > 65535) return OXM_ERR_ARGUMENT;
