@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define OXM_ABI_VERSION 1
+#define OXM_ABI_VERSION 2
 #define OXM_MAX_BANDS 64 /* spectral bands L supported by the kernels */
 
 /* Status codes; the Python host maps them onto the reference exception
@@ -93,6 +93,17 @@ OXM_API const char* oxm_last_error(void);
  * bayes.py:239-240 (done once per (sensitivity, basis, config)). */
 OXM_API int oxm_ctx_create(int device, const oxm_operators* ops, oxm_ctx** out);
 OXM_API int oxm_ctx_destroy(oxm_ctx* ctx);
+/* EM precision schedule of the fp32 map path (oxm_hybrid_maps_f32/_u16/_split).
+ * ratio > 1: fits run in fp32 while rel > ratio * rel_tol, then in fp64; a
+ * fp64 step with |rel/rel_tol - 1| < guard (or reaching max_iters) redoes
+ * its coefficient in fp64 from fit #1.  ratio <= 1: all fits in fp64.
+ * exact_below > 0: low-pass blocks holding a fallback pixel with a band below
+ * it are re-estimated all-fp64 before the fp64 pixel fallback (their
+ * cancellation would amplify the schedule's ~1e-8 spectrum deviation);
+ * 0 = never.  Default (16, 0.01, ops.fallback_below).  The drop-in fp64 entry
+ * points are always all-fp64.  Not thread-safe against concurrent launches on
+ * the same context. */
+OXM_API int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, double exact_below);
 
 /* ---- K1: multi-level Haar forward ---------------------------------------
  * Replaces haar.forward (haar.py:120-142) incl. per-level edge replication
@@ -163,14 +174,23 @@ OXM_API int oxm_expected_spectrum_f64(const oxm_ctx* ctx, const double* x, int64
  * with LL_n the recursively edge-replicated low-pass (haar.py:80-101) and
  * S = the EM spectra of LL_n / 2^n (bayes.py:185-207).
  * Workspace: oxm_hybrid_workspace_bytes(); any output pointer may be NULL.
- * f32 variant: fp64 low-pass chain + fp64 EM, fp32 per-pixel stage with an
- * fp64 recompute of pixels whose smallest band < ops.fallback_below.
+ * f32 variant: fp64 low-pass chain, EM with an fp32 lead-in and an fp64
+ * tail (fit counts bit-exact, spectra ~1e-8 relative of all-fp64; see
+ * oxm_ctx_set_em_lead), fp32 per-pixel stage with an fp64 recompute of
+ * pixels whose smallest band < ops.fallback_below.
  * Outputs are planar (batch, H, W); fits is (batch, ceil(H/2^n), ceil(W/2^n)).
- * stage_events: NULL, or 4 cudaEvent_t recorded on `stream` before the
- * low-pass kernel, before the EM kernel, before the per-pixel kernel and after
- * it (live per-kernel timing for the roofline report). */
+ * stage_events: NULL, or 5 cudaEvent_t recorded on `stream` before the
+ * low-pass kernel, before the EM's fp32 lead-in, before its fp64 kernel,
+ * before the per-pixel kernel and after it (live per-kernel timing for the
+ * roofline report; with no lead-in, events 1 and 2 coincide). */
 OXM_API size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, int64_t height,
                                   int64_t width, int n_levels);
+/* EM work counters of the last fp32-map launch that used `workspace` (same
+ * geometry): out[0] fp32 fits of the lead-in, out[1] fp64 fits of the tail,
+ * out[2] tail restarts in exact mode, out[3] low-pass blocks re-estimated
+ * all-fp64 for the fp64 pixel fallback.  Synchronises `stream`. */
+OXM_API int oxm_hybrid_em_counters(const oxm_ctx* ctx, void* workspace, int64_t batch, int64_t height,
+                                   int64_t width, int n_levels, uint64_t* out, void* stream);
 OXM_API int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,
                         int64_t width, int n_levels, double calibration, void* workspace,
                         size_t workspace_bytes, float* thb, float* so2, float* hbo, float* hb,

@@ -70,6 +70,7 @@ _SIGNATURES = {
     "oxm_last_error": (ctypes.c_char_p, []),
     "oxm_ctx_create": (_i32, [_i32, ctypes.POINTER(Operators), ctypes.POINTER(_vp)]),
     "oxm_ctx_destroy": (_i32, [_vp]),
+    "oxm_ctx_set_em_lead": (_i32, [_vp, _f64, _f64, _f64]),
     "oxm_haar_layout": (_i32, [_i64, _i64, _i32, _vp, _vp]),
     "oxm_haar_forward_f32": (_i32, [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
     "oxm_haar_forward_f64": (_i32, [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
@@ -83,6 +84,7 @@ _SIGNATURES = {
     "oxm_fit_f64": (_i32, [_vp, _vp, _i64, _f64, _vp, _vp, _vp, _vp]),
     "oxm_expected_spectrum_f64": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "oxm_hybrid_workspace_bytes": (ctypes.c_size_t, [_vp, _i64, _i64, _i64, _i32]),
+    "oxm_hybrid_em_counters": (_i32, [_vp, _vp, _i64, _i64, _i64, _i32, _vp, _vp]),
     "oxm_hybrid_maps_f32": (
         _i32,
         [_vp, _vp, _i64, _i64, _i64, _i32, _f64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],

@@ -17,6 +17,21 @@ void set_last_error(const char* where, cudaError_t err) {
                 cudaGetErrorName(err));
 }
 
+namespace {
+// fp32 lead-in defaults (tools/em_lead_sweep.py): hand over to
+// fp64 once rel <= 16 tol; redo in fp64 when a tail step has |rel/tol - 1| < 1%
+constexpr double kDefaultLeadRatio = 16.0;
+constexpr double kDefaultLeadGuard = 0.01;
+
+void set_em_lead(DevOps& d, double ratio, double guard, double exact_below) {
+  d.exact_below = exact_below;
+  const double kt = ratio * d.rel_tol;
+  d.lead_thr_f = ratio > 1.0 ? static_cast<float>(kt * kt) : 0.0f;
+  d.guard_lo = (1.0 - guard) * (1.0 - guard) * d.rel_tol * d.rel_tol;
+  d.guard_hi = (1.0 + guard) * (1.0 + guard) * d.rel_tol * d.rel_tol;
+}
+}  // namespace
+
 }  // namespace oxm
 
 using namespace oxm;
@@ -82,6 +97,16 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
       d.fitl2_f2[k][l] = make_float2(d.fitl2_f[k][l], d.fitl2_f[k][l]);
     }
   }
+  const double log2e = 1.44269504088896340736;
+  for (int l = 0; l < L; ++l) {
+    d.xl2_f[l][0] = static_cast<float>(-log2e * d.xi[l][0]);
+    d.xl2_f[l][1] = static_cast<float>(-log2e * d.xi[l][1]);
+    for (int k = 0; k < 3; ++k) {
+      d.sens_f[k][l] = static_cast<float>(d.sens[k][l]);
+      d.gain_f[l][k] = static_cast<float>(d.gain[l][k]);
+    }
+  }
+  set_em_lead(d, kDefaultLeadRatio, kDefaultLeadGuard, d.fallback_below);
   for (int l = 0; l < L; ++l) {
     d.xis[l][0] = d.xi[l][0] * kExpScale;
     d.xis[l][1] = d.xi[l][1] * kExpScale;
@@ -100,6 +125,13 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
         return OXM_ERR_NUMERICAL;
       }
   *out = c;
+  return OXM_OK;
+}
+
+extern "C" int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, double exact_below) {
+  if (!ctx || !(ratio >= 0.0) || !(guard >= 0.0 && guard < 1.0) || !(exact_below >= 0.0)) return OXM_ERR_ARGUMENT;
+  if (ratio > 1.0 && (ratio * ctx->ops.rel_tol >= 1.0 || guard <= 0.0)) return OXM_ERR_ARGUMENT;
+  set_em_lead(ctx->ops, ratio, guard, exact_below);
   return OXM_OK;
 }
 

@@ -41,6 +41,7 @@ constexpr int kLlThreads = 128;
 #endif
 constexpr int kPxThreads = OXM_PX_THREADS;  // threads per CTA in the fp32 map kernel (2 pixel columns each)
 constexpr int kFbThreads = 128;
+constexpr uint32_t kExactTag = 0x80000000u;  // fallback-list entry flag: re-estimate the block all-fp64
 
 struct LevelDims {
   int n;
@@ -105,7 +106,7 @@ template <typename Src, int NLV, bool OUT_YBAR>
 __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ DevOps ops, const Src frames,
                                                         int64_t batch, LevelDims d, double* __restrict__ out,
                                                         int64_t nll, int scale_exp, uint32_t* flags,
-                                                        double* __restrict__ xinit) {
+                                                        double* __restrict__ xinit, uint8_t* __restrict__ blkflag) {
   const int64_t idx = (int64_t)blockIdx.x * kLlThreads + threadIdx.x;
   if (idx >= nll) return;
   const int64_t hL = d.h[NLV], wL = d.w[NLV];
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
   }
   if (flags && (bad || neg)) atomicOr(flags, (bad ? OXM_FLAG_NONFINITE : 0u) | (neg ? OXM_FLAG_NEGATIVE_LL : 0u));
   if constexpr (OUT_YBAR) {
+    if (blkflag) blkflag[idx] = 0;  // exact-block marks of this launch (mark_exact_blocks)
     // fit #1 of the EM (bayes.py:241-250) while the frame streams in
     if (xinit) {
       double x0, x1, x2;
@@ -174,12 +176,6 @@ struct PxGeom {
   int n;
   double cal;
 };
-
-__device__ __forceinline__ float lg2_approx(float v) {
-  float r;
-  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
-  return r;
-}
 
 // fp32 map kernel.  CTA = kPxThreads threads x R rows of one low-pass block
 // row of one frame; each thread owns two adjacent columns (always in the same
@@ -294,6 +290,7 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   }
   const float cal = (float)g.cal;
   const float thr = (float)ops.fallback_below;
+  const float ethr = (float)ops.exact_below;
   bool any_fb = false;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -342,8 +339,10 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
           uint32_t base = 0;
           if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
           base = __shfl_sync(active, base, leader);
+          // top bit: the block's spectrum must be the all-fp64 one (mark_exact_blocks)
           if (need)
-            fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col + c);
+            fb_list[base + __popc(m & ((1u << lane) - 1u))] =
+                (uint32_t)((f * g.H + row0 + r) * g.W + col + c) | (vmin[r][c] >= ethr ? 0u : kExactTag);
         }
       }
     }
@@ -386,7 +385,7 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   const int64_t stride = (int64_t)gridDim.x * kPerCta;
   // the loop bound is uniform over each group of kFbLanes lanes (shuffles below)
   for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride) {
-    const uint32_t p = fb_list[i];
+    const uint32_t p = fb_list[i] & ~kExactTag;
     const uint32_t f = p / plane;
     const uint32_t rem = p - f * plane;
     const uint32_t row = rem / W, col = rem - row * W;
@@ -485,8 +484,16 @@ struct Workspace {
   int Lp;
   double* xinit;
   int32_t* fits;
+  int32_t* fits_out;              // the fit counts the EM writes: the caller's array, or `fits`
+  float* xh;                      // EM hand-over state of the fp32 lead-in, [3][nll]
   uint32_t* fb_count;
-  unsigned long long* em_work;  // EM chunk counter (same 256-byte block as fb_count)
+  unsigned long long* em_work;    // EM chunk counter (same 256-byte block as fb_count)
+  unsigned long long* lead_work;  // lead-in chunk counter (same block)
+  unsigned long long* em_stats;   // [3] EM work counters (same block, EmIO::stats)
+  unsigned long long* sel_work;   // chunk counter of the exact-block EM pass (same block)
+  uint32_t* blk_count;            // number of exact blocks (same block)
+  uint8_t* blk_flag;              // [nll] block marked for the exact pass (zeroed by ll_kernel)
+  uint32_t* blk_list;             // [nll] marked blocks
   uint32_t* fb_list;
 };
 
@@ -497,8 +504,9 @@ inline int padded_bands(int L) { return (L + 3) & ~3; }
 size_t workspace_bytes(int L, int64_t nll, int64_t npx) {
   return 256 + align256(sizeof(double) * 3 * (size_t)nll) +
          align256(sizeof(double) * (size_t)padded_bands(L) * (size_t)nll) +
-         align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) + 256 +
-         align256(sizeof(uint32_t) * (size_t)npx);
+         align256(sizeof(double) * 3 * (size_t)nll) + align256(sizeof(int32_t) * (size_t)nll) +
+         align256(sizeof(float) * 3 * (size_t)nll) + align256((size_t)nll) + align256(sizeof(uint32_t) * (size_t)nll) +
+         256 + align256(sizeof(uint32_t) * (size_t)npx);
 }
 
 Workspace carve(void* ws, int L, int64_t nll) {
@@ -514,9 +522,20 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.xinit = reinterpret_cast<double*>(p);
   p += align256(sizeof(double) * 3 * (size_t)nll);
   w.fits = reinterpret_cast<int32_t*>(p);
+  w.fits_out = w.fits;
   p += align256(sizeof(int32_t) * (size_t)nll);
+  w.xh = reinterpret_cast<float*>(p);
+  p += align256(sizeof(float) * 3 * (size_t)nll);
+  w.blk_flag = reinterpret_cast<uint8_t*>(p);
+  p += align256((size_t)nll);
+  w.blk_list = reinterpret_cast<uint32_t*>(p);
+  p += align256(sizeof(uint32_t) * (size_t)nll);
   w.fb_count = reinterpret_cast<uint32_t*>(p);
   w.em_work = reinterpret_cast<unsigned long long*>(p + 128);
+  w.lead_work = reinterpret_cast<unsigned long long*>(p + 192);
+  w.em_stats = reinterpret_cast<unsigned long long*>(p + 8);
+  w.blk_count = reinterpret_cast<uint32_t*>(p + 4);
+  w.sel_work = reinterpret_cast<unsigned long long*>(p + 200);
   w.fb_list = reinterpret_cast<uint32_t*>(p + 256);
   return w;
 }
@@ -524,12 +543,12 @@ Workspace carve(void* ws, int L, int64_t nll) {
 // zeroes the fallback counter as part of the low-pass launch (no memset node)
 template <typename Src, bool OUT_YBAR>
 void launch_ll_pass(const DevOps& ops, const Src& src, int64_t batch, const LevelDims& d, int nlv, double* out,
-                    int64_t count, int scale_exp, uint32_t* flags, double* xinit, cudaStream_t s) {
+                    int64_t count, int scale_exp, uint32_t* flags, double* xinit, uint8_t* blkflag, cudaStream_t s) {
   const unsigned grid = grid_1d(count, kLlThreads);
   switch (nlv) {
-    case 1: ll_kernel<Src, 1, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit); break;
-    case 2: ll_kernel<Src, 2, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit); break;
-    default: ll_kernel<Src, 3, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit); break;
+    case 1: ll_kernel<Src, 1, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit, blkflag); break;
+    case 2: ll_kernel<Src, 2, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit, blkflag); break;
+    default: ll_kernel<Src, 3, OUT_YBAR><<<grid, kLlThreads, 0, s>>>(ops, src, batch, d, out, count, scale_exp, flags, xinit, blkflag); break;
   }
 }
 
@@ -538,10 +557,10 @@ void launch_ll_pass(const DevOps& ops, const Src& src, int64_t batch, const Leve
 // ybar.  The add order per level is the reference's in every pass.
 template <typename Src>
 int launch_ll(const DevOps& ops, const Src& frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll,
-              uint32_t* flags, double* xinit, cudaStream_t s) {
+              uint32_t* flags, double* xinit, uint8_t* blkflag, cudaStream_t s) {
   const int n = d.n;
   if (n <= 3) {
-    launch_ll_pass<Src, true>(ops, frames, batch, d, n, ybar, nll, n, flags, xinit, s);
+    launch_ll_pass<Src, true>(ops, frames, batch, d, n, ybar, nll, n, flags, xinit, blkflag, s);
     return check_launch("hybrid_ll");
   }
   double* prev = nullptr;
@@ -567,11 +586,11 @@ int launch_ll(const DevOps& ops, const Src& frames, int64_t batch, const LevelDi
       }
     }
     if (done == 0)
-      launch_ll_pass<Src, false>(ops, frames, batch, dp, nl, next, count, 0, flags, nullptr, s);
+      launch_ll_pass<Src, false>(ops, frames, batch, dp, nl, next, count, 0, flags, nullptr, nullptr, s);
     else if (last)
-      launch_ll_pass<PlainSrc<double>, true>(ops, PlainSrc<double>{prev}, batch, dp, nl, ybar, count, n, flags, xinit, s);
+      launch_ll_pass<PlainSrc<double>, true>(ops, PlainSrc<double>{prev}, batch, dp, nl, ybar, count, n, flags, xinit, blkflag, s);
     else
-      launch_ll_pass<PlainSrc<double>, false>(ops, PlainSrc<double>{prev}, batch, dp, nl, next, count, 0, flags, nullptr, s);
+      launch_ll_pass<PlainSrc<double>, false>(ops, PlainSrc<double>{prev}, batch, dp, nl, next, count, 0, flags, nullptr, nullptr, s);
     st = check_launch("hybrid_ll");
     if (prev) cudaFreeAsync(prev, s);
     prev = next;
@@ -584,7 +603,7 @@ int launch_ll(const DevOps& ops, const Src& frames, int64_t batch, const LevelDi
 
 template <bool F32OUT>
 int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Workspace& w, int32_t* fits,
-                  cudaStream_t s, int reserve = 0) {
+                  cudaStream_t s, int reserve = 0, cudaEvent_t split = nullptr) {
   EmIO io{};
   io.em_reserve = reserve;
   io.y = ybar;
@@ -601,10 +620,43 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   io.xinit_ready = 1;  // computed by the low-pass kernel
   io.fits = fits ? fits : w.fits;
   io.work = w.em_work;  // zeroed by zero_counters
+  if (F32OUT) {  // fp32 lead-in + fp64 tail (the fp64 API path stays all-fp64)
+    io.xh = w.xh;
+    io.lead_work = w.lead_work;
+    io.stats = w.em_stats;
+  }
   constexpr SpecOut out = F32OUT ? SpecOut::kAosF32HiLo : SpecOut::kSoaF64;
-  if (ops.L == 26) return launch_em<26, out>(ops, io, s);
-  return launch_em<0, out>(ops, io, s);
+  if (ops.L == 26) return launch_em<26, out>(ops, io, s, split);
+  return launch_em<0, out>(ops, io, s, split);
 }
+
+// Low-pass blocks of the queued fallback pixels -> exact-block list (each
+// block once).  Their spectra came from the EM's fp32 lead-in + fp64 tail
+// (~1e-8 relative of the all-fp64 spectra), which the fallback pixels --
+// small reconstructed bands, i.e. cancellation in S + solve (rgb - ybar) --
+// would amplify; the exact pass recomputes them all-fp64 first.
+__global__ void __launch_bounds__(256) mark_exact_blocks(PxGeom g, const uint32_t* __restrict__ fb_count,
+                                                         const uint32_t* __restrict__ fb_list,
+                                                         uint8_t* __restrict__ blkflag, uint32_t* __restrict__ blk_list,
+                                                         uint32_t* __restrict__ blk_count) {
+  const uint32_t cnt = *fb_count;
+  const uint32_t plane = (uint32_t)(g.H * g.W), W = (uint32_t)g.W;
+  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < cnt; i += gridDim.x * 256) {
+    const uint32_t e = fb_list[i];
+    if (!(e & kExactTag)) continue;
+    const uint32_t p = e & ~kExactTag;
+    const uint32_t f = p / plane;
+    const uint32_t rem = p - f * plane;
+    const uint32_t row = rem / W, col = rem - row * W;
+    const uint32_t b = (uint32_t)(((int64_t)f * g.hL + (row >> g.n)) * g.wL + (col >> g.n));
+    unsigned* word = reinterpret_cast<unsigned*>(blkflag + (b & ~3u));
+    const unsigned bit = 1u << (8 * (b & 3u));
+    if (!(atomicOr(word, bit) & bit)) blk_list[atomicAdd(blk_count, 1u)] = b;
+  }
+}
+
+inline bool em_lead_active(const DevOps& ops) { return ops.L == 26 && ops.lead_thr_f > 0.0f && ops.max_iters > 2; }
+inline bool exact_blocks_active(const DevOps& ops) { return em_lead_active(ops) && ops.exact_below > 0.0; }
 
 template <int KL, bool PLANES, typename Src>
 void launch_px_rows(const DevOps& ops, const Src& frames, const PxGeom& g, dim3 grid, int R, const Workspace& w,
@@ -636,6 +688,24 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
     launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
+  if (exact_blocks_active(ops)) {
+    mark_exact_blocks<<<148 * 4, 256, 0, s>>>(g, w.fb_count, w.fb_list, w.blk_flag, w.blk_list, w.blk_count);
+    if ((st = check_launch("mark_exact_blocks"))) return st;
+    EmIO io{};
+    io.y = w.ybar;
+    io.y_soa = 1;
+    io.n = g.nll;
+    io.Shi = w.Shi;
+    io.Slo = w.Slo;
+    io.Lp = w.Lp;
+    io.xinit = w.xinit;
+    io.xinit_ready = 1;
+    io.fits = w.fits_out;
+    io.work = w.sel_work;
+    io.sel = w.blk_list;
+    io.sel_count = w.blk_count;
+    if ((st = launch_em_selected<26, SpecOut::kAosF32HiLo>(ops, io, s))) return st;
+  }
   px_fallback_kernel<Src><<<148 * 32, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
                                                         w.fb_list, thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
@@ -662,15 +732,40 @@ int hybrid_prologue(const oxm_ctx* ctx, const void* frames, int64_t batch, int64
 }
 
 // fallback + EM chunk counter reset, ordered before the low-pass kernel
-__global__ void zero_counters(uint32_t* fb, unsigned long long* em) {
+__global__ void zero_counters(uint32_t* fb, unsigned long long* em, unsigned long long* lead,
+                              unsigned long long* stats, unsigned long long* sel, uint32_t* blk) {
   *fb = 0u;
   *em = 0ull;
+  *lead = 0ull;
+  stats[0] = stats[1] = stats[2] = 0ull;
+  *sel = 0ull;
+  *blk = 0u;
 }
 
 }  // namespace
 }  // namespace oxm
 
 using namespace oxm;
+
+extern "C" int oxm_hybrid_em_counters(const oxm_ctx* ctx, void* workspace, int64_t batch, int64_t height,
+                                      int64_t width, int n_levels, uint64_t* out, void* stream) {
+  LevelDims d;
+  if (!ctx || !workspace || !out || level_dims(height, width, n_levels, d) != OXM_OK || batch < 0)
+    return OXM_ERR_ARGUMENT;
+  const Workspace w = carve(workspace, ctx->ops.L, batch * d.h[n_levels] * d.w[n_levels]);
+  DeviceGuard dg(ctx->device);
+  cudaStream_t s = as_stream(stream);
+  uint32_t blk = 0;
+  cudaError_t err = cudaMemcpyAsync(out, w.em_stats, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&blk, w.blk_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (err == cudaSuccess) err = cudaStreamSynchronize(s);
+  out[3] = blk;
+  if (err != cudaSuccess) {
+    set_last_error("oxm_hybrid_em_counters", err);
+    return OXM_ERR_CUDA;
+  }
+  return OXM_OK;
+}
 
 extern "C" size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, int64_t height, int64_t width,
                                              int n_levels) {
@@ -692,16 +787,19 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   int st = hybrid_prologue(ctx, raw, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
   if (st) return st;
   if (batch == 0) return OXM_OK;
-  // the fallback list stores 32-bit pixel indices
-  if (batch * height * width >= (int64_t)1 << 32) return OXM_ERR_ARGUMENT;
+  // the fallback list stores 31-bit pixel indices (+ the exact-block tag)
+  if (batch * height * width >= (int64_t)kExactTag) return OXM_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work);
-  if ((st = launch_ll(ctx->ops, src, batch, d, w.ybar, nll, flags, w.xinit, s))) return st;
+  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work, w.lead_work, w.em_stats, w.sel_work, w.blk_count);
+  if ((st = launch_ll(ctx->ops, src, batch, d, w.ybar, nll, flags, w.xinit, w.blk_flag, s))) return st;
   mark(ev, 1, s);
-  if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s, reserve))) return st;
-  mark(ev, 2, s);
+  if (fits) w.fits_out = fits;
+  if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s, reserve,
+                                ev ? reinterpret_cast<cudaEvent_t>(ev[2]) : nullptr)))
+    return st;
+  mark(ev, 3, s);
   if (stream_px) {  // split launch: the per-pixel stage runs on its own stream after the EM
     cudaEvent_t em_done = nullptr;
     cudaError_t err = cudaEventCreateWithFlags(&em_done, cudaEventDisableTiming);
@@ -719,7 +817,7 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
     st = launch_px_f32<26>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s);
   else
     st = launch_px_f32<0>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s);
-  mark(ev, 3, s);
+  mark(ev, 4, s);
   return st;
 }
 }  // namespace
@@ -768,11 +866,12 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work);
-  if ((st = launch_ll(ctx->ops, PlainSrc<double>{frames}, batch, d, w.ybar, nll, flags, w.xinit, s))) return st;
+  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work, w.lead_work, w.em_stats, w.sel_work, w.blk_count);
+  if ((st = launch_ll(ctx->ops, PlainSrc<double>{frames}, batch, d, w.ybar, nll, flags, w.xinit, nullptr, s))) return st;
   mark(ev, 1, s);
+  mark(ev, 2, s);  // no fp32 lead-in on the fp64 path
   if ((st = launch_em_soa<false>(ctx->ops, w.ybar, nll, w, fits, s))) return st;
-  mark(ev, 2, s);
+  mark(ev, 3, s);
   PxGeom g{height, width, d.h[n_levels], d.w[n_levels], nll, n_levels, calibration};
   const int64_t npx = batch * height * width;
   const double* S = w.S;
@@ -781,6 +880,6 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
   else
     px_f64_kernel<0><<<grid_1d(npx, 128), 128, 0, s>>>(ctx->ops, frames, g, batch, S, w.ybar, cube, hbo, hb, offset);
   st = check_launch("hybrid_px_f64");
-  mark(ev, 3, s);
+  mark(ev, 4, s);
   return st;
 }

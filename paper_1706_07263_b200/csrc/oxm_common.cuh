@@ -21,12 +21,19 @@ struct DevOps {
   float fitl2_f[3][kMaxBands];  // -ln(2) * fit_mat: x = sum_l fitl2 * log2(s)
   float2 solve_f2[kMaxBands][3];   // the same, duplicated into both halves for FFMA2
   float2 fitl2_f2[3][kMaxBands];
+  // fp32 lead-in of the EM (oxm_em.cuh, em_lead_kernel)
+  float xl2_f[kMaxBands][2];  // -xi[:, 0:2] * log2(e): e = 2^(xl2 . x - log2(e) x2)
+  float sens_f[3][kMaxBands];
+  float gain_f[kMaxBands][3];
+  float lead_thr_f;  // (K tol)^2: fp32 steps continue while |dx|^2 > lead_thr |x|^2; 0 = no lead-in
   float eps_f;
   int L;
   int max_iters;
   double eps;
   double rel_tol;
   double fallback_below;
+  double exact_below;  // with the lead-in: fallback pixels with a band below this get their block's EM redone all-fp64
+  double guard_lo, guard_hi;  // ((1 -+ m) tol)^2: an fp64 tail step with rel/tol in (1-m, 1+m) redoes the coefficient
   double solve[kMaxBands][3];  // Tikhonov ridge inverse, unmix.py:53-65
   double fitm[3][kMaxBands];   // (xi^T xi)^-1 xi^T, bayes.py:102
   double xi[kMaxBands][3];     // chromophore basis, core.py:134-158

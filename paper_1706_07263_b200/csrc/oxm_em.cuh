@@ -101,7 +101,26 @@ struct EmIO {
   unsigned long long* work;  // chunk counter, zero at launch (zeroed by em_init_kernel when it runs)
   int xinit_ready;     // x_init already computed (fused into the low-pass kernel)
   int em_reserve;      // CTA slots per SM left free for a concurrent kernel
+  // fp32 lead-in (kAosF32HiLo only, when ops.lead_thr_f > 0): em_lead_kernel
+  // writes each coefficient's hand-over state x to xh ([3][n] fp32) and its
+  // fit count to fits; the fp64 tail continues from there
+  float* xh;
+  unsigned long long* lead_work;  // lead-in chunk counter, zero at launch
+  // optional work counters (zero at launch): [0] fp32 fits committed by the
+  // lead-in, [1] fp64 fits of the tail, [2] tail restarts in exact mode
+  unsigned long long* stats;
+  // optional coefficient selection: the kernel runs coefficients sel[0 ..
+  // *sel_count) (device-side count) instead of 0 .. n; n stays the stride of
+  // the SoA arrays
+  const uint32_t* sel;
+  const uint32_t* sel_count;
 };
+
+// warp-aggregated add of each lane's v into *ctr (one atomic per warp)
+__device__ __forceinline__ void warp_count(unsigned long long* ctr, unsigned v, int lane) {
+  const unsigned t = __reduce_add_sync(0xffffffffu, v);
+  if (ctr && lane == 0 && t) atomicAdd(ctr, (unsigned long long)t);
+}
 
 constexpr int kEmThreads = 128;
 constexpr int kEmUnroll = OXM_EM_UNROLL;
@@ -217,7 +236,11 @@ __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol
   }
 }
 
-template <int KL, SpecOut OUT>
+// TAIL: continue from the fp32 lead-in's hand-over (x from io.xh, or x_init
+// when the hand-over came at fit #1; fit count from io.fits).  A tail step
+// whose rel lands within the guard band around tol, or a tail that runs into
+// max_iters, restarts its coefficient from fit #1 in exact fp64 mode.
+template <int KL, SpecOut OUT, bool TAIL = false>
 __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_kernel(const __grid_constant__ DevOps ops,
                                                                                         EmIO io) {
   constexpr int NS = kEmSlots;
@@ -240,8 +263,11 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   // first 32 * NS coefficients statically per warp, then kEmChunk-sized
   // chunks from io.work, numbered from dyn0
   const int64_t dyn0 = (int64_t)gridDim.x * kEmThreads * NS;
-  int64_t next = warp * 32 * NS;               // next unassigned coefficient of the current chunk
-  int64_t stop = min64(next + 32 * NS, io.n);  // end of the current chunk
+  // positions 0 .. count are coefficients, or indices into io.sel
+  const int64_t count = io.sel ? (int64_t)*io.sel_count : io.n;
+  auto coef = [&](int64_t pos) -> int64_t { return io.sel ? (int64_t)io.sel[pos] : pos; };
+  int64_t next = warp * 32 * NS;                // next unassigned position of the current chunk
+  int64_t stop = min64(next + 32 * NS, count);  // end of the current chunk
   bool exhausted = false;
 
   if (ops.max_iters <= 1) return;  // fit #1 is the answer: written by em_init_kernel
@@ -251,19 +277,26 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   constexpr bool kYSoa = OUT != SpecOut::kAosF64;
   int64_t idx[NS];
   int nfit[NS];
+  bool exact[NS];  // TAIL: this lane runs the coefficient from fit #1 (no guard)
+  unsigned tsteps = 0, trestarts = 0;  // TAIL work counters (io.stats)
   double y[NS][3], x[NS][3];
   auto load = [&](int sl, int64_t i) {
+    int f = 1;
+    if constexpr (TAIL) f = io.fits[i];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       y[sl][k] = kYSoa ? io.y[k * io.n + i] : io.y[3 * i + k];
-      x[sl][k] = io.xinit[k * io.n + i];
+      x[sl][k] = f > 1 ? (double)io.xh[k * io.n + i] : io.xinit[k * io.n + i];
     }
+    nfit[sl] = f;
+    exact[sl] = f <= 1;
   };
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) {
     const int64_t i = next + 32 * sl + lane;
-    idx[sl] = i < stop ? i : -1;
+    idx[sl] = i < stop ? coef(i) : -1;
     nfit[sl] = 1;
+    exact[sl] = true;
 #pragma unroll
     for (int k = 0; k < 3; ++k) y[sl][k] = x[sl][k] = 0.0;
     if (idx[sl] >= 0) load(sl, idx[sl]);
@@ -275,19 +308,20 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   auto refill = [&](int sl, unsigned m, bool done) {
     const int need = __popc(m);
     const int64_t avail = stop - next;  // warp-uniform
-    int64_t fresh = io.n, fresh_end = io.n;
+    int64_t fresh = count, fresh_end = count;
     if (avail < need && !exhausted) {
       unsigned long long b = 0;
       if (lane == 0) b = atomicAdd(io.work, (unsigned long long)kEmChunk);
       fresh = dyn0 + (int64_t)__shfl_sync(0xffffffffu, b, 0);
-      fresh_end = min64(fresh + kEmChunk, io.n);
-      exhausted = fresh >= io.n;
+      fresh_end = min64(fresh + kEmChunk, count);
+      exhausted = fresh >= count;
     }
     if (done) {
       const int r = __popc(m & lt_mask);
       const int64_t mine = r < avail ? next + r : fresh + (r - avail);
-      idx[sl] = mine < (r < avail ? stop : fresh_end) ? mine : -1;
+      idx[sl] = mine < (r < avail ? stop : fresh_end) ? coef(mine) : -1;
       nfit[sl] = 1;
+      exact[sl] = true;
       if (idx[sl] >= 0) load(sl, idx[sl]);
     }
     if (avail < need) {
@@ -351,14 +385,28 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 #pragma unroll
     for (int sl = 0; sl < NS; ++sl) {
       const double n0 = -nn[sl][0], n1 = -nn[sl][1], n2 = -nn[sl][2];
-      bool done = false;
+      bool done = false, restart = false;
       if (idx[sl] >= 0) {
         ++nfit[sl];
+        if constexpr (TAIL) ++tsteps;
         const double d0 = n0 - x[sl][0], d1 = n1 - x[sl][1], d2 = n2 - x[sl][2];
         const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
         const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x[sl][0], x[sl][0]), __dmul_rn(x[sl][1], x[sl][1])),
                                      __dmul_rn(x[sl][2], x[sl][2]));
-        done = dn2 < tol2 * fmax(xn2, 1e-16) || nfit[sl] >= ops.max_iters;
+        const double xm2 = fmax(xn2, 1e-16);
+        done = dn2 < tol2 * xm2 || nfit[sl] >= ops.max_iters;
+        if constexpr (TAIL) {
+          // the state still carries the lead-in's fp32 perturbation: a stop
+          // decision near the threshold (or one forced by max_iters) is not
+          // trusted -- redo the coefficient in exact fp64 from fit #1
+          restart = !exact[sl] && ((dn2 > ops.guard_lo * xm2 && dn2 < ops.guard_hi * xm2) || nfit[sl] >= ops.max_iters);
+          if (restart) {
+            ++trestarts;
+            done = false;
+            exact[sl] = true;
+            nfit[sl] = 1;
+          }
+        }
         if (done) {
           io.fits[idx[sl]] = nfit[sl];
           if (io.x) {
@@ -368,10 +416,20 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
           }
         }
       }
-      x[sl][0] = n0;
-      x[sl][1] = n1;
-      x[sl][2] = n2;
+      if (TAIL && restart) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) x[sl][k] = io.xinit[k * io.n + idx[sl]];
+      } else {
+        x[sl][0] = n0;
+        x[sl][1] = n1;
+        x[sl][2] = n2;
+      }
       const unsigned m = __ballot_sync(0xffffffffu, done);
+      if (TAIL && m && io.stats) {
+        warp_count(io.stats + 1, done ? tsteps : 0u, lane);
+        warp_count(io.stats + 2, done ? trestarts : 0u, lane);
+        if (done) tsteps = trestarts = 0;
+      }
       if (m) {
         // the whole warp streams the finished lanes' spectra out, then refills them
         write_spectra<KL, OUT>(io, e - lane + sl * L * es, es, L, m, idx[sl], lane, r[sl][0], r[sl][1], r[sl][2], gsm,
@@ -382,17 +440,126 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   }
 }
 
-// Persistent EM launch (enough CTAs to fill every SM once).  io.work must be
-// zero when the persistent kernel starts: em_init_kernel zeroes it when it
-// runs, otherwise (x_init fused upstream) the caller does.
-template <int KL, SpecOut OUT>
-inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
-  if (io.n <= 0) return OXM_OK;
-  if (!io.fits || !io.xinit || !io.work) return OXM_ERR_ARGUMENT;
-  if ((io.y_soa != 0) != (OUT != SpecOut::kAosF64)) return OXM_ERR_ARGUMENT;  // see em_persistent_kernel
-  io.fmt = OUT;
-  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
-  auto kern = em_persistent_kernel<KL, OUT>;
+// ---------------------------------------------------------------------------
+// fp32 lead-in of the EM (hybrid fp32-map path).
+//
+// The iteration of bayes.py:185-207 contracts (rel shrinks ~2x per fit), and a
+// "not converged" decision taken while rel is far above tol is insensitive to
+// fp32 error.  So the first fits run here in fp32 -- MUFU ex2/lg2 and FFMA
+// instead of the fp64 pipe -- for as long as |dx| > K tol |x| (K = 64 by
+// default: ops.lead_thr_f = (K tol)^2) and the next fit is not the last
+// allowed one.  The step that fails the test is not committed: the state
+// before it (x after fit k, and k) is handed to the fp64 tail
+// (em_persistent_kernel<..., TAIL>), which redoes fit k+1 onwards exactly as
+// the reference does.  The tail damps the hand-over perturbation at the
+// iteration's contraction rate while rel falls from ~K tol to tol, so final
+// spectra differ from the all-fp64 ones by ~1e-8 relative
+// (tools/mixed_em_study.py); stop decisions that land within the guard band
+// around tol are redone from fit #1 in exact fp64 (~2% of coefficients), so
+// fit counts stay bit-exact.  A hand-over at fit #1 passes x_init itself.
+template <int KL>
+__global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+  static_assert(KL > 0, "the fp32 lead-in keeps e in registers: fixed band count only");
+  constexpr float kLog2e = 1.44269504088896340736f;
+  const float eps = ops.eps_f, thr = ops.lead_thr_f;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t warp = ((int64_t)blockIdx.x * kEmThreads + threadIdx.x) >> 5;
+  const int64_t dyn0 = (int64_t)gridDim.x * kEmThreads;
+  int64_t next = warp * 32;
+  int64_t stop = min64(next + 32, io.n);
+  bool exhausted = false;
+
+  int64_t idx = next + lane < stop ? next + lane : -1;
+  int nfit = 1;
+  float y0 = 0.f, y1 = 0.f, y2 = 0.f, x0 = 0.f, x1 = 0.f, x2 = 0.f;
+  auto load = [&](int64_t i) {
+    y0 = (float)io.y[i];
+    y1 = (float)io.y[io.n + i];
+    y2 = (float)io.y[2 * io.n + i];
+    x0 = (float)io.xinit[i];
+    x1 = (float)io.xinit[io.n + i];
+    x2 = (float)io.xinit[2 * io.n + i];
+    nfit = 1;
+  };
+  if (idx >= 0) load(idx);
+  next = stop;
+
+  while (__any_sync(0xffffffffu, idx >= 0)) {
+    float e[KL];
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f;
+    const float x2t = -kLog2e * x2;  // xi[:, 2] == 1
+#pragma unroll
+    for (int l = 0; l < KL; ++l) {
+      e[l] = ex2_approx(fmaf(ops.xl2_f[l][0], x0, fmaf(ops.xl2_f[l][1], x1, x2t)));
+      c0 = fmaf(ops.sens_f[0][l], e[l], c0);
+      c1 = fmaf(ops.sens_f[1][l], e[l], c1);
+      c2 = fmaf(ops.sens_f[2][l], e[l], c2);
+    }
+    const float r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
+    float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+#pragma unroll
+    for (int l = 0; l < KL; ++l) {
+      const float sv = fmaxf(fmaf(ops.gain_f[l][2], r2, fmaf(ops.gain_f[l][1], r1, fmaf(ops.gain_f[l][0], r0, e[l]))), eps);
+      const float lg = lg2_approx(sv);
+      n0 = fmaf(ops.fitl2_f[0][l], lg, n0);
+      n1 = fmaf(ops.fitl2_f[1][l], lg, n1);
+      n2 = fmaf(ops.fitl2_f[2][l], lg, n2);
+    }
+    bool done = false;
+    if (idx >= 0) {
+      const float d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
+      const float dn2 = d0 * d0 + d1 * d1 + d2 * d2;
+      const float xn2 = fmaxf(x0 * x0 + x1 * x1 + x2 * x2, 1e-16f);
+      // commit fit nfit+1 only when the reference surely continues after it;
+      // NaN / inf (fp32 overflow) fail the test and hand over the last finite state
+      if (dn2 > thr * xn2 && dn2 <= 3.0e38f && nfit + 1 < ops.max_iters) {
+        x0 = n0;
+        x1 = n1;
+        x2 = n2;
+        ++nfit;
+      } else {
+        done = true;
+        if (nfit > 1) {
+          io.xh[idx] = x0;
+          io.xh[io.n + idx] = x1;
+          io.xh[2 * io.n + idx] = x2;
+        }
+        io.fits[idx] = nfit;
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, done);
+    if (m) {
+      if (io.stats) warp_count(io.stats, done ? (unsigned)(nfit - 1) : 0u, lane);
+      // refill finished lanes: rest of the current chunk, then a new one
+      const int need = __popc(m);
+      const int64_t avail = stop - next;
+      int64_t fresh = io.n, fresh_end = io.n;
+      if (avail < need && !exhausted) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(io.lead_work, (unsigned long long)kEmChunk);
+        fresh = dyn0 + (int64_t)__shfl_sync(0xffffffffu, b, 0);
+        fresh_end = min64(fresh + kEmChunk, io.n);
+        exhausted = fresh >= io.n;
+      }
+      if (done) {
+        const int r = __popc(m & lt_mask);
+        const int64_t mine = r < avail ? next + r : fresh + (r - avail);
+        idx = mine < (r < avail ? stop : fresh_end) ? mine : -1;
+        if (idx >= 0) load(idx);
+      }
+      if (avail < need) {
+        next = fresh_end > fresh ? min64(fresh + (need - avail), fresh_end) : fresh_end;
+        stop = fresh_end;
+      } else {
+        next += need;
+      }
+    }
+  }
+}
+
+template <typename K>
+inline int persistent_blocks(K kern, size_t smem, int reserve, int64_t need_ctas, int64_t& blocks) {
   cudaError_t err = cudaSuccess;
   if (smem > 48 * 1024) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 0, per_sm = 0;
@@ -404,20 +571,78 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s) {
     return OXM_ERR_CUDA;
   }
   if (sms < 1) sms = 1;
-  // leave `em_reserve` CTA slots per SM free so a concurrent per-pixel kernel
+  // leave `reserve` CTA slots per SM free so a concurrent per-pixel kernel
   // (split launch, other stream) can co-reside with the persistent EM
-  per_sm -= io.em_reserve;
+  per_sm -= reserve;
   if (per_sm < 1) per_sm = 1;
-  int64_t blocks = (int64_t)sms * per_sm;
+  blocks = (int64_t)sms * per_sm;
+  if (blocks > need_ctas) blocks = need_ctas;
+  return OXM_OK;
+}
+
+// Persistent EM launch (enough CTAs to fill every SM once).  io.work must be
+// zero when the persistent kernel starts: em_init_kernel zeroes it when it
+// runs, otherwise (x_init fused upstream) the caller does; likewise
+// io.lead_work for the fp32 lead-in.  `split` (optional) is recorded between
+// the lead-in and the fp64 kernel.
+template <int KL, SpecOut OUT>
+inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s, cudaEvent_t split = nullptr) {
+  if (io.n <= 0) return OXM_OK;
+  if (!io.fits || !io.xinit || !io.work) return OXM_ERR_ARGUMENT;
+  if ((io.y_soa != 0) != (OUT != SpecOut::kAosF64)) return OXM_ERR_ARGUMENT;  // see em_persistent_kernel
+  io.fmt = OUT;
+  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
   const int64_t need = ceil_div(io.n, kEmThreads);
-  if (blocks > ceil_div(need, kEmSlots)) blocks = ceil_div(need, kEmSlots);
   if (!io.xinit_ready || ops.max_iters <= 1) {
     em_init_kernel<KL><<<(unsigned)need, kEmThreads, 0, s>>>(ops, io);
     int st0 = check_launch("em_init");
     if (st0) return st0;
   }
+  constexpr bool kCanLead = KL > 0 && OUT == SpecOut::kAosF32HiLo;
+  const bool lead = kCanLead && ops.lead_thr_f > 0.0f && ops.max_iters > 2 && io.xh && io.lead_work;
+  int64_t blocks = 0;
+  int st = OXM_OK;
+  if constexpr (kCanLead) {
+    if (lead) {
+      auto lk = em_lead_kernel<(KL > 0 ? KL : 1)>;
+      if ((st = persistent_blocks(lk, 0, io.em_reserve, need, blocks))) return st;
+      lk<<<(unsigned)blocks, kEmThreads, 0, s>>>(ops, io);
+      if ((st = check_launch("em_lead"))) return st;
+    }
+  }
+  if (split) cudaEventRecord(split, s);
+  if constexpr (kCanLead) {
+    if (lead) {
+      auto tk = em_persistent_kernel<KL, OUT, true>;
+      if ((st = persistent_blocks(tk, smem, io.em_reserve, ceil_div(need, kEmSlots), blocks))) return st;
+      tk<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
+      return check_launch("em_tail");
+    }
+  }
+  auto kern = em_persistent_kernel<KL, OUT>;
+  if ((st = persistent_blocks(kern, smem, io.em_reserve, ceil_div(need, kEmSlots), blocks))) return st;
   kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
   return check_launch("em_persistent");
+}
+
+// Exact fp64 EM over a device-side coefficient list (sel, *sel_count), e.g.
+// the low-pass blocks whose pixels need the fp64 map fallback: their spectra
+// must be the all-fp64 ones, not the lead-in/tail ones.  The count is only
+// known on the device, so the grid is the full persistent one; idle CTAs
+// exit after one read.  io.work must be zero at launch.
+template <int KL, SpecOut OUT>
+inline int launch_em_selected(const DevOps& ops, EmIO io, cudaStream_t s) {
+  if (io.n <= 0) return OXM_OK;
+  if (!io.fits || !io.xinit || !io.work || !io.sel || !io.sel_count) return OXM_ERR_ARGUMENT;
+  io.fmt = OUT;
+  io.stats = nullptr;
+  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
+  auto kern = em_persistent_kernel<KL, OUT>;
+  int64_t blocks = 0;
+  int st = persistent_blocks(kern, smem, 0, ceil_div(ceil_div(io.n, kEmThreads), kEmSlots), blocks);
+  if (st) return st;
+  kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
+  return check_launch("em_selected");
 }
 
 }  // namespace oxm

@@ -49,6 +49,18 @@ __device__ __forceinline__ void load_math_tables(MathSmem& t) {
 // the log table in global memory, for kernels too short-lived to stage it
 __device__ __forceinline__ const double2* log_table_global() { return reinterpret_cast<const double2*>(kLogPair); }
 
+// MUFU (XU pipe) fp32 transcendentals: ~2 ulp, no range handling
+__device__ __forceinline__ float ex2_approx(float v) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+__device__ __forceinline__ float lg2_approx(float v) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 // exp(zs * ln2/256) for a pre-scaled argument zs
 __device__ __forceinline__ double exp_scaled(const double zs, const MathSmem& t) {
   // round-to-nearest via F2I/I2F: conversions run on the XU pipe, which the

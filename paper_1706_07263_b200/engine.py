@@ -24,12 +24,17 @@ from .core import CameraSensitivity, ChromophoreBasis, check_grids
 from .device import ptr, require_cuda, stream_handle
 from .errors import ArgumentError
 from .haar import level_dims
-from .operators import DEFAULT_FALLBACK_BELOW, OperatorSet, context
+from .operators import DEFAULT_FALLBACK_BELOW, DeviceContext, OperatorSet, context
 from .pipeline import PipelineConfig, _hybrid_operators
 
 
+# oxm_ctx_create's default EM schedule (abi.cu): fp32 fits while rel > 16 tol,
+# 1% guard band, exact re-estimate of blocks with fallback pixels
+DEFAULT_EM_LEAD = (16.0, 0.01)
+
+
 def _event_array(events):
-    """4 torch.cuda.Event -> (void*)[4] of their cudaEvent_t handles."""
+    """5 torch.cuda.Event -> (void*)[5] of their cudaEvent_t handles."""
     if events is None:
         return None
     import ctypes
@@ -39,7 +44,9 @@ def _event_array(events):
         if ev.cuda_event == 0:  # created lazily by torch: force creation
             ev.record()
         handles.append(ev.cuda_event)
-    return (ctypes.c_void_p * 4)(*handles)
+    if len(handles) != 5:
+        raise ArgumentError("stage_events: 5 events (before low-pass, EM lead-in, EM fp64, per-pixel; after)")
+    return (ctypes.c_void_p * 5)(*handles)
 
 
 @dataclass
@@ -56,8 +63,9 @@ class MapBatch:
 class HybridMapEngine:
     """Hybrid estimator for (B, H, W, 3) float32 frame batches on one GPU."""
 
-    # zero_counters, ll_kernel (+ EM fit #1), em_persistent_kernel, px_f32_kernel, px_fallback_kernel
-    KERNELS_PER_RUN = 5
+    # zero_counters, ll_kernel (+ EM fit #1), em_lead_kernel, em_persistent_kernel (tail),
+    # px_f32_kernel, px_fallback_kernel
+    KERNELS_PER_RUN = 6
 
     def __init__(
         self,
@@ -67,7 +75,14 @@ class HybridMapEngine:
         *,
         device: torch.device | None = None,
         fallback_below: float = DEFAULT_FALLBACK_BELOW,
+        em_lead: tuple | None = DEFAULT_EM_LEAD,
     ):
+        """``em_lead``: (ratio, guard[, exact_below]) of the EM's fp32 lead-in
+        (oxm_ctx_set_em_lead: fp32 fits while rel > ratio * rel_tol, then fp64;
+        fp64 redo of coefficients whose stop decision lands within ``guard``
+        of rel_tol; all-fp64 re-estimate of blocks holding a fallback pixel
+        with a band below ``exact_below``, default ``fallback_below``), or
+        None for all-fp64 EM fits."""
         check_grids(sensitivity.grid, basis.grid)
         self.cfg = cfg if cfg is not None else PipelineConfig(mode="hybrid", n_levels=2)
         if self.cfg.mode != "hybrid":
@@ -75,8 +90,17 @@ class HybridMapEngine:
         self.device = device if device is not None else require_cuda()
         base = _hybrid_operators(sensitivity, basis, self.cfg)
         self.ops = OperatorSet(**{**base.__dict__, "fallback_below": float(fallback_below)})
-        self.ctx = context(self.ops, self.device.index)
         self._lib = _native.load()
+        if em_lead == DEFAULT_EM_LEAD:
+            self.ctx = context(self.ops, self.device.index)
+        else:  # a private context: the cached one is shared
+            self.ctx = DeviceContext(self.ops, self.device.index)
+            lead = tuple(em_lead) if em_lead is not None else (0.0, DEFAULT_EM_LEAD[1])
+            ratio, guard = lead[:2]
+            exact = lead[2] if len(lead) > 2 else float(fallback_below)
+            _native.check(self._lib.oxm_ctx_set_em_lead(self.ctx.handle, float(ratio), float(guard), float(exact)),
+                          "em_lead")
+        self.em_lead = em_lead
         self._ws: torch.Tensor | None = None
 
     # ---- workspace ---------------------------------------------------------
@@ -101,6 +125,20 @@ class HybridMapEngine:
             fits=torch.empty((batch, hL, wL), dtype=torch.int32, device=self.device) if fits else None,
             flags=torch.zeros(1, dtype=torch.int32, device=self.device),
         )
+
+    def em_counters(self, batch: int, height: int, width: int) -> dict:
+        """EM work of the last launch of this geometry: fp32 lead-in fits,
+        fp64 tail fits, exact-mode restarts, blocks re-estimated all-fp64 for
+        the pixel fallback (synchronises the current stream)."""
+        import ctypes
+
+        out = (ctypes.c_uint64 * 4)()
+        st = self._lib.oxm_hybrid_em_counters(self.ctx.handle, ptr(self._workspace(self.workspace_bytes(batch, height, width))),
+                                              batch, height, width, self.cfg.n_levels, out,
+                                              stream_handle(None))
+        _native.check(st, "em_counters")
+        return {"lead_fits": int(out[0]), "tail_fits": int(out[1]), "restarts": int(out[2]),
+                "exact_blocks": int(out[3])}
 
     # ---- device-resident path ---------------------------------------------
     def launch(self, frames: torch.Tensor, out: MapBatch, *, stream: torch.cuda.Stream | None = None,

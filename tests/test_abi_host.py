@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_status_strings():
     lib = _native.load()
-    assert lib.oxm_abi_version() == 1
+    assert lib.oxm_abi_version() == 2
     for code, text in [(0, b"ok"), (-1, b"argument error"), (-2, b"data error"), (-10, b"cuda error")]:
         assert lib.oxm_status_string(code) == text
 

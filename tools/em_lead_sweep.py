@@ -1,0 +1,78 @@
+#!/usr/bin/env python3
+"""EM precision schedule sweep on the GPU (1080p n=2 textured batch).
+
+Each schedule is "K" or "K:exact_below" (K = fp32 lead-in ratio, 0 = all
+fp64; exact_below defaults to the fallback threshold, 0 disables the exact
+re-estimate of fallback blocks).  Per schedule: per-stage us/frame (5 stage
+events), EM work counters, fit-count mismatches and max THb rel / SO2 abs
+deviation against the all-fp64 schedule (itself fit-count bit-exact against
+the oracle: tests/test_gpu_pipeline.py), overall and on frame 0 split by the
+pixel's smallest reconstructed band (from the fp64 drop-in cube).
+
+    python tools/em_lead_sweep.py [batch] [schedule ...]
+"""
+import json
+import pathlib
+import sys
+
+sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
+
+BUCKETS = ((0.0, 1e-4), (1e-4, 5e-4), (5e-4, 2e-3), (2e-3, 1e9))
+
+
+def main():
+    import torch
+
+    import bench
+    import paper_1706_07263_b200 as ox
+
+    batch = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+    specs = sys.argv[2:] or ["0", "16:0", "16", "16:5e-4", "32", "8"]
+    dev = torch.device("cuda", 0)
+    sens, basis = bench.operators()
+    H, W, n = 1080, 1920, 2
+    frames = bench.make_frames(batch, H, W, 0.3, 0, dev)
+    cube, _ = ox.estimate_frame(ox.RgbImage(frames[0].double().cpu().numpy()), sens, basis,
+                                ox.PipelineConfig(n_levels=n))
+    minband = torch.from_numpy(cube.data.min(axis=2)).to(dev)
+    del cube
+    ref = None
+    for spec in specs:
+        parts = [float(v) for v in spec.split(":")]
+        k = parts[0]
+        lead = None if k <= 1 else ((k, 0.01) if len(parts) == 1 else (k, 0.01, parts[1]))
+        eng = ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev, em_lead=lead)
+        out = eng.allocate(batch, H, W, fits=True)
+        for _ in range(3):
+            eng.launch(frames, out)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(5)]
+        for e in evs:
+            eng.launch(frames, out, stage_events=e)
+        torch.cuda.synchronize()
+        eng.check_flags(out)
+        st = [sum(e[i].elapsed_time(e[i + 1]) for e in evs) / len(evs) / batch * 1e3 for i in range(4)]
+        rec = {"schedule": spec, "ll_us": round(st[0], 2), "lead_us": round(st[1], 2), "tail_us": round(st[2], 2),
+               "px_us": round(st[3], 2), "total_us": round(sum(st), 2), **eng.em_counters(batch, H, W)}
+        thb, so2, fits = out.thb.double(), out.so2.double(), out.fits.clone()
+        if ref is None:
+            ref = (thb, so2, fits)
+        else:
+            rt, rs, rf = ref
+            ok = ~torch.isnan(rs)
+            rec["fit_mismatch"] = int((fits != rf).sum())
+            rec["nan_pattern_equal"] = bool(torch.equal(torch.isnan(so2), torch.isnan(rs)))
+            trel = (thb - rt).abs() / rt.abs().clamp_min(1e-30)
+            sab = torch.where(ok, (so2 - rs).abs(), torch.zeros_like(rs))
+            rec["thb_rel_max"] = float(trel.max())
+            rec["so2_abs_max"] = float(sab.max())
+            for lo, hi in BUCKETS:
+                m = (minband >= lo) & (minband < hi)
+                if bool(m.any()):
+                    rec[f"f0_band[{lo:g},{hi:g})"] = [int(m.sum()), float(trel[0][m].max()), float(sab[0][m].max())]
+        print(json.dumps(rec), flush=True)
+        del eng, out
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
