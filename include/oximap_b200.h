@@ -97,10 +97,10 @@ OXM_API int oxm_ctx_destroy(oxm_ctx* ctx);
  * ratio > 1: fits run in fp32 while rel > ratio * rel_tol, then in fp64; a
  * fp64 step with |rel/rel_tol - 1| < guard (or reaching max_iters) redoes
  * its coefficient in fp64 from fit #1.  ratio <= 1: all fits in fp64.
- * exact_below > 0: low-pass blocks holding a fallback pixel with a band below
- * it are re-estimated all-fp64 before the fp64 pixel fallback (their
- * cancellation would amplify the schedule's ~1e-8 spectrum deviation);
- * 0 = never.  Default (16, 0.01, ops.fallback_below).  The drop-in fp64 entry
+ * exact_below > 0: low-pass blocks holding a fallback pixel with a band in
+ * [epsilon / 2, exact_below) are re-estimated all-fp64 before the fp64 pixel
+ * fallback (such small unclamped bands would amplify the schedule's ~1e-8
+ * spectrum deviation through log s); 0 = never.  Default (16, 0.01, ops.fallback_below).  The drop-in fp64 entry
  * points are always all-fp64.  Not thread-safe against concurrent launches on
  * the same context. */
 OXM_API int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, double exact_below);

@@ -41,7 +41,6 @@ constexpr int kLlThreads = 128;
 #endif
 constexpr int kPxThreads = OXM_PX_THREADS;  // threads per CTA in the fp32 map kernel (2 pixel columns each)
 constexpr int kFbThreads = 128;
-constexpr uint32_t kExactTag = 0x80000000u;  // fallback-list entry flag: re-estimate the block all-fp64
 
 struct LevelDims {
   int n;
@@ -290,7 +289,6 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   }
   const float cal = (float)g.cal;
   const float thr = (float)ops.fallback_below;
-  const float ethr = (float)ops.exact_below;
   bool any_fb = false;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -339,10 +337,8 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
           uint32_t base = 0;
           if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
           base = __shfl_sync(active, base, leader);
-          // top bit: the block's spectrum must be the all-fp64 one (mark_exact_blocks)
           if (need)
-            fb_list[base + __popc(m & ((1u << lane) - 1u))] =
-                (uint32_t)((f * g.H + row0 + r) * g.W + col + c) | (vmin[r][c] >= ethr ? 0u : kExactTag);
+            fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col + c);
         }
       }
     }
@@ -356,18 +352,37 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
 // the table log (~1 ulp; the argument is clamped at eps > 0 first, as the
 // reference does).  Operators are staged in shared memory by CTAs that have
 // work (the per-lane band index would serialise constant-bank reads).
+//
+// With the EM's fp32 lead-in (em_lead_kernel) the block spectra differ from
+// the all-fp64 ones by ~1e-8 relative, and a queued pixel amplifies that by
+// |S| / s_l through log s_l for every band s_l = S_l + solve (rgb - ybar)
+// that is small but not clamped.  Bands below eps / 2 are clamped to eps
+// either way, so a pixel is "sensitive" when some band lies in
+// [eps / 2, exact_below).  Modes:
+//   kFbAll       recompute every queued pixel (all-fp64 EM schedule);
+//   kFbClassify  recompute the insensitive ones (~85% of textured queues are
+//                clamped-only); for a sensitive one, tag its list entry
+//                (kDeferTag) and append its low-pass block (once) to the
+//                exact list that em_exact_kernel re-estimates all-fp64;
+//   kFbDeferred  recompute the tagged entries (after the exact pass).
+// Each pixel is written exactly once, from spectra that no kernel modifies
+// while it is classified: the output does not depend on scheduling.
 constexpr int kFbLanes = 4;
-template <typename Src>
+constexpr uint32_t kDeferTag = 0x80000000u;
+enum FbMode { kFbAll, kFbClassify, kFbDeferred };
+template <int KL, typename Src, int MODE>
 __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
                                                                  const Src frames, PxGeom g,
                                                                  const float* __restrict__ Shi,
                                                                  const float* __restrict__ Slo, int Lp,
                                                                  const double* __restrict__ ybar,
                                                                  const uint32_t* __restrict__ fb_count,
-                                                                 const uint32_t* __restrict__ fb_list,
+                                                                 uint32_t* __restrict__ fb_list,
                                                                  float* __restrict__ thb, float* __restrict__ so2,
                                                                  float* __restrict__ hbo, float* __restrict__ hb,
-                                                                 float* __restrict__ off) {
+                                                                 float* __restrict__ off, uint8_t* __restrict__ blkflag,
+                                                                 uint32_t* __restrict__ blk_list,
+                                                                 uint32_t* __restrict__ blk_count) {
   __shared__ double T[kMaxBands][3], F[3][kMaxBands];
   constexpr int kPerCta = kFbThreads / kFbLanes;
   const uint32_t cnt = *fb_count;
@@ -384,8 +399,14 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   const double2* logt = log_table_global();
   const int64_t stride = (int64_t)gridDim.x * kPerCta;
   // the loop bound is uniform over each group of kFbLanes lanes (shuffles below)
+  const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below;
   for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride) {
-    const uint32_t p = fb_list[i] & ~kExactTag;
+    const unsigned grp = __activemask();
+    uint32_t p = fb_list[i];
+    if constexpr (MODE == kFbDeferred) {
+      if (!(p & kDeferTag)) continue;  // group-uniform
+      p &= ~kDeferTag;
+    }
     const uint32_t f = p / plane;
     const uint32_t rem = p - f * plane;
     const uint32_t row = rem / W, col = rem - row * W;
@@ -395,17 +416,41 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
     const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + bidx];
     const float* hi = Shi + bidx * Lp;
     const float* lo = Slo + bidx * Lp;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-#pragma unroll 4
-    for (int l = sub; l < L; l += kFbLanes) {
-      const double S = (double)ldg(hi + l) + (double)ldg(lo + l);
-      const double sp = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
-      const double lg = log_tab(fmax(sp, ops.eps), logt);
-      a0 = fma(F[0][l], lg, a0);
-      a1 = fma(F[1][l], lg, a1);
-      a2 = fma(F[2][l], lg, a2);
+    constexpr int kPer = (BandCount<KL>::kMax + kFbLanes - 1) / kFbLanes;
+    double sp[kPer];
+    bool sens = false;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int l = sub + kFbLanes * k;
+      if (l < L) {
+        const double S = (double)ldg(hi + l) + (double)ldg(lo + l);
+        sp[k] = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
+        sens |= sp[k] >= lo_b && sp[k] < hi_b;
+      }
     }
-    const unsigned grp = __activemask();
+    if constexpr (MODE == kFbClassify) {
+      const unsigned lane_base = (threadIdx.x & 31) & ~(kFbLanes - 1);
+      if ((__ballot_sync(grp, sens) >> lane_base) & ((1u << kFbLanes) - 1u)) {  // this group: defer to the exact pass
+        if (sub == 0) {
+          fb_list[i] = p | kDeferTag;
+          unsigned* word = reinterpret_cast<unsigned*>(blkflag + (bidx & ~int64_t(3)));
+          const unsigned bit = 1u << (8 * (unsigned)(bidx & 3));
+          if (!(atomicOr(word, bit) & bit)) blk_list[atomicAdd(blk_count, 1u)] = (uint32_t)bidx;
+        }
+        continue;
+      }
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int l = sub + kFbLanes * k;
+      if (l < L) {
+        const double lg = log_tab(fmax(sp[k], ops.eps), logt);
+        a0 = fma(F[0][l], lg, a0);
+        a1 = fma(F[1][l], lg, a1);
+        a2 = fma(F[2][l], lg, a2);
+      }
+    }
 #pragma unroll
     for (int o = 1; o < kFbLanes; o <<= 1) {
       a0 += __shfl_xor_sync(grp, a0, o);
@@ -601,6 +646,9 @@ int launch_ll(const DevOps& ops, const Src& frames, int64_t batch, const LevelDi
   return st;
 }
 
+inline bool em_lead_active(const DevOps& ops) { return ops.L == 26 && ops.lead_thr_f > 0.0f && ops.max_iters > 2; }
+inline bool exact_blocks_active(const DevOps& ops) { return em_lead_active(ops) && ops.exact_below > 0.0; }
+
 template <bool F32OUT>
 int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Workspace& w, int32_t* fits,
                   cudaStream_t s, int reserve = 0, cudaEvent_t split = nullptr) {
@@ -629,34 +677,6 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
   if (ops.L == 26) return launch_em<26, out>(ops, io, s, split);
   return launch_em<0, out>(ops, io, s, split);
 }
-
-// Low-pass blocks of the queued fallback pixels -> exact-block list (each
-// block once).  Their spectra came from the EM's fp32 lead-in + fp64 tail
-// (~1e-8 relative of the all-fp64 spectra), which the fallback pixels --
-// small reconstructed bands, i.e. cancellation in S + solve (rgb - ybar) --
-// would amplify; the exact pass recomputes them all-fp64 first.
-__global__ void __launch_bounds__(256) mark_exact_blocks(PxGeom g, const uint32_t* __restrict__ fb_count,
-                                                         const uint32_t* __restrict__ fb_list,
-                                                         uint8_t* __restrict__ blkflag, uint32_t* __restrict__ blk_list,
-                                                         uint32_t* __restrict__ blk_count) {
-  const uint32_t cnt = *fb_count;
-  const uint32_t plane = (uint32_t)(g.H * g.W), W = (uint32_t)g.W;
-  for (uint32_t i = blockIdx.x * 256 + threadIdx.x; i < cnt; i += gridDim.x * 256) {
-    const uint32_t e = fb_list[i];
-    if (!(e & kExactTag)) continue;
-    const uint32_t p = e & ~kExactTag;
-    const uint32_t f = p / plane;
-    const uint32_t rem = p - f * plane;
-    const uint32_t row = rem / W, col = rem - row * W;
-    const uint32_t b = (uint32_t)(((int64_t)f * g.hL + (row >> g.n)) * g.wL + (col >> g.n));
-    unsigned* word = reinterpret_cast<unsigned*>(blkflag + (b & ~3u));
-    const unsigned bit = 1u << (8 * (b & 3u));
-    if (!(atomicOr(word, bit) & bit)) blk_list[atomicAdd(blk_count, 1u)] = b;
-  }
-}
-
-inline bool em_lead_active(const DevOps& ops) { return ops.L == 26 && ops.lead_thr_f > 0.0f && ops.max_iters > 2; }
-inline bool exact_blocks_active(const DevOps& ops) { return em_lead_active(ops) && ops.exact_below > 0.0; }
 
 template <int KL, bool PLANES, typename Src>
 void launch_px_rows(const DevOps& ops, const Src& frames, const PxGeom& g, dim3 grid, int R, const Workspace& w,
@@ -688,26 +708,34 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
     launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
-  if (exact_blocks_active(ops)) {
-    mark_exact_blocks<<<148 * 4, 256, 0, s>>>(g, w.fb_count, w.fb_list, w.blk_flag, w.blk_list, w.blk_count);
-    if ((st = check_launch("mark_exact_blocks"))) return st;
-    EmIO io{};
-    io.y = w.ybar;
-    io.y_soa = 1;
-    io.n = g.nll;
-    io.Shi = w.Shi;
-    io.Slo = w.Slo;
-    io.Lp = w.Lp;
-    io.xinit = w.xinit;
-    io.xinit_ready = 1;
-    io.fits = w.fits_out;
-    io.work = w.sel_work;
-    io.sel = w.blk_list;
-    io.sel_count = w.blk_count;
-    if ((st = launch_em_selected<26, SpecOut::kAosF32HiLo>(ops, io, s))) return st;
+  const unsigned fb_grid = 148 * 32;
+  if (!exact_blocks_active(ops)) {
+    px_fallback_kernel<KL, Src, kFbAll><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
+                                                                  w.fb_list, thb, so2, hbo, hb, off, nullptr, nullptr,
+                                                                  nullptr);
+    return check_launch("hybrid_fallback");
   }
-  px_fallback_kernel<Src><<<148 * 32, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
-                                                        w.fb_list, thb, so2, hbo, hb, off);
+  px_fallback_kernel<KL, Src, kFbClassify><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar,
+                                                                     w.fb_count, w.fb_list, thb, so2, hbo, hb, off,
+                                                                     w.blk_flag, w.blk_list, w.blk_count);
+  if ((st = check_launch("hybrid_fallback_classify"))) return st;
+  EmIO io{};
+  io.y = w.ybar;
+  io.y_soa = 1;
+  io.n = g.nll;
+  io.Shi = w.Shi;
+  io.Slo = w.Slo;
+  io.Lp = w.Lp;
+  io.xinit = w.xinit;
+  io.xinit_ready = 1;
+  io.fits = w.fits_out;
+  io.work = w.sel_work;
+  io.sel = w.blk_list;
+  io.sel_count = w.blk_count;
+  if ((st = launch_em_selected<26, SpecOut::kAosF32HiLo>(ops, io, s))) return st;
+  px_fallback_kernel<KL, Src, kFbDeferred><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar,
+                                                                     w.fb_count, w.fb_list, thb, so2, hbo, hb, off,
+                                                                     nullptr, nullptr, nullptr);
   return check_launch("hybrid_fallback");
 }
 
@@ -787,8 +815,8 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   int st = hybrid_prologue(ctx, raw, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
   if (st) return st;
   if (batch == 0) return OXM_OK;
-  // the fallback list stores 31-bit pixel indices (+ the exact-block tag)
-  if (batch * height * width >= (int64_t)kExactTag) return OXM_ERR_ARGUMENT;
+  // the fallback list stores 31-bit pixel indices (+ kDeferTag)
+  if (batch * height * width >= (int64_t)kDeferTag) return OXM_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);

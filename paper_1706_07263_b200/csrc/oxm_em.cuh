@@ -55,9 +55,12 @@ struct BandCount {
 // The e columns are strided by threads + 1 doubles per band: rows (one band,
 // consecutive threads) stay contiguous, and a column (one thread, consecutive
 // bands -- write_spectra) walks the banks instead of hitting one bank 26 times.
+// Each column also holds, after its L bands, the lane's residual r (3 rows)
+// and coefficient index (1 row), which write_spectra reads for the owner lane.
+constexpr int kEmColExtra = 4;
 __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
   return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands +
-         sizeof(double) * (size_t)L * (size_t)(threads + 1) * OXM_EM_SLOTS;
+         sizeof(double) * (size_t)(L + kEmColExtra) * (size_t)(threads + 1) * OXM_EM_SLOTS;
 }
 
 // ---------------------------------------------------------------------------
@@ -207,18 +210,19 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
 // lane j's e_l at ecol0[l * es + j]), its residual r and a shared-memory copy
 // of G -- the same FMAs in the same order, so the same bits.  One finished
 // lane at a time (warp-uniform loop, ~2.4 lanes finish per step); lane l
-// handles band l, so every row is stored with coalesced accesses.
+// handles band l, so every row is stored with coalesced accesses.  The
+// owner's r and index come from rows L..L+3 of its column (broadcast reads).
+// Slo == nullptr: hi parts only (the exact-block pass rewrites every block
+// whose lo parts the fp64 pixel fallback reads).
 template <int KL, SpecOut OUT>
 __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol0, int es, int L, unsigned done_mask,
-                                              int64_t idx, int lane, double r0, double r1, double r2,
-                                              const double (*gsm)[3], double eps) {
+                                              int lane, const double (*gsm)[3], double eps) {
   while (done_mask) {
     const int owner = __ffs(done_mask) - 1;
     done_mask &= done_mask - 1;
-    const int64_t oidx = __shfl_sync(0xffffffffu, idx, owner);
-    const double q0 = __shfl_sync(0xffffffffu, r0, owner);
-    const double q1 = __shfl_sync(0xffffffffu, r1, owner);
-    const double q2 = __shfl_sync(0xffffffffu, r2, owner);
+    const double* oc = ecol0 + owner;
+    const double q0 = oc[L * es], q1 = oc[(L + 1) * es], q2 = oc[(L + 2) * es];
+    const int64_t oidx = __double_as_longlong(oc[(L + 3) * es]);
 #pragma unroll
     for (int l = lane; l < BandCount<KL>::kMax; l += 32) {
       if (KL == 0 && l >= L) break;
@@ -230,7 +234,7 @@ __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol
       } else {
         const float h = __double2float_rn(s);
         io.Shi[oidx * io.Lp + l] = h;
-        io.Slo[oidx * io.Lp + l] = __double2float_rn(s - (double)h);
+        if (io.Slo) io.Slo[oidx * io.Lp + l] = __double2float_rn(s - (double)h);
       }
     }
   }
@@ -247,7 +251,8 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
   double(*gsm)[3] = reinterpret_cast<double(*)[3]>(smem_raw + sizeof(MathSmem));  // G, for write_spectra
-  // e of slot s, band l at e[(s * L + l) * es]: one column per thread and slot
+  // e of slot s, band l at e[(s * (L + kEmColExtra) + l) * es]: one column per
+  // thread and slot, then r (rows L..L+2) and the coefficient index (row L+3)
   double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem) + sizeof(ops.gain)) + threadIdx.x;
   constexpr int es = kEmThreads + 1;  // band stride of the e columns (see em_smem_bytes)
   load_math_tables(mt);
@@ -290,6 +295,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     }
     nfit[sl] = f;
     exact[sl] = f <= 1;
+    e[(sl * (L + kEmColExtra) + L + 3) * es] = __longlong_as_double(i);  // for write_spectra
   };
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) {
@@ -352,7 +358,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) {
         const double el = exp_scaled(-fma(ops.xis[l][0], x[sl][0], fma(ops.xis[l][1], x[sl][1], x2s[sl])), mt);
-        e[(sl * L + l) * es] = el;
+        e[(sl * (L + kEmColExtra) + l) * es] = el;
         c[sl][0] = fma(ops.sens[0][l], el, c[sl][0]);
         c[sl][1] = fma(ops.sens[1][l], el, c[sl][1]);
         c[sl][2] = fma(ops.sens[2][l], el, c[sl][2]);
@@ -365,6 +371,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
       for (int k = 0; k < 3; ++k) {
         r[sl][k] = y[sl][k] - c[sl][k];
         nn[sl][k] = 0.0;
+        e[(sl * (L + kEmColExtra) + L + k) * es] = r[sl][k];  // for write_spectra
       }
     // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
     // (s itself is not stored: write_spectra re-forms it for finished lanes)
@@ -373,7 +380,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) {
         const double sv = clamp_eps(
-            fma(ops.gain[l][2], r[sl][2], fma(ops.gain[l][1], r[sl][1], fma(ops.gain[l][0], r[sl][0], e[(sl * L + l) * es]))),
+            fma(ops.gain[l][2], r[sl][2], fma(ops.gain[l][1], r[sl][1], fma(ops.gain[l][0], r[sl][0], e[(sl * (L + kEmColExtra) + l) * es]))),
             eps);
         const double lg = log_tab(sv, mt.logt);
         nn[sl][0] = fma(ops.fitm[0][l], lg, nn[sl][0]);
@@ -432,8 +439,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
       }
       if (m) {
         // the whole warp streams the finished lanes' spectra out, then refills them
-        write_spectra<KL, OUT>(io, e - lane + sl * L * es, es, L, m, idx[sl], lane, r[sl][0], r[sl][1], r[sl][2], gsm,
-                               eps);
+        write_spectra<KL, OUT>(io, e - lane + sl * (L + kEmColExtra) * es, es, L, m, lane, gsm, eps);
         refill(sl, m, done);
       }
     }
@@ -627,22 +633,156 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s, cudaEvent_t spl
 
 // Exact fp64 EM over a device-side coefficient list (sel, *sel_count), e.g.
 // the low-pass blocks whose pixels need the fp64 map fallback: their spectra
-// must be the all-fp64 ones, not the lead-in/tail ones.  The count is only
-// known on the device, so the grid is the full persistent one; idle CTAs
-// exit after one read.  io.work must be zero at launch.
+// must be the all-fp64 ones, not the lead-in/tail ones.  The list is short
+// (~6% of the coefficients), so one lane per coefficient would leave most of
+// the GPU idle and each warp waiting for its slowest lanes; here a group of
+// kXLanes lanes shares a coefficient (bands sub, sub + kXLanes, ...; the
+// C e and fit sums are reduced with xor shuffles, which leave bit-identical
+// sums in every lane of the group) and takes the next list entry from a
+// global counter when it finishes.  Same fp64 table exp/log and the same
+// per-band arithmetic as em_persistent_kernel; only the order of the 26-term
+// sums differs (~1 ulp, like any other summation order of the reference's
+// BLAS products).  The count is device-side, so the grid is the resident
+// one; io.work must be zero at launch.
+constexpr int kXLanes = 4;
+constexpr int kXThreads = 128;
+struct alignas(16) XBand {  // per-band operator row, staged in shared memory (lanes read different bands)
+  double xs0, xs1, c0, c1, c2, g0, g1, g2, f0, f1, f2, pad;
+};
+
+template <int KL, SpecOut OUT>
+__global__ void __launch_bounds__(kXThreads) em_exact_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+  static_assert(KL > 0, "fixed band count");
+  constexpr int NB = (KL + kXLanes - 1) / kXLanes;  // bands per lane
+  __shared__ MathSmem mt;
+  __shared__ XBand ob[KL];
+  load_math_tables(mt);
+  for (int l = threadIdx.x; l < KL; l += kXThreads) {
+    ob[l] = XBand{ops.xis[l][0], ops.xis[l][1], ops.sens[0][l], ops.sens[1][l], ops.sens[2][l], ops.gain[l][0],
+                  ops.gain[l][1], ops.gain[l][2], ops.fitm[0][l], ops.fitm[1][l], ops.fitm[2][l], 0.0};
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, sub = lane & (kXLanes - 1), lead = lane & ~(kXLanes - 1);
+  const double eps = ops.eps, tol2 = ops.rel_tol * ops.rel_tol;
+  const int64_t count = io.sel ? (int64_t)*io.sel_count : io.n;
+  int64_t idx = -1;
+  int nfit = 1;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, x0 = 0.0, x1 = 0.0, x2 = 0.0;
+  bool want = true;  // this group needs its next coefficient
+  for (;;) {
+    if (want) {  // group-uniform
+      unsigned long long j = 0;
+      if (sub == 0) j = atomicAdd(io.work, 1ull);
+      j = __shfl_sync(__activemask(), j, lead);
+      idx = (int64_t)j < count ? (io.sel ? (int64_t)io.sel[j] : (int64_t)j) : -1;
+      if (idx >= 0) {
+        y0 = io.y[idx];
+        y1 = io.y[io.n + idx];
+        y2 = io.y[2 * io.n + idx];
+        x0 = io.xinit[idx];
+        x1 = io.xinit[io.n + idx];
+        x2 = io.xinit[2 * io.n + idx];
+        nfit = 1;
+      }
+      want = false;
+    }
+    if (!__any_sync(0xffffffffu, idx >= 0)) break;
+    // phase A: e = exp(-xi x) for this lane's bands, C e reduced over the group
+    double e[NB];
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    const double x2s = x2 * kExpScale;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int l = sub + kXLanes * k;
+      if (l < KL) {
+        const XBand& b = ob[l];
+        e[k] = exp_scaled(-fma(b.xs0, x0, fma(b.xs1, x1, x2s)), mt);
+        c0 = fma(b.c0, e[k], c0);
+        c1 = fma(b.c1, e[k], c1);
+        c2 = fma(b.c2, e[k], c2);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < kXLanes; o <<= 1) {
+      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+    }
+    const double r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
+    // phase B: s = max(e + G r, eps), fit of log s reduced over the group
+    double sv[NB];
+    double n0 = 0.0, n1 = 0.0, n2 = 0.0;
+#pragma unroll
+    for (int k = 0; k < NB; ++k) {
+      const int l = sub + kXLanes * k;
+      if (l < KL) {
+        const XBand& b = ob[l];
+        sv[k] = clamp_eps(fma(b.g2, r2, fma(b.g1, r1, fma(b.g0, r0, e[k]))), eps);
+        const double lg = log_tab(sv[k], mt.logt);
+        n0 = fma(b.f0, lg, n0);
+        n1 = fma(b.f1, lg, n1);
+        n2 = fma(b.f2, lg, n2);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < kXLanes; o <<= 1) {
+      n0 += __shfl_xor_sync(0xffffffffu, n0, o);
+      n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+      n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    }
+    n0 = -n0;
+    n1 = -n1;
+    n2 = -n2;
+    if (idx >= 0) {  // group-uniform from here on
+      ++nfit;
+      const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
+      const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+      const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
+      x0 = n0;
+      x1 = n1;
+      x2 = n2;
+      if (dn2 < tol2 * fmax(xn2, 1e-16) || nfit >= ops.max_iters) {
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+          const int l = sub + kXLanes * k;
+          if (l < KL) {
+            if constexpr (OUT == SpecOut::kSoaF64) {
+              io.S[(int64_t)l * io.n + idx] = sv[k];
+            } else if constexpr (OUT == SpecOut::kAosF64) {
+              io.S[idx * KL + l] = sv[k];
+            } else {
+              const float h = __double2float_rn(sv[k]);
+              io.Shi[idx * io.Lp + l] = h;
+              io.Slo[idx * io.Lp + l] = __double2float_rn(sv[k] - (double)h);
+            }
+          }
+        }
+        if (sub == 0) {
+          io.fits[idx] = nfit;
+          if (io.x) {
+            io.x[3 * idx] = n0;
+            io.x[3 * idx + 1] = n1;
+            io.x[3 * idx + 2] = n2;
+          }
+        }
+        want = true;
+      }
+    }
+  }
+}
+
 template <int KL, SpecOut OUT>
 inline int launch_em_selected(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (io.n <= 0) return OXM_OK;
   if (!io.fits || !io.xinit || !io.work || !io.sel || !io.sel_count) return OXM_ERR_ARGUMENT;
+  if (ops.max_iters <= 1) return OXM_ERR_ARGUMENT;  // fit #1 would be final: nothing to redo
   io.fmt = OUT;
-  io.stats = nullptr;
-  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
-  auto kern = em_persistent_kernel<KL, OUT>;
+  auto kern = em_exact_kernel<KL, OUT>;
   int64_t blocks = 0;
-  int st = persistent_blocks(kern, smem, 0, ceil_div(ceil_div(io.n, kEmThreads), kEmSlots), blocks);
+  int st = persistent_blocks(kern, 0, 0, ceil_div(io.n * kXLanes, kXThreads), blocks);
   if (st) return st;
-  kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
-  return check_launch("em_selected");
+  kern<<<(unsigned)blocks, kXThreads, 0, s>>>(ops, io);
+  return check_launch("em_exact");
 }
 
 }  // namespace oxm

@@ -14,12 +14,9 @@ import sys
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-VARIANTS = {
+VARIANTS = {  # name -> extra -D defines (the last sweep: EM slots / occupancy)
     "base": (),
-    "m5": ("OXM_EM_MIN_BLOCKS=5",),
-    "s2m3": ("OXM_EM_SLOTS=2", "OXM_EM_MIN_BLOCKS=3"),
-    "s2m3a13": ("OXM_EM_SLOTS=2", "OXM_EM_MIN_BLOCKS=3", "OXM_EM_UNROLL=13", "OXM_EM_UNROLL_B=13"),
-    "s2m2": ("OXM_EM_SLOTS=2", "OXM_EM_MIN_BLOCKS=2"),
+    "m4": ("OXM_EM_MIN_BLOCKS=4",),
 }
 
 
