@@ -179,10 +179,12 @@ OXM_API int oxm_expected_spectrum_f64(const oxm_ctx* ctx, const double* x, int64
  * oxm_ctx_set_em_lead), fp32 per-pixel stage with an fp64 recompute of
  * pixels whose smallest band < ops.fallback_below.
  * Outputs are planar (batch, H, W); fits is (batch, ceil(H/2^n), ceil(W/2^n)).
- * stage_events: NULL, or 5 cudaEvent_t recorded on `stream` before the
+ * stage_events: NULL, or 6 cudaEvent_t recorded on `stream` before the
  * low-pass kernel, before the EM's fp32 lead-in, before its fp64 kernel,
- * before the per-pixel kernel and after it (live per-kernel timing for the
- * roofline report; with no lead-in, events 1 and 2 coincide). */
+ * before the per-pixel kernel, before the fp64 pixel fixup (fallback
+ * classification, exact-block EM, deferred pixels) and after it (live
+ * per-kernel timing for the roofline report; with no lead-in, events 1 and 2
+ * coincide). */
 OXM_API size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, int64_t height,
                                   int64_t width, int n_levels);
 /* EM work counters of the last fp32-map launch that used `workspace` (same

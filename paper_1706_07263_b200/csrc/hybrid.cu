@@ -8,22 +8,26 @@
 //     cube(p) = S[b] + solve (rgb(p) - LL_n[b] / 2^n)
 // exactly (SURVEY.md §8a "collapse identity"), where LL_n is the reference's
 // recursively edge-replicated low-pass (haar.py:80-101) and S the EM spectra
-// of LL_n / 2^n (bayes.py:185-207).  Three launches per batch:
+// of LL_n / 2^n (bayes.py:185-207).  Launches per batch (fp32 map path):
+//   0. zero_counters  fallback / EM work counters
 //   1. ll_kernel      one thread per low-pass coefficient: the LL chain in
 //                     fp64 with the reference's add order (bit-exact LL),
-//                     non-finite / negative checks -> flags
-//   2. em_soa_kernel  one thread per coefficient: K4 in fp64 -> S (SoA)
-//   3. px kernel      one thread per (column, 2^n-row block segment): rebuild
-//                     the 26-band spectrum in registers, log, 3x26 fit,
-//                     THb/SO2.  fp32 variant: S as an fp32 (hi, lo) pair per
-//                     band, MUFU lg2, R rows per thread interleaved for ILP;
-//                     pixels whose smallest band < fallback_below are
-//                     appended (warp-aggregated) to a list and
-//   4. fallback       recomputed in fp64 by a small grid-stride kernel
-//                     (cancellation guard; ~0.6 % of textured pixels), so
-//                     the hot kernel has no divergent fp64 code at all.
-//                     fp64 variant (drop-in API): everything fp64, optional
-//                     (H, W, L) cube, no fallback needed.
+//                     non-finite / negative checks -> flags, EM fit #1
+//   2. em_lead_kernel fp32 fits while rel > K tol (oxm_em.cuh)
+//   3. em_persistent_kernel<TAIL>  the remaining fits in fp64 -> S as an
+//                     fp32 (hi, lo) pair per band
+//   4. px kernel      one thread per (2 columns, R rows of a block): rebuild
+//                     the 26-band spectrum in registers, MUFU lg2, 3x26 fit,
+//                     THb/SO2; pixels whose smallest band < fallback_below
+//                     are appended (warp-aggregated) to a list
+//   5. px_fallback_kernel<kFbClassify>  fp64 recompute of the queued pixels
+//                     (cancellation guard; ~0.4 % of textured pixels), except
+//                     the "sensitive" ones, whose blocks go to
+//   6. em_exact_kernel all-fp64 EM of those blocks (~1 % of them), then
+//   7. px_fallback_kernel<kFbDeferred>  the deferred pixels.
+// With the all-fp64 EM schedule (oxm_ctx_set_em_lead ratio <= 1) 2, 5-7
+// become one all-fp64 persistent EM and one fallback pass.  The fp64 variant
+// (drop-in API): everything fp64, optional (H, W, L) cube, no fallback.
 // Neither the directional planes nor the 26-channel cube touch HBM on the
 // fp32 path: HBM traffic is the frame read twice, the per-block spectra
 // (8 B/band/coefficient) once, and the maps written once.
@@ -400,8 +404,10 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   const int64_t stride = (int64_t)gridDim.x * kPerCta;
   // the loop bound is uniform over each group of kFbLanes lanes (shuffles below)
   const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below;
+  // group collectives use the group's own lanes: other groups of the warp may
+  // have left the loop or skipped this entry
+  const unsigned grp = ((1u << kFbLanes) - 1u) << ((threadIdx.x & 31) & ~(kFbLanes - 1));
   for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride) {
-    const unsigned grp = __activemask();
     uint32_t p = fb_list[i];
     if constexpr (MODE == kFbDeferred) {
       if (!(p & kDeferTag)) continue;  // group-uniform
@@ -429,8 +435,7 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
       }
     }
     if constexpr (MODE == kFbClassify) {
-      const unsigned lane_base = (threadIdx.x & 31) & ~(kFbLanes - 1);
-      if ((__ballot_sync(grp, sens) >> lane_base) & ((1u << kFbLanes) - 1u)) {  // this group: defer to the exact pass
+      if (__ballot_sync(grp, sens)) {  // this group's pixel: defer to the exact pass
         if (sub == 0) {
           fb_list[i] = p | kDeferTag;
           unsigned* word = reinterpret_cast<unsigned*>(blkflag + (bidx & ~int64_t(3)));
@@ -689,7 +694,8 @@ void launch_px_rows(const DevOps& ops, const Src& frames, const PxGeom& g, dim3 
 
 template <int KL, typename Src>
 int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t batch, const Workspace& w,
-                  float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
+                  float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s,
+                  cudaEvent_t fixup_ev = nullptr) {
   if (!thb || !so2) return OXM_ERR_ARGUMENT;
   // the planes are written all three or none
   const bool planes = hbo || hb || off;
@@ -708,6 +714,7 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
     launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
+  if (fixup_ev) cudaEventRecord(fixup_ev, s);
   const unsigned fb_grid = 148 * 32;
   if (!exact_blocks_active(ops)) {
     px_fallback_kernel<KL, Src, kFbAll><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
@@ -738,6 +745,8 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
                                                                      nullptr, nullptr, nullptr);
   return check_launch("hybrid_fallback");
 }
+
+inline cudaEvent_t as_event(void* e) { return reinterpret_cast<cudaEvent_t>(e); }
 
 inline void mark(void* const* ev, int i, cudaStream_t s) {
   if (ev && ev[i]) cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev[i]), s);
@@ -825,7 +834,7 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   mark(ev, 1, s);
   if (fits) w.fits_out = fits;
   if ((st = launch_em_soa<true>(ctx->ops, w.ybar, nll, w, fits, s, reserve,
-                                ev ? reinterpret_cast<cudaEvent_t>(ev[2]) : nullptr)))
+                                ev ? as_event(ev[2]) : nullptr)))
     return st;
   mark(ev, 3, s);
   if (stream_px) {  // split launch: the per-pixel stage runs on its own stream after the EM
@@ -842,10 +851,10 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   }
   PxGeom g{height, width, d.h[n_levels], d.w[n_levels], nll, n_levels, calibration};
   if (ctx->ops.L == 26)
-    st = launch_px_f32<26>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s);
+    st = launch_px_f32<26>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s, ev ? as_event(ev[4]) : nullptr);
   else
-    st = launch_px_f32<0>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s);
-  mark(ev, 4, s);
+    st = launch_px_f32<0>(ctx->ops, src, g, batch, w, thb, so2, hbo, hb, offset, s, ev ? as_event(ev[4]) : nullptr);
+  mark(ev, 5, s);
   return st;
 }
 }  // namespace
@@ -908,6 +917,7 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
   else
     px_f64_kernel<0><<<grid_1d(npx, 128), 128, 0, s>>>(ctx->ops, frames, g, batch, S, w.ybar, cube, hbo, hb, offset);
   st = check_launch("hybrid_px_f64");
-  mark(ev, 4, s);
+  mark(ev, 4, s);  // no separate fixup stage on the fp64 path
+  mark(ev, 5, s);
   return st;
 }

@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kXThreads) em_exact_kernel(const __grid_consta
     if (want) {  // group-uniform
       unsigned long long j = 0;
       if (sub == 0) j = atomicAdd(io.work, 1ull);
-      j = __shfl_sync(__activemask(), j, lead);
+      j = __shfl_sync(((1u << kXLanes) - 1u) << lead, j, lead);
       idx = (int64_t)j < count ? (io.sel ? (int64_t)io.sel[j] : (int64_t)j) : -1;
       if (idx >= 0) {
         y0 = io.y[idx];

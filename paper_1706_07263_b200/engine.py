@@ -1,9 +1,9 @@
 """Batched throughput API for video: THb / SO2 maps for many frames per launch.
 
 ``HybridMapEngine.run`` is the device-resident path benchmarked as ``value``
-(frames already in HBM): five launches per batch (counter reset, low-pass chain
-with the EM start fit, persistent EM, fused per-pixel map, fp64 fixup of the
-flagged pixels).  ``HybridMapEngine.maps_from_host`` is the end-to-end path
+(frames already in HBM): eight launches per batch (counter reset, low-pass chain
+with the EM start fit, fp32 EM lead-in, fp64 EM tail, fused per-pixel map, fp64
+fixup of the flagged pixels with an all-fp64 EM of the few blocks it needs).  ``HybridMapEngine.maps_from_host`` is the end-to-end path
 (``e2e``): pinned host frames -> H2D -> kernels -> D2H of the maps, chunked
 over three streams so copies in both directions overlap the compute.
 
@@ -34,7 +34,7 @@ DEFAULT_EM_LEAD = (16.0, 0.01)
 
 
 def _event_array(events):
-    """5 torch.cuda.Event -> (void*)[5] of their cudaEvent_t handles."""
+    """6 torch.cuda.Event -> (void*)[6] of their cudaEvent_t handles."""
     if events is None:
         return None
     import ctypes
@@ -44,9 +44,9 @@ def _event_array(events):
         if ev.cuda_event == 0:  # created lazily by torch: force creation
             ev.record()
         handles.append(ev.cuda_event)
-    if len(handles) != 5:
-        raise ArgumentError("stage_events: 5 events (before low-pass, EM lead-in, EM fp64, per-pixel; after)")
-    return (ctypes.c_void_p * 5)(*handles)
+    if len(handles) != 6:
+        raise ArgumentError("stage_events: 6 events (before low-pass, EM lead-in, EM fp64, per-pixel, fixup; after)")
+    return (ctypes.c_void_p * 6)(*handles)
 
 
 @dataclass
@@ -64,8 +64,8 @@ class HybridMapEngine:
     """Hybrid estimator for (B, H, W, 3) float32 frame batches on one GPU."""
 
     # zero_counters, ll_kernel (+ EM fit #1), em_lead_kernel, em_persistent_kernel (tail),
-    # px_f32_kernel, px_fallback_kernel
-    KERNELS_PER_RUN = 6
+    # px_f32_kernel, px_fallback_kernel (classify), em_exact_kernel, px_fallback_kernel (deferred)
+    KERNELS_PER_RUN = 8
 
     def __init__(
         self,

@@ -45,14 +45,14 @@ def main():
         out = eng.allocate(batch, H, W, fits=True)
         for _ in range(3):
             eng.launch(frames, out)
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(5)]
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(5)]
         for e in evs:
             eng.launch(frames, out, stage_events=e)
         torch.cuda.synchronize()
         eng.check_flags(out)
-        st = [sum(e[i].elapsed_time(e[i + 1]) for e in evs) / len(evs) / batch * 1e3 for i in range(4)]
+        st = [sum(e[i].elapsed_time(e[i + 1]) for e in evs) / len(evs) / batch * 1e3 for i in range(5)]
         rec = {"schedule": spec, "ll_us": round(st[0], 2), "lead_us": round(st[1], 2), "tail_us": round(st[2], 2),
-               "px_us": round(st[3], 2), "total_us": round(sum(st), 2), **eng.em_counters(batch, H, W)}
+               "px_us": round(st[3], 2), "fixup_us": round(st[4], 2), "total_us": round(sum(st), 2), **eng.em_counters(batch, H, W)}
         thb, so2, fits = out.thb.double(), out.so2.double(), out.fits.clone()
         if ref is None:
             ref = (thb, so2, fits)
