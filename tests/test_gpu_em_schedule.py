@@ -1,0 +1,124 @@
+"""GPU tests of the EM precision schedule of the fp32 map path (oxm_em.cuh:
+fp32 lead-in -> fp64 tail with guard-band restarts -> all-fp64 re-estimate of
+the blocks holding "sensitive" fallback pixels).
+
+The schedule must not change any discrete decision: per-coefficient fit
+counts equal the all-fp64 schedule's (which equal the oracle's,
+test_gpu_pipeline.py), and maps stay within a small multiple of fp32
+rounding of the all-fp64 schedule, far inside the north-star tolerances."""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1706_07263_b200 as ox
+from oracle import oximap_oracle as O
+from paper_1706_07263_b200 import _native, synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(cuda, sensitivity, basis, frames, n, em_lead):
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=n), em_lead=em_lead)
+    x = torch.from_numpy(frames.astype(np.float32)).to(cuda)
+    out = eng.run(x, fits=True)
+    torch.cuda.synchronize()
+    B, H, W = frames.shape[:3]
+    return eng, out, eng.em_counters(B, H, W)
+
+
+def _maps(out):
+    return out.thb.double().cpu().numpy(), out.so2.double().cpu().numpy(), out.fits.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def textured(sensitivity, basis):
+    # 2 textured 1080p frames: thousands of fallback pixels, some sensitive
+    return np.stack([synth.phantom_rgb_f32(1080, 1920, s, sensitivity, basis) for s in (11, 12)])
+
+
+def test_schedule_matches_all_fp64(cuda, sensitivity, basis, textured):
+    _, ref, c0 = _run(cuda, sensitivity, basis, textured, 2, None)
+    assert c0["lead_fits"] == 0 and c0["exact_blocks"] == 0
+    rt, rs, rf = _maps(ref)
+    for lead in ((16.0, 0.01), (8.0, 0.01), (64.0, 0.01)):
+        _, out, c = _run(cuda, sensitivity, basis, textured, 2, lead)
+        t, s, f = _maps(out)
+        assert np.array_equal(f, rf), f"{lead}: {np.sum(f != rf)} fit-count differences"
+        assert np.array_equal(np.isnan(s), np.isnan(rs))
+        ok = ~np.isnan(rs)
+        assert np.max(np.abs(t - rt) / np.abs(rt)) < 1e-5, lead
+        assert np.max(np.abs(s[ok] - rs[ok])) < 5e-6, lead
+        assert c["lead_fits"] > 0 and c["tail_fits"] > 0
+        # the counters account for every fit past fit #1 (restarted work on top)
+        assert c["lead_fits"] + c["tail_fits"] >= int(f.sum()) - f.size
+        assert c["exact_blocks"] > 0  # textured 1080p frames always hold sensitive fallback pixels
+
+
+def test_schedule_vs_oracle_textured(cuda, sensitivity, basis, textured):
+    _, out, _ = _run(cuda, sensitivity, basis, textured[:1], 2, (16.0, 0.01))
+    ref = O.estimate_frame(textured[0], sensitivity.c, basis.xi, n_levels=2, want_cube=False,
+                           threads=O.default_threads())
+    t, s, f = _maps(out)
+    assert np.array_equal(f[0], ref["fits"])
+    assert np.array_equal(np.isnan(s[0]), np.isnan(ref["so2"]))
+    assert np.all(np.abs(t[0] - ref["thb"]) <= 1e-4 * np.abs(ref["thb"]))
+    ok = ~np.isnan(ref["so2"])
+    assert np.max(np.abs(s[0][ok] - ref["so2"][ok])) <= 1e-5
+
+
+def test_exact_blocks_needed(cuda, sensitivity, basis, textured):
+    """Without the exact re-estimate the sensitive fallback pixels carry the
+    schedule's spectrum deviation amplified by cancellation (the reason the
+    pass exists); fit counts are still exact."""
+    _, ref, _ = _run(cuda, sensitivity, basis, textured, 2, None)
+    _, out, c = _run(cuda, sensitivity, basis, textured, 2, (16.0, 0.01, 0.0))
+    assert c["exact_blocks"] == 0
+    rt, rs, rf = _maps(ref)
+    t, s, f = _maps(out)
+    assert np.array_equal(f, rf)
+    with_exact = _maps(_run(cuda, sensitivity, basis, textured, 2, (16.0, 0.01))[1])
+    dev_without = np.max(np.abs(t - rt) / np.abs(rt))
+    dev_with = np.max(np.abs(with_exact[0] - rt) / np.abs(rt))
+    assert dev_with < dev_without
+
+
+def test_schedule_deterministic(cuda, sensitivity, basis, textured):
+    eng, a, _ = _run(cuda, sensitivity, basis, textured, 2, (16.0, 0.01))
+    b = eng.run(torch.from_numpy(textured.astype(np.float32)).to(cuda), fits=True)
+    assert torch.equal(a.thb, b.thb)
+    assert torch.equal(a.so2.nan_to_num(-1.0), b.so2.nan_to_num(-1.0))
+    assert torch.equal(a.fits, b.fits)
+
+
+def test_max_iters_small_with_lead(cuda, sensitivity, basis):
+    """max_iters 2 and 3: the lead-in may commit no fit / one fit; counts and
+    maps must still equal the oracle's (capped coefficients restart exactly)."""
+    rgb = synth.phantom_rgb_f32(64, 96, 3, sensitivity, basis)
+    for it in (2, 3):
+        cfg = ox.PipelineConfig(n_levels=2, bayes=ox.BayesConfig(max_iters=it))
+        eng = ox.HybridMapEngine(sensitivity, basis, cfg)
+        out = eng.run(torch.from_numpy(rgb[None].astype(np.float32)).to(cuda), fits=True)
+        ref = O.estimate_frame(rgb, sensitivity.c, basis.xi, n_levels=2, max_iters=it, want_cube=False)
+        assert np.array_equal(out.fits[0].cpu().numpy(), ref["fits"]), it
+        assert np.all(np.abs(out.thb[0].cpu().numpy() - ref["thb"]) <= 1e-4 * np.abs(ref["thb"]))
+
+
+def test_set_em_lead_validation(cuda, sensitivity, basis):
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2), em_lead=None)
+    lib, h = _native.load(), eng.ctx.handle
+    ok, bad = _native.OXM_OK, _native.OXM_ERR_ARGUMENT
+    assert lib.oxm_ctx_set_em_lead(h, 16.0, 0.01, 2e-3) == ok
+    assert lib.oxm_ctx_set_em_lead(h, 0.0, 0.01, 0.0) == ok   # all-fp64
+    assert lib.oxm_ctx_set_em_lead(h, 1e4, 0.01, 0.0) == bad  # ratio * tol >= 1
+    assert lib.oxm_ctx_set_em_lead(h, 16.0, 1.0, 0.0) == bad  # guard >= 1
+    assert lib.oxm_ctx_set_em_lead(h, 16.0, 0.0, 0.0) == bad  # lead-in without a guard band
+    assert lib.oxm_ctx_set_em_lead(h, -1.0, 0.01, 0.0) == bad
+    assert lib.oxm_ctx_set_em_lead(h, 16.0, 0.01, -1.0) == bad
+    assert lib.oxm_ctx_set_em_lead(None, 16.0, 0.01, 0.0) == bad
+    out = (ctypes.c_uint64 * 4)()
+    assert lib.oxm_hybrid_em_counters(None, None, 1, 8, 8, 1, out, None) == bad
