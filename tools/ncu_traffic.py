@@ -4,8 +4,8 @@ DRAM bytes (read + write) per frame for each bench stage.
     python tools/ncu_traffic.py rep.ncu-rep FRAMES_PER_LAUNCH"""
 import csv, io, json, pathlib, subprocess, sys
 
-STAGES = {"ll_kernel": ("ll_kernel",), "em": ("em_persistent", "em_spectra"),
-          "px_f32_kernel": ("px_f32", "px_fallback")}
+STAGES = {"ll_kernel": ("ll_kernel",), "em_lead": ("em_lead",), "em": ("em_persistent",),
+          "px_f32_kernel": ("px_f32",), "fixup": ("px_fallback", "em_exact")}
 
 
 def main():

@@ -32,7 +32,7 @@ def main():
     tag = "r01"
     (P / f"{tag}_launches.txt").write_text(launches(lcsv))
     summ = subprocess.run([sys.executable, str(ROOT / "tools" / "ncu_summary.py"), rep], capture_output=True, text=True).stdout
-    for k in ("em_init", "em_persistent", "px_f32", "px_fallback", "ll_kernel"):
+    for k in ("em_lead", "em_persistent", "em_exact", "px_f32", "px_fallback", "ll_kernel"):
         summ += f"== opcode mix {k}\n" + subprocess.run(
             [sys.executable, str(ROOT / "tools" / "ncu_opmix.py"), rep, k, "--top", "16"], capture_output=True, text=True).stdout
     (P / f"{tag}_ncu_summary.txt").write_text(f"source: {rep} (tools/profile_hybrid.py, {frames} frames per launch)\n" + summ)
