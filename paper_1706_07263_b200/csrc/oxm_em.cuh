@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
   int64_t idx[NS];
   int nfit[NS];
   bool exact[NS];  // TAIL: this lane runs the coefficient from fit #1 (no guard)
-  unsigned tsteps = 0, trestarts = 0;  // TAIL work counters (io.stats)
+  unsigned long long wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats)
   double y[NS][3], x[NS][3];
   auto load = [&](int sl, int64_t i) {
     int f = 1;
@@ -338,14 +338,15 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     }
   };
 
-  auto any_active = [&]() {
-    bool a = false;
+  for (;;) {
+    unsigned act = 0;
 #pragma unroll
-    for (int sl = 0; sl < NS; ++sl) a |= idx[sl] >= 0;
-    return __any_sync(0xffffffffu, a);
-  };
-
-  while (any_active()) {
+    for (int sl = 0; sl < NS; ++sl) act |= __ballot_sync(0xffffffffu, idx[sl] >= 0);
+    if (!act) break;
+    if constexpr (TAIL) {
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) wsteps += __popc(__ballot_sync(0xffffffffu, idx[sl] >= 0));
+    }
     // ---- phase A: expected spectrum e = exp(-xi x) and residual r = y - C e
     double c[NS][3], x2s[NS];
 #pragma unroll
@@ -395,7 +396,6 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
       bool done = false, restart = false;
       if (idx[sl] >= 0) {
         ++nfit[sl];
-        if constexpr (TAIL) ++tsteps;
         const double d0 = n0 - x[sl][0], d1 = n1 - x[sl][1], d2 = n2 - x[sl][2];
         const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
         const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x[sl][0], x[sl][0]), __dmul_rn(x[sl][1], x[sl][1])),
@@ -408,7 +408,6 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
           // trusted -- redo the coefficient in exact fp64 from fit #1
           restart = !exact[sl] && ((dn2 > ops.guard_lo * xm2 && dn2 < ops.guard_hi * xm2) || nfit[sl] >= ops.max_iters);
           if (restart) {
-            ++trestarts;
             done = false;
             exact[sl] = true;
             nfit[sl] = 1;
@@ -431,18 +430,18 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
         x[sl][1] = n1;
         x[sl][2] = n2;
       }
+      if constexpr (TAIL) wrestarts += __popc(__ballot_sync(0xffffffffu, restart));
       const unsigned m = __ballot_sync(0xffffffffu, done);
-      if (TAIL && m && io.stats) {
-        warp_count(io.stats + 1, done ? tsteps : 0u, lane);
-        warp_count(io.stats + 2, done ? trestarts : 0u, lane);
-        if (done) tsteps = trestarts = 0;
-      }
       if (m) {
         // the whole warp streams the finished lanes' spectra out, then refills them
         write_spectra<KL, OUT>(io, e - lane + sl * (L + kEmColExtra) * es, es, L, m, lane, gsm, eps);
         refill(sl, m, done);
       }
     }
+  }
+  if (TAIL && io.stats && lane == 0) {
+    atomicAdd(io.stats + 1, wsteps);
+    atomicAdd(io.stats + 2, wrestarts);
   }
 }
 
@@ -452,7 +451,7 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
 // The iteration of bayes.py:185-207 contracts (rel shrinks ~2x per fit), and a
 // "not converged" decision taken while rel is far above tol is insensitive to
 // fp32 error.  So the first fits run here in fp32 -- MUFU ex2/lg2 and FFMA
-// instead of the fp64 pipe -- for as long as |dx| > K tol |x| (K = 64 by
+// instead of the fp64 pipe -- for as long as |dx| > K tol |x| (K = 16 by
 // default: ops.lead_thr_f = (K tol)^2) and the next fit is not the last
 // allowed one.  The step that fails the test is not committed: the state
 // before it (x after fit k, and k) is handed to the fp64 tail
