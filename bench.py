@@ -45,7 +45,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--batch", type=int, default=32, help="frames per step per GPU")
+    p.add_argument("--batch", type=int, default=64, help="frames per step per GPU")
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--levels", type=int, default=2)

@@ -99,11 +99,11 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
   }
   const double log2e = 1.44269504088896340736;
   for (int l = 0; l < L; ++l) {
-    d.xl2_f[l][0] = static_cast<float>(-log2e * d.xi[l][0]);
-    d.xl2_f[l][1] = static_cast<float>(-log2e * d.xi[l][1]);
+    d.xl2_t[0][l] = static_cast<float>(-log2e * d.xi[l][0]);
+    d.xl2_t[1][l] = static_cast<float>(-log2e * d.xi[l][1]);
     for (int k = 0; k < 3; ++k) {
       d.sens_f[k][l] = static_cast<float>(d.sens[k][l]);
-      d.gain_f[l][k] = static_cast<float>(d.gain[l][k]);
+      d.gain_t[k][l] = static_cast<float>(d.gain[l][k]);
     }
   }
   set_em_lead(d, kDefaultLeadRatio, kDefaultLeadGuard, d.fallback_below);

@@ -22,9 +22,10 @@ struct DevOps {
   float2 solve_f2[kMaxBands][3];   // the same, duplicated into both halves for FFMA2
   float2 fitl2_f2[3][kMaxBands];
   // fp32 lead-in of the EM (oxm_em.cuh, em_lead_kernel)
-  float xl2_f[kMaxBands][2];  // -xi[:, 0:2] * log2(e): e = 2^(xl2 . x - log2(e) x2)
+  // (band-major rows: bands l, l+1 form one float2 FFMA2 operand)
+  float xl2_t[2][kMaxBands];  // -xi[:, 0:2]^T * log2(e): e = 2^(xl2 . x - log2(e) x2)
   float sens_f[3][kMaxBands];
-  float gain_f[kMaxBands][3];
+  float gain_t[3][kMaxBands];  // gain^T
   float lead_thr_f;  // (K tol)^2: fp32 steps continue while |dx|^2 > lead_thr |x|^2; 0 = no lead-in
   float eps_f;
   int L;

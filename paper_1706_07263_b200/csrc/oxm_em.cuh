@@ -338,11 +338,14 @@ __global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_k
     }
   };
 
-  for (;;) {
-    unsigned act = 0;
+  auto any_active = [&]() {
+    bool a = false;
 #pragma unroll
-    for (int sl = 0; sl < NS; ++sl) act |= __ballot_sync(0xffffffffu, idx[sl] >= 0);
-    if (!act) break;
+    for (int sl = 0; sl < NS; ++sl) a |= idx[sl] >= 0;
+    return __any_sync(0xffffffffu, a);
+  };
+
+  while (any_active()) {
     if constexpr (TAIL) {
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) wsteps += __popc(__ballot_sync(0xffffffffu, idx[sl] >= 0));
@@ -490,27 +493,37 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
   if (idx >= 0) load(idx);
   next = stop;
 
+  // bands l, l+1 share one packed FFMA2 (two partial sums per accumulator,
+  // added at the end: the lead-in needs no particular summation order)
+  static_assert(KL % 2 == 0, "band pairs");
+  auto pair = [](const float* row, int l) { return *reinterpret_cast<const float2*>(row + l); };
+  auto dup = [](float v) { return make_float2(v, v); };
   while (__any_sync(0xffffffffu, idx >= 0)) {
-    float e[KL];
-    float c0 = 0.f, c1 = 0.f, c2 = 0.f;
-    const float x2t = -kLog2e * x2;  // xi[:, 2] == 1
+    float2 e[KL / 2];
+    float2 c0 = dup(0.f), c1 = c0, c2 = c0;
+    const float2 X0 = dup(x0), X1 = dup(x1), X2 = dup(-kLog2e * x2);  // xi[:, 2] == 1
 #pragma unroll
-    for (int l = 0; l < KL; ++l) {
-      e[l] = ex2_approx(fmaf(ops.xl2_f[l][0], x0, fmaf(ops.xl2_f[l][1], x1, x2t)));
-      c0 = fmaf(ops.sens_f[0][l], e[l], c0);
-      c1 = fmaf(ops.sens_f[1][l], e[l], c1);
-      c2 = fmaf(ops.sens_f[2][l], e[l], c2);
+    for (int q = 0; q < KL / 2; ++q) {
+      const int l = 2 * q;
+      const float2 t = __ffma2_rn(pair(ops.xl2_t[0], l), X0, __ffma2_rn(pair(ops.xl2_t[1], l), X1, X2));
+      e[q] = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+      c0 = __ffma2_rn(pair(ops.sens_f[0], l), e[q], c0);
+      c1 = __ffma2_rn(pair(ops.sens_f[1], l), e[q], c1);
+      c2 = __ffma2_rn(pair(ops.sens_f[2], l), e[q], c2);
     }
-    const float r0 = y0 - c0, r1 = y1 - c1, r2 = y2 - c2;
-    float n0 = 0.f, n1 = 0.f, n2 = 0.f;
+    const float2 R0 = dup(y0 - (c0.x + c0.y)), R1 = dup(y1 - (c1.x + c1.y)), R2 = dup(y2 - (c2.x + c2.y));
+    float2 m0 = dup(0.f), m1 = m0, m2 = m0;
 #pragma unroll
-    for (int l = 0; l < KL; ++l) {
-      const float sv = fmaxf(fmaf(ops.gain_f[l][2], r2, fmaf(ops.gain_f[l][1], r1, fmaf(ops.gain_f[l][0], r0, e[l]))), eps);
-      const float lg = lg2_approx(sv);
-      n0 = fmaf(ops.fitl2_f[0][l], lg, n0);
-      n1 = fmaf(ops.fitl2_f[1][l], lg, n1);
-      n2 = fmaf(ops.fitl2_f[2][l], lg, n2);
+    for (int q = 0; q < KL / 2; ++q) {
+      const int l = 2 * q;
+      const float2 sv = __ffma2_rn(pair(ops.gain_t[2], l), R2,
+                                   __ffma2_rn(pair(ops.gain_t[1], l), R1, __ffma2_rn(pair(ops.gain_t[0], l), R0, e[q])));
+      const float2 lg = make_float2(lg2_approx(fmaxf(sv.x, eps)), lg2_approx(fmaxf(sv.y, eps)));
+      m0 = __ffma2_rn(pair(ops.fitl2_f[0], l), lg, m0);
+      m1 = __ffma2_rn(pair(ops.fitl2_f[1], l), lg, m1);
+      m2 = __ffma2_rn(pair(ops.fitl2_f[2], l), lg, m2);
     }
+    const float n0 = m0.x + m0.y, n1 = m1.x + m1.y, n2 = m2.x + m2.y;
     bool done = false;
     if (idx >= 0) {
       const float d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
