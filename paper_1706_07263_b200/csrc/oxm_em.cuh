@@ -36,6 +36,12 @@
 #ifndef OXM_EM_SLOTS
 #define OXM_EM_SLOTS 1
 #endif
+#ifndef OXM_TAIL_MIN_BLOCKS
+#define OXM_TAIL_MIN_BLOCKS 5
+#endif
+#ifndef OXM_X_MIN_BLOCKS
+#define OXM_X_MIN_BLOCKS 1
+#endif
 #ifndef OXM_EM_MIN_BLOCKS
 #define OXM_EM_MIN_BLOCKS 5
 #endif
@@ -245,8 +251,8 @@ __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol
 // whose rel lands within the guard band around tol, or a tail that runs into
 // max_iters, restarts its coefficient from fit #1 in exact fp64 mode.
 template <int KL, SpecOut OUT, bool TAIL = false>
-__global__ void __launch_bounds__(kEmThreads, OXM_EM_MIN_BLOCKS) em_persistent_kernel(const __grid_constant__ DevOps ops,
-                                                                                        EmIO io) {
+__global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_EM_MIN_BLOCKS)
+    em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
   constexpr int NS = kEmSlots;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
@@ -663,7 +669,7 @@ struct alignas(16) XBand {  // per-band operator row, staged in shared memory (l
 };
 
 template <int KL, SpecOut OUT>
-__global__ void __launch_bounds__(kXThreads) em_exact_kernel(const __grid_constant__ DevOps ops, EmIO io) {
+__global__ void __launch_bounds__(kXThreads, OXM_X_MIN_BLOCKS) em_exact_kernel(const __grid_constant__ DevOps ops, EmIO io) {
   static_assert(KL > 0, "fixed band count");
   constexpr int NB = (KL + kXLanes - 1) / kXLanes;  // bands per lane
   __shared__ MathSmem mt;

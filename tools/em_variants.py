@@ -14,9 +14,12 @@ import sys
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-VARIANTS = {  # name -> extra -D defines (the last sweep: EM slots / occupancy)
+VARIANTS = {  # name -> extra -D defines (the last sweep: tail / exact-pass occupancy)
     "base": (),
-    "m4": ("OXM_EM_MIN_BLOCKS=4",),
+    "tail4": ("OXM_TAIL_MIN_BLOCKS=4",),
+    "tail6": ("OXM_TAIL_MIN_BLOCKS=6",),
+    "x8": ("OXM_X_MIN_BLOCKS=8",),
+    "x10": ("OXM_X_MIN_BLOCKS=10",),
 }
 
 
