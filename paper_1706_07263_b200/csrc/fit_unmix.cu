@@ -53,27 +53,31 @@ __global__ void __launch_bounds__(kRows) unmix_kernel(const __grid_constant__ Ma
   for (int64_t k = threadIdx.x; k < cnt * L; k += kRows) dst[k] = sout[k];
 }
 
-template <typename T>
+// KL > 0: band count fixed at compile time (staging index math by constant
+// division, band loop unrolled); KL == 0: generic L.  32-bit index math
+// inside a CTA slab (cnt * L <= kRows * kMaxBands).
+template <typename T, int KL>
 __global__ void __launch_bounds__(kRows) fit_kernel(const __grid_constant__ DevOps ops, const T* __restrict__ cube,
                                                     int64_t n, double cal, T* __restrict__ hbo, T* __restrict__ hb,
                                                     T* __restrict__ off) {
   extern __shared__ unsigned char smem_raw[];
   T* stage = reinterpret_cast<T*>(smem_raw);
-  const int L = ops.L;
+  const int L = KL > 0 ? KL : ops.L;
   const int LS = L | 1;  // odd row stride: conflict-free per-thread row walks
   const int64_t base = (int64_t)blockIdx.x * kRows;
-  const int64_t cnt = min64(kRows, n - base);
+  const int cnt = (int)min64(kRows, n - base);
   const T* src = cube + base * L;
-  for (int64_t k = threadIdx.x; k < cnt * L; k += kRows) {
-    const int64_t r = k / L, l = k - r * L;
+  for (int k = threadIdx.x; k < cnt * L; k += kRows) {
+    const int r = k / L, l = k - r * L;
     stage[r * LS + l] = ldg(src + k);
   }
   __syncthreads();
-  if (threadIdx.x >= cnt) return;
+  if ((int)threadIdx.x >= cnt) return;
   const T* row = stage + threadIdx.x * LS;
   T x0, x1, x2;
   if constexpr (sizeof(T) == 8) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+#pragma unroll(KL > 0 ? KL : 1)
     for (int l = 0; l < L; ++l) {
       const double lg = log(fmax((double)row[l], ops.eps));
       a0 = fma(ops.fitm[0][l], lg, a0);
@@ -85,6 +89,7 @@ __global__ void __launch_bounds__(kRows) fit_kernel(const __grid_constant__ DevO
     x2 = -a2;
   } else {
     float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll(KL > 0 ? KL : 1)
     for (int l = 0; l < L; ++l) {
       const float lg = __log2f(fmaxf((float)row[l], ops.eps_f));
       a0 = fmaf(ops.fitl2_f[0][l], lg, a0);
@@ -145,9 +150,9 @@ int fit_impl(const oxm_ctx* ctx, const T* cube, int64_t n, double cal, T* hbo, T
   if (n == 0) return OXM_OK;
   DeviceGuard dg(ctx->device);
   const size_t smem = sizeof(T) * kRows * (ctx->ops.L | 1);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(fit_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  fit_kernel<T><<<grid_1d(n, kRows), kRows, smem, s>>>(ctx->ops, cube, n, cal, hbo, hb, off);
+  auto kern = ctx->ops.L == 26 ? fit_kernel<T, 26> : fit_kernel<T, 0>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<grid_1d(n, kRows), kRows, smem, s>>>(ctx->ops, cube, n, cal, hbo, hb, off);
   return check_launch("fit");
 }
 

@@ -28,6 +28,26 @@ struct FwdGeom {
   int64_t off[kMaxPass + 1][4];              // element offsets of lp,dh,dv,dd per level (1..NL)
 };
 
+// t -> (channel c, column J, row I) of the coarsest plane; 32-bit divisions
+// whenever the index space fits (64-bit division is a ~70-instruction
+// sequence, which made these streaming kernels issue-bound)
+__device__ __forceinline__ void split_index(int64_t t, int64_t total, int64_t C, int64_t w, int64_t& c, int64_t& J,
+                                            int64_t& I) {
+  if (total <= 0xffffffffll) {
+    const uint32_t tt = (uint32_t)t, CC = (uint32_t)C, ww = (uint32_t)w;
+    const uint32_t rest = tt / CC;
+    c = tt - rest * CC;
+    const uint32_t Ii = rest / ww;
+    J = rest - Ii * ww;
+    I = Ii;
+  } else {
+    c = t % C;
+    const int64_t rest = t / C;
+    J = rest % w;
+    I = rest / w;
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ bool is_bad(T v) {
   return !isfinite(v);
@@ -40,10 +60,8 @@ __global__ void __launch_bounds__(256) haar_fwd_kernel(const T* __restrict__ src
   const int64_t C = g.C;
   const int64_t total = g.h[NL] * g.w[NL] * C;
   if (t >= total) return;
-  const int64_t c = t % C;
-  const int64_t rest = t / C;
-  const int64_t J = rest % g.w[NL];
-  const int64_t I = rest / g.w[NL];
+  int64_t c, J, I;
+  split_index(t, total, C, g.w[NL], c, J, I);
   constexpr int S0 = 1 << NL;
 
   T p[S0][S0];
@@ -109,10 +127,8 @@ __global__ void __launch_bounds__(256) haar_inv_kernel(const T* __restrict__ top
   const int64_t C = g.C;
   const int64_t total = g.h[NL] * g.w[NL] * C;
   if (t >= total) return;
-  const int64_t c = t % C;
-  const int64_t rest = t / C;
-  const int64_t J = rest % g.w[NL];
-  const int64_t I = rest / g.w[NL];
+  int64_t c, J, I;
+  split_index(t, total, C, g.w[NL], c, J, I);
   constexpr int S0 = 1 << NL;
 
   T p[S0][S0];
