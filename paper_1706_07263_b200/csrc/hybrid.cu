@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
     for (int k = 0; k < kPer; ++k) {
       const int l = sub + kFbLanes * k;
       if (l < L) {
-        const double S = (double)ldg(hi + l) + (double)ldg(lo + l);
+        // classify: the tail stored hi parts only (insensitive pixels need no more; the
+        // sensitive ones are recomputed from the exact pass's hi + lo)
+        const double S = MODE == kFbClassify ? (double)ldg(hi + l) : (double)ldg(hi + l) + (double)ldg(lo + l);
         sp[k] = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
         sens |= sp[k] >= lo_b && sp[k] < hi_b;
       }
@@ -677,6 +679,8 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
     io.xh = w.xh;
     io.lead_work = w.lead_work;
     io.stats = w.em_stats;
+    // with the exact-block pass, only its blocks' lo parts are ever read
+    if (exact_blocks_active(ops)) io.Slo = nullptr;
   }
   constexpr SpecOut out = F32OUT ? SpecOut::kAosF32HiLo : SpecOut::kSoaF64;
   if (ops.L == 26) return launch_em<26, out>(ops, io, s, split);

@@ -301,7 +301,6 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
     }
     nfit[sl] = f;
     exact[sl] = f <= 1;
-    e[(sl * (L + kEmColExtra) + L + 3) * es] = __longlong_as_double(i);  // for write_spectra
   };
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) {
@@ -312,6 +311,7 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
 #pragma unroll
     for (int k = 0; k < 3; ++k) y[sl][k] = x[sl][k] = 0.0;
     if (idx[sl] >= 0) load(sl, idx[sl]);
+    e[(sl * (L + kEmColExtra) + L + 3) * es] = __longlong_as_double(idx[sl]);  // for write_spectra
   }
   next = stop;
 
@@ -443,8 +443,13 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
       const unsigned m = __ballot_sync(0xffffffffu, done);
       if (m) {
         // the whole warp streams the finished lanes' spectra out, then refills them
-        write_spectra<KL, OUT>(io, e - lane + sl * (L + kEmColExtra) * es, es, L, m, lane, gsm, eps);
+        // refill first: the new coefficients' global loads are in flight while
+        // the warp streams the finished spectra out (which reads the old
+        // index rows, so the new ones are stored afterwards)
         refill(sl, m, done);
+        write_spectra<KL, OUT>(io, e - lane + sl * (L + kEmColExtra) * es, es, L, m, lane, gsm, eps);
+        __syncwarp();
+        if (done) e[(sl * (L + kEmColExtra) + L + 3) * es] = __longlong_as_double(idx[sl]);
       }
     }
   }
