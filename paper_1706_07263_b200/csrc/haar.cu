@@ -48,32 +48,31 @@ __device__ __forceinline__ void split_index(int64_t t, int64_t total, int64_t C,
   }
 }
 
-template <typename T>
-__device__ __forceinline__ bool is_bad(T v) {
-  return !isfinite(v);
-}
 
-template <typename T, int NL>
+// IT: index type -- int32_t whenever the source plane and every output plane
+// fit (the launcher checks), so the per-thread address math is 32-bit.
+template <typename T, int NL, typename IT>
 __global__ void __launch_bounds__(256) haar_fwd_kernel(const T* __restrict__ src, FwdGeom g,
                                                        T* __restrict__ out, uint32_t* flags) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t C = g.C;
-  const int64_t total = g.h[NL] * g.w[NL] * C;
+  const int64_t total = g.h[NL] * g.w[NL] * g.C;
   if (t >= total) return;
-  int64_t c, J, I;
-  split_index(t, total, C, g.w[NL], c, J, I);
+  int64_t c64, J64, I64;
+  split_index(t, total, g.C, g.w[NL], c64, J64, I64);
+  const IT C = (IT)g.C, c = (IT)c64, J = (IT)J64, I = (IT)I64;
+  const IT H0 = (IT)g.h[0], W0 = (IT)g.w[0];
   constexpr int S0 = 1 << NL;
 
   T p[S0][S0];
   bool bad = false;
 #pragma unroll
   for (int r = 0; r < S0; ++r) {
-    const int64_t row = min(I * S0 + r, g.h[0] - 1);
+    const IT row = min(I * S0 + r, H0 - 1);
 #pragma unroll
     for (int s = 0; s < S0; ++s) {
-      const int64_t col = min(J * S0 + s, g.w[0] - 1);
-      const T v = ldg(src + (row * g.w[0] + col) * C + c);
-      bad |= is_bad(v);
+      const IT col = min(J * S0 + s, W0 - 1);
+      const T v = ldg(src + (row * W0 + col) * C + c);
+      bad |= !isfinite(v);
       p[r][s] = v;
     }
   }
@@ -83,15 +82,20 @@ __global__ void __launch_bounds__(256) haar_fwd_kernel(const T* __restrict__ src
   for (int k = 0; k < NL; ++k) {
     const int Sk = S0 >> k;
     const int Sn = Sk >> 1;
-    const int64_t br = I * Sk, bc = J * Sk;  // global position of p[0][0] at level k
-    const int64_t hn = g.h[k + 1], wn = g.w[k + 1];
+    const IT br = I * Sk, bc = J * Sk;  // global position of p[0][0] at level k
+    const IT hk = (IT)g.h[k], wk = (IT)g.w[k];
+    const IT hn = (IT)g.h[k + 1], wn = (IT)g.w[k + 1];
+    T* const o0 = out + g.off[k + 1][0];
+    T* const o1 = out + g.off[k + 1][1];
+    T* const o2 = out + g.off[k + 1][2];
+    T* const o3 = out + g.off[k + 1][3];
 #pragma unroll
     for (int i = 0; i < Sn; ++i) {
 #pragma unroll
       for (int j = 0; j < Sn; ++j) {
         // edge replication: the odd partner row/col falls back to its twin
-        const bool rowok = br + 2 * i + 1 < g.h[k];
-        const bool colok = bc + 2 * j + 1 < g.w[k];
+        const bool rowok = br + 2 * i + 1 < hk;
+        const bool colok = bc + 2 * j + 1 < wk;
         const T a = p[2 * i][2 * j];
         const T b = colok ? p[2 * i][2 * j + 1] : a;
         const T cc = rowok ? p[2 * i + 1][2 * j] : a;
@@ -100,13 +104,13 @@ __global__ void __launch_bounds__(256) haar_fwd_kernel(const T* __restrict__ src
         const T dh = T(0.5) * (((a + b) - cc) - d);
         const T dv = T(0.5) * (((a - b) - cc) + d);
         const T dd = T(0.5) * (((a - b) + cc) - d);
-        const int64_t gi = (br >> 1) + i, gj = (bc >> 1) + j;
+        const IT gi = (br >> 1) + i, gj = (bc >> 1) + j;
         if (gi < hn && gj < wn) {
-          const int64_t e = (gi * wn + gj) * C + c;
-          out[g.off[k + 1][0] + e] = lp;
-          out[g.off[k + 1][1] + e] = dh;
-          out[g.off[k + 1][2] + e] = dv;
-          out[g.off[k + 1][3] + e] = dd;
+          const IT e = (gi * wn + gj) * C + c;
+          o0[e] = lp;
+          o1[e] = dh;
+          o2[e] = dv;
+          o3[e] = dd;
         }
         p[i][j] = lp;  // (i,j) <= (2i,2j): only already-consumed windows are overwritten
       }
@@ -120,44 +124,48 @@ struct InvGeom {
   int64_t off[kMaxPass + 1][3];              // dh,dv,dd element offsets at level l (1..NL)
 };
 
-template <typename T, int NL>
+template <typename T, int NL, typename IT>
 __global__ void __launch_bounds__(256) haar_inv_kernel(const T* __restrict__ top, const T* __restrict__ dirs,
                                                        InvGeom g, T* __restrict__ out) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t C = g.C;
-  const int64_t total = g.h[NL] * g.w[NL] * C;
+  const IT C = (IT)g.C;
+  const int64_t total = g.h[NL] * g.w[NL] * g.C;
   if (t >= total) return;
-  int64_t c, J, I;
-  split_index(t, total, C, g.w[NL], c, J, I);
+  int64_t c64, J64, I64;
+  split_index(t, total, g.C, g.w[NL], c64, J64, I64);
+  const IT c = (IT)c64, J = (IT)J64, I = (IT)I64;
   constexpr int S0 = 1 << NL;
 
   T p[S0][S0];
-  p[0][0] = ldg(top + (I * g.w[NL] + J) * C + c);
+  p[0][0] = ldg(top + (I * (IT)g.w[NL] + J) * C + c);
 #pragma unroll
   for (int l = NL; l >= 1; --l) {
     const int Sl = 1 << (NL - l);  // positions per side owned at level l
-    const int64_t br = I * Sl, bc = J * Sl;
-    const int64_t hl = g.h[l], wl = g.w[l];
-    const int64_t ho = g.h[l - 1], wo = g.w[l - 1];
+    const IT br = I * Sl, bc = J * Sl;
+    const IT hl = (IT)g.h[l], wl = (IT)g.w[l];
+    const IT ho = (IT)g.h[l - 1], wo = (IT)g.w[l - 1];
+    const T* const d0 = dirs + g.off[l][0];
+    const T* const d1 = dirs + g.off[l][1];
+    const T* const d2 = dirs + g.off[l][2];
     // walk backwards so in-place expansion never overwrites an unread parent
 #pragma unroll
     for (int i = Sl - 1; i >= 0; --i) {
 #pragma unroll
       for (int j = Sl - 1; j >= 0; --j) {
-        const int64_t gi = br + i, gj = bc + j;
+        const IT gi = br + i, gj = bc + j;
         T lp = p[i][j], dh = T(0), dv = T(0), dd = T(0);
         if (gi < hl && gj < wl) {
-          const int64_t e = (gi * wl + gj) * C + c;
-          dh = ldg(dirs + g.off[l][0] + e);
-          dv = ldg(dirs + g.off[l][1] + e);
-          dd = ldg(dirs + g.off[l][2] + e);
+          const IT e = (gi * wl + gj) * C + c;
+          dh = ldg(d0 + e);
+          dv = ldg(d1 + e);
+          dd = ldg(d2 + e);
         }
         const T o00 = T(0.5) * (((lp + dh) + dv) + dd);
         const T o01 = T(0.5) * (((lp + dh) - dv) - dd);
         const T o10 = T(0.5) * (((lp - dh) - dv) + dd);
         const T o11 = T(0.5) * (((lp - dh) + dv) - dd);
         if (l == 1) {
-          const int64_t r0 = 2 * gi, c0 = 2 * gj;
+          const IT r0 = 2 * gi, c0 = 2 * gj;
           if (r0 < ho) {
             if (c0 < wo) out[(r0 * wo + c0) * C + c] = o00;
             if (c0 + 1 < wo) out[(r0 * wo + c0 + 1) * C + c] = o01;
@@ -202,10 +210,20 @@ int haar_forward_impl(const T* image, int64_t H, int64_t W, int64_t C, int n, T*
     const int64_t total = g.h[NL] * g.w[NL] * C;
     const int threads = 128;
     const unsigned grid = grid_1d(total, threads);
-    switch (NL) {
-      case 1: haar_fwd_kernel<T, 1><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
-      case 2: haar_fwd_kernel<T, 2><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
-      default: haar_fwd_kernel<T, 3><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+    // 32-bit in-plane indices when the source plane and the largest output plane fit
+    const bool i32 = g.h[0] * g.w[0] * C < ((int64_t)1 << 31);
+    if (i32) {
+      switch (NL) {
+        case 1: haar_fwd_kernel<T, 1, int32_t><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+        case 2: haar_fwd_kernel<T, 2, int32_t><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+        default: haar_fwd_kernel<T, 3, int32_t><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+      }
+    } else {
+      switch (NL) {
+        case 1: haar_fwd_kernel<T, 1, int64_t><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+        case 2: haar_fwd_kernel<T, 2, int64_t><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+        default: haar_fwd_kernel<T, 3, int64_t><<<grid, threads, 0, stream>>>(src, g, planes, flags); break;
+      }
     }
     int st = check_launch("haar_forward");
     if (st) return st;
@@ -275,10 +293,19 @@ int haar_inverse_impl(const T* coarse_lp, const T* dirs, const int64_t* shp, int
     const int64_t total = g.h[NLc] * g.w[NLc] * C;
     const int threads = 128;
     const unsigned grid = grid_1d(total, threads);
-    switch (NLc) {
-      case 1: haar_inv_kernel<T, 1><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
-      case 2: haar_inv_kernel<T, 2><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
-      default: haar_inv_kernel<T, 3><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+    // 32-bit in-plane indices when the output plane (the largest) fits
+    if (g.h[0] * g.w[0] * C < ((int64_t)1 << 31)) {
+      switch (NLc) {
+        case 1: haar_inv_kernel<T, 1, int32_t><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+        case 2: haar_inv_kernel<T, 2, int32_t><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+        default: haar_inv_kernel<T, 3, int32_t><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+      }
+    } else {
+      switch (NLc) {
+        case 1: haar_inv_kernel<T, 1, int64_t><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+        case 2: haar_inv_kernel<T, 2, int64_t><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+        default: haar_inv_kernel<T, 3, int64_t><<<grid, threads, 0, stream>>>(top, dirs, g, dst); break;
+      }
     }
     st = check_launch("haar_inverse");
     if (prev_scratch) cudaFreeAsync(prev_scratch, stream);
