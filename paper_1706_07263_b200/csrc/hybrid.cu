@@ -114,9 +114,19 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
   if (idx >= nll) return;
   const int64_t hL = d.h[NLV], wL = d.w[NLV];
   const int64_t per = hL * wL;
-  const int64_t f = idx / per;
-  const int64_t rem = idx - f * per;
-  const int64_t by = rem / wL, bx = rem - by * wL;
+  int64_t f, by, bx;
+  if (nll <= 0xffffffffll) {  // 32-bit divisions (64-bit ones are ~70-instruction sequences)
+    const uint32_t i32 = (uint32_t)idx, p32 = (uint32_t)per, w32 = (uint32_t)wL;
+    const uint32_t f32 = i32 / p32, r32 = i32 - f32 * p32, y32 = r32 / w32;
+    f = f32;
+    by = y32;
+    bx = r32 - y32 * w32;
+  } else {
+    f = idx / per;
+    const int64_t rem = idx - f * per;
+    by = rem / wL;
+    bx = rem - by * wL;
+  }
   const int64_t base = f * d.h[0] * d.w[0] * 3;
   const double inv = ldexp(1.0, -scale_exp);  // exact
   bool bad = false;
