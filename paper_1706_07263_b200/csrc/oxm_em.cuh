@@ -668,6 +668,7 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s, cudaEvent_t spl
 // BLAS products).  The count is device-side, so the grid is the resident
 // one; io.work must be zero at launch.
 constexpr int kXLanes = 4;
+constexpr int64_t kExactSeqMinN = int64_t(1) << 21;  // low-pass coefficients (~16 1080p n=2 frames)
 constexpr int kXThreads = 128;
 struct alignas(16) XBand {  // per-band operator row, staged in shared memory (lanes read different bands)
   double xs0, xs1, c0, c1, c2, g0, g1, g2, f0, f1, f2, pad;
@@ -800,11 +801,24 @@ inline int launch_em_selected(const DevOps& ops, EmIO io, cudaStream_t s) {
   if (!io.fits || !io.xinit || !io.work || !io.sel || !io.sel_count) return OXM_ERR_ARGUMENT;
   if (ops.max_iters <= 1) return OXM_ERR_ARGUMENT;  // fit #1 would be final: nothing to redo
   io.fmt = OUT;
-  auto kern = em_exact_kernel<KL, OUT>;
   int64_t blocks = 0;
-  int st = persistent_blocks(kern, 0, 0, ceil_div(io.n * kXLanes, kXThreads), blocks);
-  if (st) return st;
-  kern<<<(unsigned)blocks, kXThreads, 0, s>>>(ops, io);
+  int st = OXM_OK;
+  // The list is ~1% of the coefficients.  Large batches give it enough
+  // coefficients per warp for the one-lane-per-coefficient persistent kernel
+  // (cheaper per fit); small ones leave that kernel latency-bound, where the
+  // 4-lane groups finish each coefficient ~3x sooner (tools/em_variants.py:
+  // 8 frames 10.3 vs 10.6 us/frame, 32 frames 5.6 vs 5.2, 64 frames 5.3 vs 4.7).
+  if (io.n >= kExactSeqMinN) {
+    io.stats = nullptr;
+    const size_t smem = em_smem_bytes(ops.L, kEmThreads);
+    auto kern = em_persistent_kernel<KL, OUT>;
+    if ((st = persistent_blocks(kern, smem, 0, ceil_div(ceil_div(io.n, kEmThreads), kEmSlots), blocks))) return st;
+    kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
+  } else {
+    auto kern = em_exact_kernel<KL, OUT>;
+    if ((st = persistent_blocks(kern, 0, 0, ceil_div(io.n * kXLanes, kXThreads), blocks))) return st;
+    kern<<<(unsigned)blocks, kXThreads, 0, s>>>(ops, io);
+  }
   return check_launch("em_exact");
 }
 

@@ -14,12 +14,10 @@ import sys
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-VARIANTS = {  # name -> extra -D defines (the last sweep: tail / exact-pass occupancy)
+VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
     "base": (),
     "tail4": ("OXM_TAIL_MIN_BLOCKS=4",),
-    "tail6": ("OXM_TAIL_MIN_BLOCKS=6",),
-    "x8": ("OXM_X_MIN_BLOCKS=8",),
-    "x10": ("OXM_X_MIN_BLOCKS=10",),
+    "x6": ("OXM_X_MIN_BLOCKS=6",),
 }
 
 
