@@ -122,3 +122,27 @@ def test_set_em_lead_validation(cuda, sensitivity, basis):
     assert lib.oxm_ctx_set_em_lead(None, 16.0, 0.01, 0.0) == bad
     out = (ctypes.c_uint64 * 4)()
     assert lib.oxm_hybrid_em_counters(None, None, 1, 8, 8, 1, out, None) == bad
+
+
+def test_large_batch_exact_pass_matches_small(cuda, sensitivity, basis):
+    """Batches of >= 2^21 low-pass coefficients run the exact-block pass on the
+    one-lane persistent kernel, smaller ones on 4-lane groups: same fit counts,
+    maps equal to within fp32 rounding (the two differ only in the summation
+    order of the 26-term sums)."""
+    import bench
+
+    frames = bench.make_frames(17, 1080, 1920, 0.3, 0, cuda)  # 17 x 129600 > 2^21 coefficients
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2))
+    big = eng.run(frames, fits=True)
+    c = eng.em_counters(17, 1080, 1920)
+    assert c["exact_blocks"] > 0
+    for b0 in range(0, 17, 4):
+        small = eng.run(frames[b0:b0 + 4].contiguous(), fits=True)
+        nb = small.thb.shape[0]
+        assert torch.equal(small.fits, big.fits[b0:b0 + nb])
+        rt = big.thb[b0:b0 + nb].double()
+        assert float(((small.thb.double() - rt).abs() / rt.abs()).max()) < 1e-6
+        rs, ss = big.so2[b0:b0 + nb], small.so2
+        assert torch.equal(torch.isnan(rs), torch.isnan(ss))
+        ok = ~torch.isnan(rs)
+        assert float((rs[ok] - ss[ok]).abs().max()) < 1e-6
