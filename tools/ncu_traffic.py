@@ -4,8 +4,10 @@ DRAM bytes (read + write) per frame for each bench stage.
     python tools/ncu_traffic.py rep.ncu-rep FRAMES_PER_LAUNCH"""
 import csv, io, json, pathlib, subprocess, sys
 
-STAGES = {"ll_kernel": ("ll_kernel",), "em_lead": ("em_lead",), "em": ("em_persistent",),
-          "px_f32_kernel": ("px_f32",), "fixup": ("px_fallback", "em_exact")}
+STAGES = {"ll_kernel": ("ll_kernel",), "em_lead": ("em_lead",), "em": ("em_persistent_kernel<26, 1, 1>",),
+          "px_f32_kernel": ("px_f32",),
+          # the exact-block pass: 4-lane kernel (small batches) or the one-lane persistent kernel
+          "fixup": ("px_fallback", "em_exact", "em_persistent_kernel<26, 1, 0>")}
 
 
 def main():

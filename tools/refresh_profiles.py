@@ -19,7 +19,7 @@ def launches(path: str) -> str:
             if "oxm::" in k and not any(x in k for x in ("probe", "synth_kernel", "patch_mean", "pack_hwc3"))}
     tot = sum(sum(v) for v in ours.values())
     out = ["ncu --metrics gpu__time_duration.sum --clock-control none python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu",
-           "(cold-cache, serialised launches: compare SHARES; batch = 32 frames 1080p n=2;",
+           "(cold-cache, serialised launches: compare SHARES; batch = 64 frames 1080p n=2;",
            " untimed input staging (synth_kernel) and the roofline probes excluded)",
            f"{'kernel (hot path only)':70s} {'n':>3} {'mean ns':>12} {'share':>7}"]
     for k, v in sorted(ours.items(), key=lambda x: -sum(x[1])):
