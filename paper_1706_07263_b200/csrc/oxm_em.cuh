@@ -16,11 +16,15 @@
 // rank-3 update: 78+78 FMAs instead of a 676-FMA dense matvec.
 //
 // Performance shape (fp64-pipe bound): the expected spectrum e (L doubles)
-// lives in shared memory, not registers, and the band loops are only 4-way
-// unrolled around the table-driven exp/log of oxm_math.cuh, so the kernel
-// stays near 64 registers and its loop fits the instruction cache.  The
-// stopping test compares squared norms (no sqrt/div); it differs from the
-// reference's rel < tol only when rel is within ~1e-16 of tol.
+// lives in shared memory, not registers, and both band loops are fully
+// unrolled around the table-driven exp/log of oxm_math.cuh (96 registers, 5
+// CTAs per SM).  The stopping test compares squared norms (no sqrt/div); it
+// differs from the reference's rel < tol only when rel is within ~1e-16 of tol.
+//
+// Kernels here: em_init_kernel (fit #1), em_persistent_kernel (all-fp64, or
+// the fp64 tail of the fp32 map path), em_lead_kernel (fp32 lead-in) and
+// em_exact_kernel (all-fp64 on a short coefficient list, 4 lanes each); the
+// precision schedule that combines them is described at em_lead_kernel.
 #pragma once
 
 #include "oxm_common.cuh"
