@@ -401,6 +401,13 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   constexpr int kPerCta = kFbThreads / kFbLanes;
   const uint32_t cnt = *fb_count;
   if ((int64_t)blockIdx.x * kPerCta >= cnt) return;  // whole CTA idle: skip the staging
+  const int64_t stride = (int64_t)gridDim.x * kPerCta;
+  if constexpr (MODE == kFbDeferred) {  // most CTAs hold no deferred entry: skip the staging too
+    bool any = false;
+    for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride)
+      any |= (fb_list[i] & kDeferTag) != 0;
+    if (!__syncthreads_or(any)) return;
+  }
   const int L = ops.L;
   for (int q = threadIdx.x; q < 3 * L; q += kFbThreads) {
     T[q / 3][q % 3] = ops.solve[q / 3][q % 3];
@@ -411,7 +418,6 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   // pixel indices are < 2^32 (checked at launch): 32-bit index arithmetic
   const uint32_t plane = (uint32_t)(g.H * g.W), W = (uint32_t)g.W;
   const double2* logt = log_table_global();
-  const int64_t stride = (int64_t)gridDim.x * kPerCta;
   // the loop bound is uniform over each group of kFbLanes lanes (shuffles below)
   const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below;
   // group collectives use the group's own lanes: other groups of the warp may
