@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   int64_t idx[NS];
   int nfit[NS];
   bool exact[NS];  // TAIL: this lane runs the coefficient from fit #1 (no guard)
-  unsigned long long wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats)
+  unsigned wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats; < 2^32 per warp)
   double y[NS][3], x[NS][3];
   auto load = [&](int sl, int64_t i) {
     int f = 1;
@@ -458,8 +458,8 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
     }
   }
   if (TAIL && io.stats && lane == 0) {
-    atomicAdd(io.stats + 1, wsteps);
-    atomicAdd(io.stats + 2, wrestarts);
+    atomicAdd(io.stats + 1, (unsigned long long)wsteps);
+    atomicAdd(io.stats + 2, (unsigned long long)wrestarts);
   }
 }
 
