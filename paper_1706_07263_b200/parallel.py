@@ -62,3 +62,39 @@ def gather_to_root(local: torch.Tensor, n_frames: int, root: int = 0) -> torch.T
             dist.recv(buf, src=r)
             out[lo:hi] = buf
     return out
+
+
+def gather_chunk_to_root(local: torch.Tensor, n_frames: int, chunk: int, c: int, root: int = 0):
+    """Streamed variant of gather_to_root for videos processed chunk by chunk
+    (the final NVLink gather overlapped with the next chunk's
+    compute).  Every rank calls it for chunk ``c`` with its maps of frames
+    [lo + c * chunk, lo + (c + 1) * chunk) of its block (possibly empty when its
+    block is shorter); the root receives the other ranks' chunks with batched
+    point-to-point transfers and returns [(first frame index, tensor)] for all
+    ranks' chunk c (its own included); other ranks return None.  Identity
+    (single entry) without torch.distributed."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return [(c * chunk, local)]
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    spans = []
+    for r in range(ws):
+        lo, hi = shard_range(n_frames, r, ws)
+        a, b = min(hi, lo + c * chunk), min(hi, lo + (c + 1) * chunk)
+        spans.append((a, b))
+    if rank != root:
+        a, b = spans[rank]
+        if b > a:
+            dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), root)])[0].wait()
+        return None
+    ops, out = [], []
+    for r in range(ws):
+        a, b = spans[r]
+        if r == root:
+            out.append((a, local))
+        elif b > a:
+            buf = torch.empty((b - a,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+            ops.append(dist.P2POp(dist.irecv, buf, r))
+            out.append((a, buf))
+    for w in (dist.batch_isend_irecv(ops) if ops else []):
+        w.wait()
+    return sorted(out, key=lambda t: t[0])

@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1706_07263_b200.parallel import gather_to_root, max_over_ranks, shard_range
+from paper_1706_07263_b200.parallel import gather_chunk_to_root, gather_to_root, max_over_ranks, shard_range
 
 
 def test_shard_range_partitions():
@@ -42,7 +42,14 @@ def _worker(rank: int, ws: int, port: int, q):
         local = torch.arange(lo, hi, dtype=torch.float32)[:, None, None].expand(hi - lo, 2, 3).contiguous()
         full = gather_to_root(local, n)
         t = max_over_ranks(0.5 + rank)
-        q.put((rank, t, None if full is None else full[:, 0, 0].tolist()))
+        # streamed gather, chunks of 2 frames (rank blocks 0..2 and 3..4: uneven)
+        streamed = []
+        for c in range(2):
+            cl = local[2 * c:2 * c + 2]
+            got = gather_chunk_to_root(cl, n, 2, c)
+            if got is not None:
+                streamed.extend((a, t_[:, 0, 0].tolist()) for a, t_ in got)
+        q.put((rank, t, None if full is None else full[:, 0, 0].tolist(), streamed if rank == 0 else None))
     finally:
         dist.destroy_process_group()
 
@@ -61,3 +68,5 @@ def test_gloo_two_ranks():
     assert res[0][1] == res[1][1] == 1.5  # max over ranks
     assert res[0][2] == [0.0, 1.0, 2.0, 3.0, 4.0]  # gathered in frame order on rank 0
     assert res[1][2] is None
+    # streamed gather: chunk 0 of both blocks, then chunk 1 (rank 1's block is exhausted)
+    assert res[0][3] == [(0, [0.0, 1.0]), (3, [3.0, 4.0]), (2, [2.0])]

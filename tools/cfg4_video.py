@@ -28,13 +28,15 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=4096)
     ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--gather", action="store_true",
+                    help="also stream every chunk's THb/SO2 maps to rank 0 (NCCL p2p) and time that run")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
 
     import bench
     import paper_1706_07263_b200 as ox
-    from paper_1706_07263_b200.parallel import max_over_ranks, shard_range, world
+    from paper_1706_07263_b200.parallel import gather_chunk_to_root, max_over_ranks, shard_range, world
     from paper_1706_07263_b200 import _native
     from paper_1706_07263_b200.device import ptr, stream_handle
 
@@ -59,31 +61,45 @@ def main():
     sums = torch.empty(nloc, dtype=torch.float64, device=dev)
     counts = torch.empty(nloc, dtype=torch.int64, device=dev)
     outs = [out] + ([eng.allocate(args.chunk, H, W)] if nloc > args.chunk else [])
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for k, c0 in enumerate(range(0, nloc, args.chunk)):
-        nb = min(args.chunk, nloc - c0)
-        res = outs[k % len(outs)]
-        thb = res.thb[:nb]
-        if nb < args.chunk:  # last partial chunk (uneven shards)
-            res = eng.allocate(nb, H, W)
-            thb = res.thb
-        eng.launch(pool[:nb], res)
-        st = lib.oxm_patch_mean_f32(ptr(thb), nb, H, W, *rect, ptr(sums[c0:c0 + nb]), ptr(counts[c0:c0 + nb]),
-                                    stream_handle())
-        _native.check(st, "patch_mean")
-    b.record()
-    b.synchronize()
-    total_ms = a.elapsed_time(b)
+    n_chunks = max(-(-(b - a) // args.chunk) for a, b in (shard_range(args.frames, r, ws) for r in range(ws)))
+
+    def run(gather: bool) -> float:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if ws > 1:
+            dist.barrier()
+        a.record()
+        for k in range(n_chunks):  # every rank takes part in every chunk's gather
+            c0 = k * args.chunk
+            nb = max(0, min(args.chunk, nloc - c0))
+            res = outs[k % len(outs)]
+            if 0 < nb < args.chunk:  # last partial chunk (uneven shards)
+                res = eng.allocate(nb, H, W)
+            if nb:
+                eng.launch(pool[:nb], res)
+                st = lib.oxm_patch_mean_f32(ptr(res.thb), nb, H, W, *rect, ptr(sums[c0:c0 + nb]),
+                                            ptr(counts[c0:c0 + nb]), stream_handle())
+                _native.check(st, "patch_mean")
+            if gather:  # maps of chunk k of every rank to rank 0 over NVLink (NCCL p2p)
+                gather_chunk_to_root(res.thb[:nb], args.frames, args.chunk, k)
+                gather_chunk_to_root(res.so2[:nb], args.frames, args.chunk, k)
+        b.record()
+        b.synchronize()
+        return max_over_ranks(a.elapsed_time(b) * 1e-3, dev)
+
+    t = run(False)
+    tg = run(True) if args.gather else None
     trace = (sums / counts.clamp_min(1)).cpu().numpy().tolist()
     eng.check_flags(out)
-    t = max_over_ranks(total_ms * 1e-3, dev)
     if rank == 0:
-        print(json.dumps({"config": "cfg4 1080p n=2, 4096-frame synthetic video, frame-sharded",
-                          "frames": args.frames, "gpus": ws, "chunk": args.chunk, "seconds": t,
-                          "frames_per_s": args.frames / t, "thb_patch_mean_first": trace[:4],
-                          "note": "device-synthesised input excluded from the timed region; maps reduced to "
-                                  "the patch-mean THb trace on the device"}))
+        rec = {"config": "cfg4 1080p n=2, 4096-frame synthetic video, frame-sharded",
+               "frames": args.frames, "gpus": ws, "chunk": args.chunk, "seconds": t,
+               "frames_per_s": args.frames / t, "thb_patch_mean_first": trace[:4],
+               "note": "device-synthesised input excluded from the timed region; maps reduced to "
+                       "the patch-mean THb trace on the device"}
+        if tg is not None:
+            rec.update({"gathered_seconds": tg, "gathered_frames_per_s": args.frames / tg,
+                        "gather": "every chunk's THb + SO2 maps to rank 0 (gather_chunk_to_root)"})
+        print(json.dumps(rec))
     if ws > 1:
         dist.destroy_process_group()
 
