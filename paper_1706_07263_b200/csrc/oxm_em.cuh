@@ -66,8 +66,9 @@ struct BandCount {
 // consecutive threads) stay contiguous, and a column (one thread, consecutive
 // bands -- write_spectra) walks the banks instead of hitting one bank 26 times.
 // Each column also holds, after its L bands, the lane's residual r (3 rows)
-// and coefficient index (1 row), which write_spectra reads for the owner lane.
-constexpr int kEmColExtra = 4;
+// and coefficient index (1 row), which write_spectra reads for the owner lane,
+// and its data y (3 rows: kept in shared memory rather than six registers).
+constexpr int kEmColExtra = 7;  // r (3), coefficient index (1), y (3)
 __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
   return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands +
          sizeof(double) * (size_t)(L + kEmColExtra) * (size_t)(threads + 1) * OXM_EM_SLOTS;
@@ -294,13 +295,14 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   int nfit[NS];
   bool exact[NS];  // TAIL: this lane runs the coefficient from fit #1 (no guard)
   unsigned wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats; < 2^32 per warp)
-  double y[NS][3], x[NS][3];
+  double x[NS][3];
+  auto ycol = [&](int sl, int k) -> double& { return e[(sl * (L + kEmColExtra) + L + 4 + k) * es]; };
   auto load = [&](int sl, int64_t i) {
     int f = 1;
     if constexpr (TAIL) f = io.fits[i];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      y[sl][k] = kYSoa ? io.y[k * io.n + i] : io.y[3 * i + k];
+      ycol(sl, k) = kYSoa ? io.y[k * io.n + i] : io.y[3 * i + k];
       x[sl][k] = f > 1 ? (double)io.xh[k * io.n + i] : io.xinit[k * io.n + i];
     }
     nfit[sl] = f;
@@ -313,7 +315,7 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
     nfit[sl] = 1;
     exact[sl] = true;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) y[sl][k] = x[sl][k] = 0.0;
+    for (int k = 0; k < 3; ++k) ycol(sl, k) = x[sl][k] = 0.0;
     if (idx[sl] >= 0) load(sl, idx[sl]);
     e[(sl * (L + kEmColExtra) + L + 3) * es] = __longlong_as_double(idx[sl]);  // for write_spectra
   }
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
     for (int sl = 0; sl < NS; ++sl)
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        r[sl][k] = y[sl][k] - c[sl][k];
+        r[sl][k] = ycol(sl, k) - c[sl][k];
         nn[sl][k] = 0.0;
         e[(sl * (L + kEmColExtra) + L + k) * es] = r[sl][k];  // for write_spectra
       }
