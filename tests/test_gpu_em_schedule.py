@@ -146,3 +146,22 @@ def test_large_batch_exact_pass_matches_small(cuda, sensitivity, basis):
         assert torch.equal(torch.isnan(rs), torch.isnan(ss))
         ok = ~torch.isnan(rs)
         assert float((rs[ok] - ss[ok]).abs().max()) < 1e-6
+
+
+@pytest.mark.parametrize("gain", [1e-4, 3e-2, 30.0])
+def test_schedule_extreme_exposure(cuda, sensitivity, basis, gain):
+    """Very dark / very bright frames push the fp32 lead-in toward underflow,
+    clamping and overflow (non-finite fp32 steps hand over the last finite
+    state): fit counts must still equal the all-fp64 schedule's."""
+    rgb = (synth.phantom_rgb_f32(96, 128, 21, sensitivity, basis) * gain).astype(np.float32).astype(np.float64)
+    frames = rgb[None]
+    _, ref, _ = _run(cuda, sensitivity, basis, frames, 2, None)
+    _, out, _ = _run(cuda, sensitivity, basis, frames, 2, (16.0, 0.01))
+    rt, rs, rf = _maps(ref)
+    t, s, f = _maps(out)
+    assert np.array_equal(f, rf)
+    assert np.array_equal(np.isnan(s), np.isnan(rs))
+    ok = np.isfinite(rt) & (np.abs(rt) > 0)
+    assert np.max(np.abs(t[ok] - rt[ok]) / np.abs(rt[ok]), initial=0.0) < 1e-5
+    oks = ~np.isnan(rs)
+    assert np.max(np.abs(s[oks] - rs[oks]), initial=0.0) < 5e-6
