@@ -228,6 +228,31 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
 template <int KL, SpecOut OUT>
 __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol0, int es, int L, unsigned done_mask,
                                               int lane, const double (*gsm)[3], double eps) {
+  if constexpr (KL > 0 && KL <= 32) {
+    // one band per lane: its G row is loaded once for all finished lanes
+    if (lane >= KL) {  // lanes without a band only take part in the shuffle-free loop
+      return;
+    }
+    const double g0 = gsm[lane][0], g1 = gsm[lane][1], g2 = gsm[lane][2];
+    while (done_mask) {
+      const int owner = __ffs(done_mask) - 1;
+      done_mask &= done_mask - 1;
+      const double* oc = ecol0 + owner;
+      const double q0 = oc[KL * es], q1 = oc[(KL + 1) * es], q2 = oc[(KL + 2) * es];
+      const int64_t oidx = __double_as_longlong(oc[(KL + 3) * es]);
+      const double s = clamp_eps(fma(g2, q2, fma(g1, q1, fma(g0, q0, ecol0[lane * es + owner]))), eps);
+      if constexpr (OUT == SpecOut::kSoaF64) {
+        io.S[(int64_t)lane * io.n + oidx] = s;
+      } else if constexpr (OUT == SpecOut::kAosF64) {
+        io.S[oidx * KL + lane] = s;
+      } else {
+        const float h = __double2float_rn(s);
+        io.Shi[oidx * io.Lp + lane] = h;
+        if (io.Slo) io.Slo[oidx * io.Lp + lane] = __double2float_rn(s - (double)h);
+      }
+    }
+    return;
+  }
   while (done_mask) {
     const int owner = __ffs(done_mask) - 1;
     done_mask &= done_mask - 1;
