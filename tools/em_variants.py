@@ -51,13 +51,7 @@ def time_one(batch: int) -> dict:
         eng.launch(frames, out, stage_events=e)
     torch.cuda.synchronize()
     st = [sum(e[i].elapsed_time(e[i + 1]) for e in evs) / len(evs) / batch * 1e3 for i in range(5)]
-    # fallback pixel count: the counter after the carve sections (hybrid.cu carve())
-    nll = batch * 270 * 480
-    a256 = lambda b: (b + 255) // 256 * 256
-    base = (eng._ws.data_ptr() + 255) // 256 * 256 - eng._ws.data_ptr()
-    off = base + a256(24 * nll) + a256(8 * 28 * nll) + a256(24 * nll) + a256(4 * nll) + a256(12 * nll)
-    fb = int(eng._ws[off:off + 4].view(torch.int32).item())
-    return {"ll_us": st[0], "em_lead_us": st[1], "em_us": st[2], "px_us": st[3], "fixup_us": st[4], "fits": int(out.fits.sum()), "fallback_px": fb,
+    return {"ll_us": st[0], "em_lead_us": st[1], "em_us": st[2], "px_us": st[3], "fixup_us": st[4], "fits": int(out.fits.sum()), **eng.em_counters(batch, 1080, 1920),
             "thb": float(out.thb.double().sum())}
 
 
