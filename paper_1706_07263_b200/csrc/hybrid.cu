@@ -32,6 +32,7 @@
 // fp32 path: HBM traffic is the frame read twice, the per-block spectra
 // (8 B/band/coefficient) once, and the maps written once.
 #include <algorithm>
+#include <type_traits>
 
 #include "oxm_em.cuh"
 
@@ -132,9 +133,48 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
   bool bad = false;
   bool neg = false;
   double yv[3];
+  double ll[3];
+  // fp32 frames, 2 levels, a block whose 4 x 4 pixels are all inside the frame
+  // (no edge replication at either level) and 16-byte aligned rows: the four
+  // 12-float rows as three float4s each instead of 48 strided scalars; same
+  // fp64 adds in the same order as LowPass<>
+  bool fast = false;
+  if constexpr (NLV == 2 && Src::kF32 && std::is_same<Src, PlainSrc<float>>::value) {
+    fast = ((reinterpret_cast<uintptr_t>(frames.p) & 15) == 0) && (d.w[0] & 3) == 0 && 4 * by + 4 <= d.h[0] &&
+           4 * bx + 4 <= d.w[0];
+    if (fast) {
+      float px[4][12];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float4* rp = reinterpret_cast<const float4*>(frames.p + base + ((4 * by + r) * d.w[0] + 4 * bx) * 3);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const float4 v = ldg(rp + q);
+          px[r][4 * q] = v.x;
+          px[r][4 * q + 1] = v.y;
+          px[r][4 * q + 2] = v.z;
+          px[r][4 * q + 3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        double l1[2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const double a = px[2 * i][(2 * j) * 3 + c], b2 = px[2 * i][(2 * j + 1) * 3 + c];
+            const double cc = px[2 * i + 1][(2 * j) * 3 + c], dd = px[2 * i + 1][(2 * j + 1) * 3 + c];
+            bad |= !isfinite(a) || !isfinite(b2) || !isfinite(cc) || !isfinite(dd);
+            l1[i][j] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b2), cc), dd);
+          }
+        ll[c] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(l1[0][0], l1[0][1]), l1[1][0]), l1[1][1]);
+      }
+    }
+  }
 #pragma unroll
   for (int c = 0; c < 3; ++c) {
-    double v = LowPass<Src, NLV>::at(frames, base, d, by, bx, c, bad);
+    double v = fast ? ll[c] : LowPass<Src, NLV>::at(frames, base, d, by, bx, c, bad);
     if constexpr (OUT_YBAR) {
       v *= inv;
       neg |= v < 0.0;
