@@ -31,7 +31,10 @@ def main():
     dev = torch.device("cuda", 0)
     sens, basis = bench.operators()
     H, W, n = 1080, 1920, 2
-    frames = bench.make_frames(batch, H, W, 0.3, 0, dev)
+    import os
+
+    # OXM_SWEEP_RANK=r: another set of seeded phantoms (bench.make_frames seeds by rank)
+    frames = bench.make_frames(batch, H, W, 0.3, int(os.environ.get("OXM_SWEEP_RANK", "0")), dev)
     cube, _ = ox.estimate_frame(ox.RgbImage(frames[0].double().cpu().numpy()), sens, basis,
                                 ox.PipelineConfig(n_levels=n))
     minband = torch.from_numpy(cube.data.min(axis=2)).to(dev)
