@@ -284,9 +284,16 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # OXM_BENCH_BACKEND=gloo exercises the multi-rank path with several ranks on one
+    # GPU (functional check only: ranks share the device, the numbers are not scaling)
+    backend = os.environ.get("OXM_BENCH_BACKEND", "nccl")
     if world > 1:
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
     torch.cuda.set_device(dev)
 

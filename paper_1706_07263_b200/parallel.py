@@ -37,6 +37,8 @@ def max_over_ranks(value: float, device: torch.device | None = None) -> float:
     torch.distributed is not initialised."""
     if not (dist.is_available() and dist.is_initialized()):
         return float(value)
+    if dist.get_backend() == "gloo":
+        device = None  # gloo reduces host tensors
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
