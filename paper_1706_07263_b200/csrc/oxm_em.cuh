@@ -144,6 +144,10 @@ constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 #endif
 constexpr int kEmChunk = OXM_EM_CHUNK;  // coefficients per dynamically assigned chunk (>= 32)
 constexpr int kEmSlots = OXM_EM_SLOTS;  // coefficients in flight per thread
+#ifndef OXM_LEAD_POLY_PAIRS
+#define OXM_LEAD_POLY_PAIRS 0
+#endif
+constexpr int kLeadPolyPairs = OXM_LEAD_POLY_PAIRS;  // lead-in band pairs whose ex2 runs on the FMA pipe
 static_assert(kEmChunk >= 32, "a refill may need up to 32 fresh coefficients");
 
 // Fit #1 of one coefficient (bayes.py:241-250, 193): x = -F log(max(start, eps))
@@ -548,7 +552,8 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
     for (int q = 0; q < KL / 2; ++q) {
       const int l = 2 * q;
       const float2 t = __ffma2_rn(pair(ops.xl2_t[0], l), X0, __ffma2_rn(pair(ops.xl2_t[1], l), X1, X2));
-      e[q] = make_float2(ex2_approx(t.x), ex2_approx(t.y));
+      // the first kLeadPolyPairs band pairs take their ex2 on the FMA pipe
+      e[q] = q < kLeadPolyPairs ? ex2_poly2(t) : make_float2(ex2_approx(t.x), ex2_approx(t.y));
       c0 = __ffma2_rn(pair(ops.sens_f[0], l), e[q], c0);
       c1 = __ffma2_rn(pair(ops.sens_f[1], l), e[q], c1);
       c2 = __ffma2_rn(pair(ops.sens_f[2], l), e[q], c2);

@@ -61,6 +61,29 @@ __device__ __forceinline__ float lg2_approx(float v) {
   return r;
 }
 
+// 2^t for a pair on the FMA pipe (FADD2/FFMA2 + two integer adds), < 2 ulp like
+// ex2.approx: t clamped to [-125, 127] (the lead-in's e feeds sums with the eps
+// clamp downstream, so 2^-125 for an underflowing band is as good as 0), rounded
+// with the 1.5 * 2^23 trick, 2^r on [-1/2, 1/2] by a degree-5 fit at Chebyshev
+// nodes, then n added to the exponent field ((0x4B400000 + n) << 23 == n << 23
+// mod 2^32).  Lets the MUFU-bound fp32 EM lead-in move a share of its ex2s off
+// the XU pipe.
+__device__ __forceinline__ float2 ex2_poly2(float2 t) {
+  t.x = fminf(fmaxf(t.x, -125.f), 127.f);
+  t.y = fminf(fmaxf(t.y, -125.f), 127.f);
+  const float2 k = __fadd2_rn(t, make_float2(12582912.f, 12582912.f));
+  const float2 n = __fadd2_rn(k, make_float2(-12582912.f, -12582912.f));  // round(t), exact
+  const float2 r = __ffma2_rn(n, make_float2(-1.f, -1.f), t);                // t - n, exact
+  float2 p = __ffma2_rn(r, make_float2(1.3400432653725147e-3f, 1.3400432653725147e-3f),
+                        make_float2(9.676037356257439e-3f, 9.676037356257439e-3f));
+  p = __ffma2_rn(p, r, make_float2(5.550327152013779e-2f, 5.550327152013779e-2f));
+  p = __ffma2_rn(p, r, make_float2(2.402210682630539e-1f, 2.402210682630539e-1f));
+  p = __ffma2_rn(p, r, make_float2(6.931471824645996e-1f, 6.931471824645996e-1f));
+  p = __ffma2_rn(p, r, make_float2(1.0000001192092896f, 1.0000001192092896f));
+  return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(k.x) << 23)),
+                     __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(k.y) << 23)));
+}
+
 // exp(zs * ln2/256) for a pre-scaled argument zs
 __device__ __forceinline__ double exp_scaled(const double zs, const MathSmem& t) {
   // round-to-nearest via F2I/I2F: conversions run on the XU pipe, which the

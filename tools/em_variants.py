@@ -16,8 +16,10 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
     "base": (),
-    "tail4": ("OXM_TAIL_MIN_BLOCKS=4",),
-    "x6": ("OXM_X_MIN_BLOCKS=6",),
+    "poly1": ("OXM_LEAD_POLY_PAIRS=1",),
+    "poly2": ("OXM_LEAD_POLY_PAIRS=2",),
+    "poly3": ("OXM_LEAD_POLY_PAIRS=3",),
+    "poly4": ("OXM_LEAD_POLY_PAIRS=4",),
 }
 
 
