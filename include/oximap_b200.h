@@ -190,7 +190,8 @@ OXM_API size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, int
 /* EM work counters of the last fp32-map launch that used `workspace` (same
  * geometry): out[0] fp32 fits of the lead-in, out[1] fp64 fits of the tail,
  * out[2] tail restarts in exact mode, out[3] low-pass blocks re-estimated
- * all-fp64 for the fp64 pixel fallback.  Synchronises `stream`. */
+ * all-fp64 for the fp64 pixel fallback, out[4] pixels queued for the fp64
+ * fallback (`out` holds 5 values).  Synchronises `stream`. */
 OXM_API int oxm_hybrid_em_counters(const oxm_ctx* ctx, void* workspace, int64_t batch, int64_t height,
                                    int64_t width, int n_levels, uint64_t* out, void* stream);
 OXM_API int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,

@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   }
 }
 
-// fp64 recompute of the queued pixels (~0.4% of them): kFbLanes threads per
+// fp64 recompute of the queued pixels (~0.4% of them): kFbLanes (2) threads per
 // pixel, each taking every kFbLanes-th band, partial fit sums reduced with
 // two shuffles; grid-stride over the device-side count.  Each thread issues
 // its loads (rgb, ybar, its part of the hi/lo spectrum row) together and uses
@@ -421,7 +421,14 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
 //   kFbDeferred  recompute the tagged entries (after the exact pass).
 // Each pixel is written exactly once, from spectra that no kernel modifies
 // while it is classified: the output does not depend on scheduling.
-constexpr int kFbLanes = 4;
+#ifndef OXM_FB_LANES
+#define OXM_FB_LANES 2
+#endif
+constexpr int kFbLanes = OXM_FB_LANES;  // threads per queued pixel (1, 2 or 4)
+#ifndef OXM_FB_PREFETCH
+#define OXM_FB_PREFETCH 0
+#endif
+constexpr bool kFbPrefetch = OXM_FB_PREFETCH;  // list entry loaded one iteration ahead
 constexpr uint32_t kDeferTag = 0x80000000u;
 enum FbMode { kFbAll, kFbClassify, kFbDeferred };
 template <int KL, typename Src, int MODE>
@@ -463,8 +470,18 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   // group collectives use the group's own lanes: other groups of the warp may
   // have left the loop or skipped this entry
   const unsigned grp = ((1u << kFbLanes) - 1u) << ((threadIdx.x & 31) & ~(kFbLanes - 1));
-  for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride) {
-    uint32_t p = fb_list[i];
+  int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes;
+  // the next entry of this group is loaded one iteration ahead (only this
+  // group reads or tags it), so each iteration waits on one load level
+  uint32_t p_next = kFbPrefetch && i < cnt ? fb_list[i] : 0u;
+  for (; i < cnt; i += stride) {
+    uint32_t p;
+    if constexpr (kFbPrefetch) {
+      p = p_next;
+      if (i + stride < cnt) p_next = fb_list[i + stride];
+    } else {
+      p = fb_list[i];
+    }
     if constexpr (MODE == kFbDeferred) {
       if (!(p & kDeferTag)) continue;  // group-uniform
       p &= ~kDeferTag;
@@ -852,11 +869,13 @@ extern "C" int oxm_hybrid_em_counters(const oxm_ctx* ctx, void* workspace, int64
   const Workspace w = carve(workspace, ctx->ops.L, batch * d.h[n_levels] * d.w[n_levels]);
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
-  uint32_t blk = 0;
+  uint32_t blk = 0, queued = 0;
   cudaError_t err = cudaMemcpyAsync(out, w.em_stats, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (err == cudaSuccess) err = cudaMemcpyAsync(&blk, w.blk_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&queued, w.fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
   if (err == cudaSuccess) err = cudaStreamSynchronize(s);
   out[3] = blk;
+  out[4] = queued;
   if (err != cudaSuccess) {
     set_last_error("oxm_hybrid_em_counters", err);
     return OXM_ERR_CUDA;

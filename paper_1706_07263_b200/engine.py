@@ -129,16 +129,17 @@ class HybridMapEngine:
     def em_counters(self, batch: int, height: int, width: int) -> dict:
         """EM work of the last launch of this geometry: fp32 lead-in fits,
         fp64 tail fits, exact-mode restarts, blocks re-estimated all-fp64 for
-        the pixel fallback (synchronises the current stream)."""
+        the pixel fallback, pixels queued for the fp64 fallback (synchronises
+        the current stream)."""
         import ctypes
 
-        out = (ctypes.c_uint64 * 4)()
+        out = (ctypes.c_uint64 * 5)()
         st = self._lib.oxm_hybrid_em_counters(self.ctx.handle, ptr(self._workspace(self.workspace_bytes(batch, height, width))),
                                               batch, height, width, self.cfg.n_levels, out,
                                               stream_handle(None))
         _native.check(st, "em_counters")
         return {"lead_fits": int(out[0]), "tail_fits": int(out[1]), "restarts": int(out[2]),
-                "exact_blocks": int(out[3])}
+                "exact_blocks": int(out[3]), "queued_px": int(out[4])}
 
     # ---- device-resident path ---------------------------------------------
     def launch(self, frames: torch.Tensor, out: MapBatch, *, stream: torch.cuda.Stream | None = None,

@@ -16,10 +16,8 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
     "base": (),
-    "poly1": ("OXM_LEAD_POLY_PAIRS=1",),
-    "poly2": ("OXM_LEAD_POLY_PAIRS=2",),
-    "poly3": ("OXM_LEAD_POLY_PAIRS=3",),
-    "poly4": ("OXM_LEAD_POLY_PAIRS=4",),
+    "fbpf": ("OXM_FB_PREFETCH=1",),
+    "fb4": ("OXM_FB_LANES=4",),
 }
 
 
