@@ -425,10 +425,9 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
 #define OXM_FB_LANES 2
 #endif
 constexpr int kFbLanes = OXM_FB_LANES;  // threads per queued pixel (1, 2 or 4)
-#ifndef OXM_FB_PREFETCH
-#define OXM_FB_PREFETCH 0
+#ifndef OXM_FB_CTAS_PER_SM
+#define OXM_FB_CTAS_PER_SM 32
 #endif
-constexpr bool kFbPrefetch = OXM_FB_PREFETCH;  // list entry loaded one iteration ahead
 constexpr uint32_t kDeferTag = 0x80000000u;
 enum FbMode { kFbAll, kFbClassify, kFbDeferred };
 template <int KL, typename Src, int MODE>
@@ -470,18 +469,8 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   // group collectives use the group's own lanes: other groups of the warp may
   // have left the loop or skipped this entry
   const unsigned grp = ((1u << kFbLanes) - 1u) << ((threadIdx.x & 31) & ~(kFbLanes - 1));
-  int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes;
-  // the next entry of this group is loaded one iteration ahead (only this
-  // group reads or tags it), so each iteration waits on one load level
-  uint32_t p_next = kFbPrefetch && i < cnt ? fb_list[i] : 0u;
-  for (; i < cnt; i += stride) {
-    uint32_t p;
-    if constexpr (kFbPrefetch) {
-      p = p_next;
-      if (i + stride < cnt) p_next = fb_list[i + stride];
-    } else {
-      p = fb_list[i];
-    }
+  for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride) {
+    uint32_t p = fb_list[i];
     if constexpr (MODE == kFbDeferred) {
       if (!(p & kDeferTag)) continue;  // group-uniform
       p &= ~kDeferTag;
@@ -792,7 +781,7 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
   if (fixup_ev) cudaEventRecord(fixup_ev, s);
-  const unsigned fb_grid = 148 * 32;
+  const unsigned fb_grid = 148 * OXM_FB_CTAS_PER_SM;
   if (!exact_blocks_active(ops)) {
     px_fallback_kernel<KL, Src, kFbAll><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
                                                                   w.fb_list, thb, so2, hbo, hb, off, nullptr, nullptr,

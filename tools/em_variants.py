@@ -16,8 +16,8 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
     "base": (),
-    "fbpf": ("OXM_FB_PREFETCH=1",),
-    "fb4": ("OXM_FB_LANES=4",),
+    "g64": ("OXM_FB_CTAS_PER_SM=64",),
+    "g16": ("OXM_FB_CTAS_PER_SM=16",),
 }
 
 
