@@ -144,6 +144,9 @@ constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 #endif
 constexpr int kEmChunk = OXM_EM_CHUNK;  // coefficients per dynamically assigned chunk (>= 32)
 constexpr int kEmSlots = OXM_EM_SLOTS;  // coefficients in flight per thread
+#ifndef OXM_LEAD_RESID64
+#define OXM_LEAD_RESID64 0  // 1: the lead-in's residual y - C e in fp64 (tools/lead_noise_study.py)
+#endif
 #ifndef OXM_LEAD_POLY_PAIRS
 #define OXM_LEAD_POLY_PAIRS 0
 #endif
@@ -526,11 +529,17 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
 
   int64_t idx = next + lane < stop ? next + lane : -1;
   int nfit = 1;
-  float y0 = 0.f, y1 = 0.f, y2 = 0.f, x0 = 0.f, x1 = 0.f, x2 = 0.f;
+#if OXM_LEAD_RESID64
+  using YT = double;
+#else
+  using YT = float;
+#endif
+  YT y0 = 0, y1 = 0, y2 = 0;
+  float x0 = 0.f, x1 = 0.f, x2 = 0.f;
   auto load = [&](int64_t i) {
-    y0 = (float)io.y[i];
-    y1 = (float)io.y[io.n + i];
-    y2 = (float)io.y[2 * io.n + i];
+    y0 = (YT)io.y[i];
+    y1 = (YT)io.y[io.n + i];
+    y2 = (YT)io.y[2 * io.n + i];
     x0 = (float)io.xinit[i];
     x1 = (float)io.xinit[io.n + i];
     x2 = (float)io.xinit[2 * io.n + i];
@@ -547,6 +556,9 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
   while (__any_sync(0xffffffffu, idx >= 0)) {
     float2 e[KL / 2];
     float2 c0 = dup(0.f), c1 = c0, c2 = c0;
+#if OXM_LEAD_RESID64
+    double cd0 = 0.0, cd1 = 0.0, cd2 = 0.0;
+#endif
     const float2 X0 = dup(x0), X1 = dup(x1), X2 = dup(-kLog2e * x2);  // xi[:, 2] == 1
 #pragma unroll
     for (int q = 0; q < KL / 2; ++q) {
@@ -554,11 +566,22 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
       const float2 t = __ffma2_rn(pair(ops.xl2_t[0], l), X0, __ffma2_rn(pair(ops.xl2_t[1], l), X1, X2));
       // the first kLeadPolyPairs band pairs take their ex2 on the FMA pipe
       e[q] = q < kLeadPolyPairs ? ex2_poly2(t) : make_float2(ex2_approx(t.x), ex2_approx(t.y));
+#if OXM_LEAD_RESID64
+      const double ex = e[q].x, ey = e[q].y;
+      cd0 = fma(ops.sens[0][l + 1], ey, fma(ops.sens[0][l], ex, cd0));
+      cd1 = fma(ops.sens[1][l + 1], ey, fma(ops.sens[1][l], ex, cd1));
+      cd2 = fma(ops.sens[2][l + 1], ey, fma(ops.sens[2][l], ex, cd2));
+#else
       c0 = __ffma2_rn(pair(ops.sens_f[0], l), e[q], c0);
       c1 = __ffma2_rn(pair(ops.sens_f[1], l), e[q], c1);
       c2 = __ffma2_rn(pair(ops.sens_f[2], l), e[q], c2);
+#endif
     }
+#if OXM_LEAD_RESID64
+    const float2 R0 = dup((float)(y0 - cd0)), R1 = dup((float)(y1 - cd1)), R2 = dup((float)(y2 - cd2));
+#else
     const float2 R0 = dup(y0 - (c0.x + c0.y)), R1 = dup(y1 - (c1.x + c1.y)), R2 = dup(y2 - (c2.x + c2.y));
+#endif
     float2 m0 = dup(0.f), m1 = m0, m2 = m0;
 #pragma unroll
     for (int q = 0; q < KL / 2; ++q) {

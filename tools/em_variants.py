@@ -18,6 +18,7 @@ VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
     "base": (),
     "g64": ("OXM_FB_CTAS_PER_SM=64",),
     "g16": ("OXM_FB_CTAS_PER_SM=16",),
+    "r64": ("OXM_LEAD_RESID64=1",),  # lead-in residual in fp64 (tools/lead_noise_study.py)
 }
 
 
