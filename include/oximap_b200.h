@@ -233,6 +233,15 @@ OXM_API int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, int64
 OXM_API int oxm_synth_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t height, int64_t width,
                          int64_t count, double noise_sigma, double exposure, uint64_t seed,
                          uint64_t frame0, float* out, void* stream);
+/* Pulse sequence on the device: synth.py:187-231 (pulse_sequence) -- frame
+ * frame0 + f scales both haemoglobin truth planes by
+ * 1 + amplitude * sin(2 pi pulse_hz (frame0 + f) / fps) (offset unchanged), then
+ * the forward model / noise / projection of oxm_synth_frames_f32.  Requires
+ * amplitude >= 0 and, when amplitude > 0, 0 < pulse_hz < fps / 2 (synth.py:209-216). */
+OXM_API int oxm_synth_pulse_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t height, int64_t width,
+                         int64_t count, double noise_sigma, double exposure, uint64_t seed,
+                         uint64_t frame0, double fps, double pulse_hz, double amplitude, float* out,
+                         void* stream);
 /* Patch-mean THb trace: timeseries.py:44-73 -- per frame, the sum and count
  * of finite THb values in rect (x, y, w, h) of (batch, H, W) maps. */
 OXM_API int oxm_patch_mean_f32(const float* thb, int64_t batch, int64_t height, int64_t width, int x, int y,

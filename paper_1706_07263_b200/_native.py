@@ -102,6 +102,10 @@ _SIGNATURES = {
         [_vp, _vp, _i32, _f64, _i64, _i64, _i64, _i32, _f64, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     ),
     "oxm_synth_frames_f32": (_i32, [_vp, _vp, _i64, _i64, _i64, _f64, _f64, ctypes.c_uint64, ctypes.c_uint64, _vp, _vp]),
+    "oxm_synth_pulse_frames_f32": (
+        _i32,
+        [_vp, _vp, _i64, _i64, _i64, _f64, _f64, ctypes.c_uint64, ctypes.c_uint64, _f64, _f64, _f64, _vp, _vp],
+    ),
     "oxm_patch_mean_f32": (_i32, [_vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp]),
     "oxm_pack_hwc3_f32": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "oxm_probe_fp64_fma": (_i32, [_i32, _i32, _vp, _vp, _vp]),

@@ -48,12 +48,17 @@ __global__ void __launch_bounds__(kSynthThreads) synth_kernel(const __grid_const
                                                               const float* __restrict__ truth, int64_t npx,
                                                               int64_t count, float sigma, float exposure,
                                                               uint2 key, unsigned long long frame0,
+                                                              double amplitude, double pulse_hz, double fps,
                                                               float* __restrict__ out) {
   const int64_t t = (int64_t)blockIdx.x * kSynthThreads + threadIdx.x;
   if (t >= npx * count) return;
   const int64_t f = t / npx, p = t - f * npx;
-  const float x0 = ldg(truth + 3 * p), x1 = ldg(truth + 3 * p + 1), x2 = ldg(truth + 3 * p + 2);
   const unsigned long long fr = frame0 + (unsigned long long)f;
+  // pulse_sequence (synth.py:218-222): frame fr scales both haemoglobin planes by
+  // m = 1 + amplitude sin(2 pi f fr / fps), same expression order, fp64
+  const float m = amplitude != 0.0 ? (float)(1.0 + amplitude * sin(2.0 * 3.141592653589793 * pulse_hz * (double)fr / fps))
+                                   : 1.0f;
+  const float x0 = ldg(truth + 3 * p) * m, x1 = ldg(truth + 3 * p + 1) * m, x2 = ldg(truth + 3 * p + 2);
   float r0 = 0.f, r1 = 0.f, r2 = 0.f;
   const int L = ops.L;
   for (int l0 = 0; l0 < L; l0 += 4) {
@@ -173,10 +178,13 @@ extern "C" int oxm_pack_hwc3_f32(const float* a, const float* b, const float* c,
   return check_launch("pack_hwc3");
 }
 
-extern "C" int oxm_synth_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t height, int64_t width,
-                                    int64_t count, double noise_sigma, double exposure, uint64_t seed,
-                                    uint64_t frame0, float* out, void* stream) {
+extern "C" int oxm_synth_pulse_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t height, int64_t width,
+                                          int64_t count, double noise_sigma, double exposure, uint64_t seed,
+                                          uint64_t frame0, double fps, double pulse_hz, double amplitude, float* out,
+                                          void* stream) {
   if (!ctx || height < 1 || width < 1 || count < 0 || noise_sigma < 0 || !(exposure > 0)) return OXM_ERR_ARGUMENT;
+  // synth.py:209-216 argument checks (amplitude 0 = static phantom frames)
+  if (amplitude < 0 || (amplitude > 0 && !(fps > 0 && pulse_hz > 0 && pulse_hz < fps / 2))) return OXM_ERR_ARGUMENT;
   if (count == 0) return OXM_OK;
   if (!truth || !out) return OXM_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
@@ -190,8 +198,16 @@ extern "C" int oxm_synth_frames_f32(const oxm_ctx* ctx, const float* truth, int6
   const int64_t npx = height * width;
   const uint2 key = make_uint2((unsigned)seed, (unsigned)(seed >> 32));
   synth_kernel<<<grid_1d(npx * count, kSynthThreads), kSynthThreads, 0, as_stream(stream)>>>(
-      s, truth, npx, count, (float)noise_sigma, (float)exposure, key, (unsigned long long)frame0, out);
+      s, truth, npx, count, (float)noise_sigma, (float)exposure, key, (unsigned long long)frame0, amplitude, pulse_hz,
+      amplitude > 0 ? fps : 1.0, out);
   return check_launch("synth_frames");
+}
+
+extern "C" int oxm_synth_frames_f32(const oxm_ctx* ctx, const float* truth, int64_t height, int64_t width,
+                                    int64_t count, double noise_sigma, double exposure, uint64_t seed,
+                                    uint64_t frame0, float* out, void* stream) {
+  return oxm_synth_pulse_frames_f32(ctx, truth, height, width, count, noise_sigma, exposure, seed, frame0, 1.0, 0.0,
+                                    0.0, out, stream);
 }
 
 extern "C" int oxm_patch_mean_f32(const float* thb, int64_t batch, int64_t height, int64_t width, int x, int y,

@@ -373,7 +373,13 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
           off[p + 1] = a2[r].y;
         }
       }
-      any_fb |= !(vmin[r][0] >= thr) || (two && !(vmin[r][1] >= thr));  // also catches NaN
+      // fminf drops NaN operands, so a NaN band (non-finite input: flagged by the
+      // low-pass kernel, and launch() callers must check the flags) is caught
+      // through the fit sums it poisons instead
+      const bool nan0 = isnan(a0[r].x + a1[r].x), nan1 = two && isnan(a0[r].y + a1[r].y);
+      vmin[r][0] = nan0 ? -1.f : vmin[r][0];
+      vmin[r][1] = nan1 ? -1.f : vmin[r][1];
+      any_fb |= !(vmin[r][0] >= thr) || (two && !(vmin[r][1] >= thr));
     }
   }
   // cancellation guard: queue pixels for the fp64 fixup kernel (rare)
@@ -781,7 +787,7 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
   if (fixup_ev) cudaEventRecord(fixup_ev, s);
-  const unsigned fb_grid = 148 * OXM_FB_CTAS_PER_SM;
+  const unsigned fb_grid = (unsigned)device_sms() * OXM_FB_CTAS_PER_SM;
   if (!exact_blocks_active(ops)) {
     px_fallback_kernel<KL, Src, kFbAll><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
                                                                   w.fb_list, thb, so2, hbo, hb, off, nullptr, nullptr,

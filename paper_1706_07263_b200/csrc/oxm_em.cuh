@@ -325,7 +325,10 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   constexpr bool kYSoa = OUT != SpecOut::kAosF64;
   int64_t idx[NS];
   int nfit[NS];
-  bool exact[NS];  // TAIL: this lane runs the coefficient from fit #1 (no guard)
+  // TAIL state per lane: 0 = exact (runs the coefficient from fit #1, no guard),
+  // 1 = continuing a hand-over (guarded), 2 = the next step is the fp64 redo of the
+  // lead-in's uncommitted fit
+  int mode[NS];
   unsigned wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats; < 2^32 per warp)
   double x[NS][3];
   auto ycol = [&](int sl, int k) -> double& { return e[(sl * (L + kEmColExtra) + L + 4 + k) * es]; };
@@ -338,14 +341,14 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
       x[sl][k] = f > 1 ? (double)io.xh[k * io.n + i] : io.xinit[k * io.n + i];
     }
     nfit[sl] = f;
-    exact[sl] = f <= 1;
+    mode[sl] = f <= 1 ? 0 : 2;
   };
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) {
     const int64_t i = next + 32 * sl + lane;
     idx[sl] = i < stop ? coef(i) : -1;
     nfit[sl] = 1;
-    exact[sl] = true;
+    mode[sl] = 0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) ycol(sl, k) = x[sl][k] = 0.0;
     if (idx[sl] >= 0) load(sl, idx[sl]);
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
       const int64_t mine = r < avail ? next + r : fresh + (r - avail);
       idx[sl] = mine < (r < avail ? stop : fresh_end) ? coef(mine) : -1;
       nfit[sl] = 1;
-      exact[sl] = true;
+      mode[sl] = 0;
       if (idx[sl] >= 0) load(sl, idx[sl]);
     }
     if (avail < need) {
@@ -452,11 +455,16 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
         if constexpr (TAIL) {
           // the state still carries the lead-in's fp32 perturbation: a stop
           // decision near the threshold (or one forced by max_iters) is not
-          // trusted -- redo the coefficient in exact fp64 from fit #1
-          restart = !exact[sl] && ((dn2 > ops.guard_lo * xm2 && dn2 < ops.guard_hi * xm2) || nfit[sl] >= ops.max_iters);
+          // trusted -- redo the coefficient in exact fp64 from fit #1.  The
+          // first tail step redoes the lead-in's uncommitted fit from the fp32
+          // state itself, so its decision sees that perturbation undamped: a
+          // stop there is never trusted either (rare: rel must fall from
+          // > K tol to < tol in one fit)
+          restart = mode[sl] != 0 && ((dn2 > ops.guard_lo * xm2 && dn2 < ops.guard_hi * xm2) ||
+                                      nfit[sl] >= ops.max_iters || (mode[sl] == 2 && done));
+          mode[sl] = restart ? 0 : min(mode[sl], 1);
           if (restart) {
             done = false;
-            exact[sl] = true;
             nfit[sl] = 1;
           }
         }

@@ -151,7 +151,12 @@ class HybridMapEngine:
         use one engine per concurrent stream.
 
         ``frames``: CUDA (B, H, W, 3) float32 values, or uint16 PPM counts
-        (sample = count * ``scale``; ``big_endian`` as stored in the file)."""
+        (sample = count * ``scale``; ``big_endian`` as stored in the file).
+
+        Data errors (non-finite samples, negative low-pass) only set bits in
+        ``out.flags``: call ``check_flags(out)`` once the stream has finished
+        (``run`` and ``maps_from_host`` do) -- the maps of a launch with flags
+        set are not the reference's (it raises instead of returning them)."""
         if frames.dim() != 4 or frames.shape[-1] != 3 or not frames.is_cuda:
             raise ArgumentError("frames must be a CUDA (B, H, W, 3) tensor")
         if frames.dtype not in (torch.float32, torch.uint16):

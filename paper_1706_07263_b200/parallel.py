@@ -83,10 +83,14 @@ def gather_chunk_to_root(local: torch.Tensor, n_frames: int, chunk: int, c: int,
         lo, hi = shard_range(n_frames, r, ws)
         a, b = min(hi, lo + c * chunk), min(hi, lo + (c + 1) * chunk)
         spans.append((a, b))
+    # gloo moves host tensors only: CUDA maps are staged through host memory
+    # (the multi-rank functional check on one GPU); NCCL sends device memory
+    host = dist.get_backend() == "gloo" and local.is_cuda
     if rank != root:
         a, b = spans[rank]
         if b > a:
-            dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), root)])[0].wait()
+            t = local.contiguous().cpu() if host else local.contiguous()
+            dist.batch_isend_irecv([dist.P2POp(dist.isend, t, root)])[0].wait()
         return None
     ops, out = [], []
     for r in range(ws):
@@ -94,9 +98,12 @@ def gather_chunk_to_root(local: torch.Tensor, n_frames: int, chunk: int, c: int,
         if r == root:
             out.append((a, local))
         elif b > a:
-            buf = torch.empty((b - a,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+            buf = torch.empty((b - a,) + tuple(local.shape[1:]), dtype=local.dtype,
+                              device="cpu" if host else local.device)
             ops.append(dist.P2POp(dist.irecv, buf, r))
             out.append((a, buf))
     for w in (dist.batch_isend_irecv(ops) if ops else []):
         w.wait()
+    if host:
+        out = [(a, t if t.device == local.device else t.to(local.device)) for a, t in out]
     return sorted(out, key=lambda t: t[0])

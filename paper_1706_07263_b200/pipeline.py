@@ -201,7 +201,55 @@ def estimate_sequence(
     cfg: PipelineConfig,
     timings: list | None = None,
 ) -> Iterator[ConcentrationMap]:
-    """Stream maps for a frame sequence (pipeline.py:220-245)."""
+    """Stream maps for a frame sequence (pipeline.py:220-245).
+
+    Hybrid RgbImage sequences are pipelined over two slots: while map i is
+    copied back and handed out, frame i+1 is already uploaded and running
+    (K6 fp64, workspaces reused, one stream per slot), so the sequence is
+    bound by host copies and PCIe, not by the kernels.  Frame i+1 is read from
+    the iterator before map i is yielded; errors keep the reference's order
+    (a dimension change or bad frame raises after every earlier map has been
+    yielded).  ``timings`` gets, per frame, the wall-clock seconds the
+    pipeline spent on it (from its submission, or from the previous map being
+    ready if later, until its map is ready)."""
+    if cfg.mode != "hybrid":
+        yield from _sequence_plain(frames, sensitivity, basis, cfg, timings)
+        return
+    runner = None
+    pending: list = []
+    last_ready = None
+    shape = None
+
+    def finish(job):
+        nonlocal last_ready
+        cmap, t_sub = runner.collect(job)
+        t = time.perf_counter()
+        if timings is not None:
+            timings.append(t - max(t_sub, last_ready if last_ready is not None else t_sub))
+        last_ready = t
+        return cmap
+
+    for frame in frames:
+        dims = (frame.height, frame.width)
+        if shape is None:
+            shape = dims
+        if dims != shape or not isinstance(frame, RgbImage):
+            while pending:
+                yield finish(pending.pop(0))
+            if dims != shape:
+                raise DataError(f"frame dimensions changed mid-stream: {shape} -> {dims}")
+            yield estimate_frame(frame, sensitivity, basis, cfg)[1]  # raises the reference's error
+            continue
+        if runner is None:
+            runner = _SequenceRunner(sensitivity, basis, cfg, dims)
+        if len(pending) == 2:
+            yield finish(pending.pop(0))
+        pending.append(runner.submit(frame))
+    while pending:
+        yield finish(pending.pop(0))
+
+
+def _sequence_plain(frames, sensitivity, basis, cfg, timings):
     shape = None
     for frame in frames:
         dims = (frame.height, frame.width)
@@ -210,20 +258,72 @@ def estimate_sequence(
         elif dims != shape:
             raise DataError(f"frame dimensions changed mid-stream: {shape} -> {dims}")
         t0 = time.perf_counter()
-        cmap = _frame_map(frame, sensitivity, basis, cfg)
+        cmap = estimate_frame(frame, sensitivity, basis, cfg)[1]
         if timings is not None:
             timings.append(time.perf_counter() - t0)
         yield cmap
 
 
-def _frame_map(frame, sensitivity, basis, cfg: PipelineConfig) -> ConcentrationMap:
-    """estimate_frame's map only: the sequence API discards the cube
-    (pipeline.py:241-245), so the hybrid path skips materialising it."""
-    if cfg.mode != "hybrid" or not isinstance(frame, RgbImage):
-        return estimate_frame(frame, sensitivity, basis, cfg)[1]
-    check_grids(sensitivity.grid, basis.grid)
-    ops = _hybrid_operators(sensitivity, basis, cfg)
-    out = hybrid_device(upload(frame.data[None], torch.float64, require_cuda()), ops, cfg.n_levels,
-                        cfg.calibration_scale, want_cube=False)
-    xs = download(out["x"][:, 0])
-    return ConcentrationMap(hbo=xs[0], hb=xs[1], offset=xs[2])
+class _SequenceRunner:
+    """Two pipeline slots for estimate_sequence: pinned host staging, device
+    frame, workspace and fp64 map planes per slot, each on its own stream."""
+
+    def __init__(self, sensitivity, basis, cfg: PipelineConfig, dims):
+        check_grids(sensitivity.grid, basis.grid)
+        H, W = dims
+        n = cfg.n_levels
+        if H < 2**n or W < 2**n:
+            raise ArgumentError(f"frame {H}x{W} is smaller than 2^{n} in one dimension")
+        self.lib = _native.load()
+        self.dev = require_cuda()
+        self.ctx = context(_hybrid_operators(sensitivity, basis, cfg), self.dev.index)
+        self.H, self.W, self.n, self.cal = H, W, n, float(cfg.calibration_scale)
+        hL, wL = level_dims(H, W, n)[-1]
+        self.ws_bytes = int(self.lib.oxm_hybrid_workspace_bytes(self.ctx.handle, 1, H, W, n))
+        d = dict(device=self.dev)
+        self.slots = []
+        for _ in range(2):
+            self.slots.append({
+                "stream": torch.cuda.Stream(device=self.dev),
+                "h_in": torch.empty((1, H, W, 3), dtype=torch.float64).pin_memory(),
+                "d_in": torch.empty((1, H, W, 3), dtype=torch.float64, **d),
+                "ws": torch.empty(self.ws_bytes, dtype=torch.uint8, **d),
+                "x": torch.empty((3, 1, H, W), dtype=torch.float64, **d),
+                "fits": torch.empty((1, hL, wL), dtype=torch.int32, **d),
+                "flags": torch.zeros(1, dtype=torch.int32, **d),
+                "h_x": torch.empty((3, 1, H, W), dtype=torch.float64).pin_memory(),
+                "h_flags": torch.zeros(1, dtype=torch.int32).pin_memory(),
+                "done": torch.cuda.Event(),
+            })
+        self.turn = 0
+
+    def submit(self, frame: RgbImage):
+        sl = self.slots[self.turn]
+        self.turn ^= 1
+        t_sub = time.perf_counter()
+        sl["done"].synchronize()  # the slot's previous frame has been collected
+        np.copyto(sl["h_in"].numpy()[0], frame.data)
+        s = sl["stream"]
+        with torch.cuda.stream(s):
+            sl["d_in"].copy_(sl["h_in"], non_blocking=True)
+            sl["flags"].zero_()
+            x = sl["x"]
+            st = self.lib.oxm_hybrid_frame_f64(
+                self.ctx.handle, ptr(sl["d_in"]), 1, self.H, self.W, self.n, self.cal, ptr(sl["ws"]), self.ws_bytes,
+                None, ptr(x[0]), ptr(x[1]), ptr(x[2]), ptr(sl["fits"]), ptr(sl["flags"]), stream_handle(s), None)
+            _native.check(st, "hybrid_frame_f64")
+            sl["h_x"].copy_(x, non_blocking=True)
+            sl["h_flags"].copy_(sl["flags"], non_blocking=True)
+            sl["done"].record(s)
+        return sl, t_sub
+
+    def collect(self, job):
+        sl, t_sub = job
+        sl["done"].synchronize()
+        f = int(sl["h_flags"][0])
+        if f & _native.FLAG_NONFINITE:
+            raise ArgumentError("image contains non-finite values")
+        if f & _native.FLAG_NEGATIVE_LL:
+            raise ArgumentError("low-pass coefficients must be finite and non-negative")
+        xs = sl["h_x"].numpy()[:, 0]
+        return ConcentrationMap(hbo=xs[0].copy(), hb=xs[1].copy(), offset=xs[2].copy()), t_sub

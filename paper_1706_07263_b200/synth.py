@@ -11,7 +11,9 @@ benchmark batches on the device.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
+from typing import Iterator
 
 import numpy as np
 
@@ -175,6 +177,54 @@ def generate_phantom(
     return truth, cube, synthesize_rgb(cube, sensitivity, exposure)
 
 
+def _check_pulse(fps: float, pulse_hz: float, amplitude: float) -> None:
+    """synth.py:209-216 argument checks (duration checked by the caller)."""
+    if fps <= 0:
+        raise ArgumentError(f"fps must be > 0, got {fps}")
+    if not 0 < pulse_hz < fps / 2:
+        raise ArgumentError(f"pulse_hz must satisfy 0 < pulse_hz < fps/2 = {fps / 2:g}, got {pulse_hz}")
+    if amplitude < 0:
+        raise ArgumentError(f"amplitude must be >= 0, got {amplitude}")
+
+
+def pulse_modulation(t: int, fps: float, pulse_hz: float, amplitude: float) -> float:
+    """Frame t's haemoglobin scale 1 + a sin(2 pi f t / fps) (synth.py:218)."""
+    return 1.0 + amplitude * math.sin(2.0 * math.pi * pulse_hz * t / fps)
+
+
+def pulse_sequence(
+    spec: PhantomSpec,
+    fps: float,
+    duration_s: float,
+    pulse_hz: float,
+    amplitude: float,
+    sensitivity: CameraSensitivity,
+    basis: ChromophoreBasis,
+    exposure: float = 1.0,
+) -> Iterator[RgbImage]:
+    """Frames whose THb truth is modulated by a sinusoidal pulse
+    (synth.py:187-231): frame t scales hbo and hb by 1 + a sin(2 pi f t/fps),
+    then forward model, per-frame reflectance noise (the reference's seeded
+    draw order, so frames are bit-identical to it) and RGB synthesis.  Host
+    input generator, like generate_phantom; ``device_pulse_frames`` renders
+    the same sequence on the GPU for long videos."""
+    if fps <= 0:
+        raise ArgumentError(f"fps must be > 0, got {fps}")
+    if duration_s <= 0:
+        raise ArgumentError(f"duration_s must be > 0, got {duration_s}")
+    _check_pulse(fps, pulse_hz, amplitude)
+    truth = truth_map(spec)
+    n_frames = int(round(duration_s * fps))
+    rng = np.random.default_rng(spec.seed)
+    for t in range(n_frames):
+        m = pulse_modulation(t, fps, pulse_hz, amplitude)
+        cube = forward_msi(ConcentrationMap(hbo=truth.hbo * m, hb=truth.hb * m, offset=truth.offset), basis)
+        data = cube.data
+        if spec.noise_sigma > 0:
+            data = np.clip(data + rng.normal(0.0, spec.noise_sigma, size=data.shape), REFLECTANCE_FLOOR, None)
+        yield synthesize_rgb(SpectralCube(grid=cube.grid, data=data), sensitivity, exposure)
+
+
 def phantom_rgb_f32(
     height: int,
     width: int,
@@ -215,14 +265,48 @@ def device_frames(
     from .device import ptr, stream_handle
     from .operators import context, make_operator_set
 
+    return device_pulse_frames(truth, sensitivity, basis, count, noise_sigma=noise_sigma, seed=seed, frame0=frame0,
+                               exposure=exposure, device=device)
+
+
+def device_pulse_frames(
+    truth: ConcentrationMap,
+    sensitivity: CameraSensitivity,
+    basis: ChromophoreBasis,
+    count: int,
+    *,
+    fps: float = 1.0,
+    pulse_hz: float = 0.0,
+    amplitude: float = 0.0,
+    noise_sigma: float = 0.01,
+    seed: int = 0,
+    frame0: int = 0,
+    exposure: float = 1.0,
+    device=None,
+):
+    """pulse_sequence on the device (synth.py:187-231, oxm_synth_pulse_frames_f32):
+    frames frame0 .. frame0 + count - 1 of the pulse-modulated sequence of
+    ``truth`` as a (count, H, W, 3) float32 CUDA tensor.  The per-frame scale
+    1 + a sin(2 pi f t / fps) is the reference's; the noise is the kernel's
+    counter-based Philox stream (statistically, not bitwise, the reference's).
+    amplitude 0 gives static phantom frames (device_frames)."""
+    import torch
+
+    from . import _native
+    from .device import ptr, stream_handle
+    from .operators import context, make_operator_set
+
     check_grids(sensitivity.grid, basis.grid)
+    if amplitude != 0.0:
+        _check_pulse(fps, pulse_hz, amplitude)
     dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
     ops = make_operator_set(n_bands=basis.grid.count, xi=basis.xi, sens=sensitivity.c)
     ctx = context(ops, dev.index)
     x = torch.from_numpy(np.ascontiguousarray(truth.stacked(), dtype=np.float32)).to(dev)
     H, W = truth.hbo.shape
     out = torch.empty((count, H, W, 3), dtype=torch.float32, device=dev)
-    st = _native.load().oxm_synth_frames_f32(ctx.handle, ptr(x), H, W, count, float(noise_sigma), float(exposure),
-                                             int(seed) & (2**64 - 1), int(frame0), ptr(out), stream_handle())
-    _native.check(st, "synth_frames")
+    st = _native.load().oxm_synth_pulse_frames_f32(ctx.handle, ptr(x), H, W, count, float(noise_sigma),
+                                                   float(exposure), int(seed) & (2**64 - 1), int(frame0), float(fps),
+                                                   float(pulse_hz), float(amplitude), ptr(out), stream_handle())
+    _native.check(st, "synth_pulse_frames")
     return out

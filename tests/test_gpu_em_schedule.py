@@ -165,3 +165,37 @@ def test_schedule_extreme_exposure(cuda, sensitivity, basis, gain):
     assert np.max(np.abs(t[ok] - rt[ok]) / np.abs(rt[ok]), initial=0.0) < 1e-5
     oks = ~np.isnan(rs)
     assert np.max(np.abs(s[oks] - rs[oks]), initial=0.0) < 5e-6
+
+
+def test_bench_configuration_vs_oracle(cuda, sensitivity, basis):
+    """The bench's own workload (bench.py: 64 device-synthesised textured 1080p
+    frames, n = 2) through the engine exactly as timed: 8.3 M low-pass
+    coefficients, so the exact-block pass runs the one-lane persistent kernel
+    over the selection list (kExactSeqMinN = 2^21).  One frame of each of the
+    four truth maps, plus the last frame, against the pinned oracle: fit counts
+    bit-exact, THb <= 1e-4 relative, SO2 <= 1e-5 absolute, NaN pattern
+    identical; and every coefficient of the batch against the all-fp64 EM
+    schedule (em_lead=None): 0 fit-count differences."""
+    import bench
+
+    B, H, W = 64, 1080, 1920
+    frames = bench.make_frames(B, H, W, 0.3, 0, cuda)
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2))
+    out = eng.run(frames, fits=True)
+    torch.cuda.synchronize()
+    c = eng.em_counters(B, H, W)
+    nll = out.fits.numel()
+    assert nll >= 2**21 and c["exact_blocks"] > 0 and c["restarts"] > 0
+    ref64 = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2), em_lead=None).run(frames, fits=True)
+    flips = int((ref64.fits != out.fits).sum())
+    assert flips == 0, f"{flips} fit-count differences vs the all-fp64 schedule over {nll} coefficients"
+    thb, so2, fits = out.thb.cpu().numpy(), out.so2.cpu().numpy(), out.fits.cpu().numpy()
+    host = frames.cpu().numpy().astype(np.float64)
+    for b in (0, 16, 32, 48, 63):
+        ref = O.estimate_frame(host[b], sensitivity.c, basis.xi, n_levels=2, want_cube=False,
+                               threads=O.default_threads())
+        assert np.array_equal(fits[b], ref["fits"]), f"frame {b}: {np.sum(fits[b] != ref['fits'])} fit-count flips"
+        assert np.array_equal(np.isnan(so2[b]), np.isnan(ref["so2"])), b
+        assert np.all(np.abs(thb[b] - ref["thb"]) <= 1e-4 * np.abs(ref["thb"])), b
+        ok = ~np.isnan(ref["so2"])
+        assert np.max(np.abs(so2[b][ok] - ref["so2"][ok])) <= 1e-5, b

@@ -86,3 +86,37 @@ def test_ppm_to_spc1_files(cuda, tmp_path, sensitivity, basis):
         bad = tmp_path / "b.ppm"
         bad.write_bytes(b"P6\n100 72\n255\n" + b"\0" * 10)
         read_ppm_raw(bad)
+
+
+def test_device_pulse_frames_match_pulse_sequence(cuda, golden, sensitivity, basis):
+    """Device pulse_sequence (oxm_synth_pulse_frames_f32) without noise equals
+    the reference's noise-free pulse_sequence frames (golden) to fp32 rounding
+    of the forward model; frame0 offsets the pulse phase like frame index t."""
+    g = golden("api")
+    ref = g["pulse_clean"]
+    spec = ox.tissue_phantom_spec(24, 32, seed=5, noise_sigma=0.0, texture_density=0.3)
+    truth = synth.truth_map(spec)
+    dev = synth.device_pulse_frames(truth, sensitivity, basis, ref.shape[0], fps=30.0, pulse_hz=1.2, amplitude=0.1,
+                                    noise_sigma=0.0, device=cuda).double().cpu().numpy()
+    assert np.max(np.abs(dev - ref) / np.abs(ref)) < 2e-5
+    tail = synth.device_pulse_frames(truth, sensitivity, basis, 2, fps=30.0, pulse_hz=1.2, amplitude=0.1,
+                                     noise_sigma=0.0, frame0=3, device=cuda).double().cpu().numpy()
+    assert np.max(np.abs(tail - ref[3:5]) / np.abs(ref[3:5])) < 2e-5
+    # the modulation is what moves THb: frames differ from the static phantom
+    static = synth.device_frames(truth, sensitivity, basis, 1, noise_sigma=0.0, device=cuda).double().cpu().numpy()
+    assert np.max(np.abs(dev[1] - static[0])) > 1e-3
+    with pytest.raises(ox.ArgumentError):
+        synth.device_pulse_frames(truth, sensitivity, basis, 1, fps=30.0, pulse_hz=16.0, amplitude=0.1, device=cuda)
+
+
+def test_analyze_pulse_matches_reference(cuda, golden):
+    """analyze_pulse with the patch mean on the device (fp32 THb) against the
+    reference's all-host report: trace to fp32 rounding, same peak."""
+    g = golden("api")
+    maps = []
+    for k in range(90):
+        m = 1.0 + 0.05 * np.sin(2 * np.pi * 1.1 * k / 30.0)
+        maps.append(ox.ConcentrationMap(hbo=g["ap_hbo"] * m, hb=g["ap_hb"] * m, offset=g["ap_off"]))
+    rep = ox.analyze_pulse(maps, (4, 4, 16, 16), 30.0)
+    assert np.max(np.abs(rep.trace.values - g["ap_trace"]) / g["ap_trace"]) < 1e-6
+    assert abs(rep.peak_hz - g["ap_peak"][0]) < 1e-3 and abs(rep.bpm - g["ap_peak"][2]) < 0.06

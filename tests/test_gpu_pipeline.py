@@ -131,8 +131,12 @@ def _engine_vs_oracle(cuda, sensitivity, basis, frames64, n, *, fits=True):
 def test_engine_cfg1_256(cuda, golden, sensitivity, basis):
     g = golden("frames")
     eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=1))
-    out = eng.run(torch.from_numpy(g["rgb5"][None].astype(np.float32)).to(cuda))
+    out = eng.run(torch.from_numpy(g["rgb5"][None].astype(np.float32)).to(cuda), fits=True)
     assert_maps_close(out.thb[0].cpu().numpy(), out.so2[0].cpu().numpy(), g["thb5"], g["so2"+"5"])
+    # the fp32 engine's discrete decisions: per-coefficient fit counts == the oracle's
+    # (the oracle is pinned bit-for-bit to the reference on this golden frame)
+    ref = O.estimate_frame(g["rgb5"], sensitivity.c, basis.xi, n_levels=1, want_cube=False)
+    assert np.array_equal(out.fits[0].cpu().numpy(), ref["fits"])
 
 
 @pytest.mark.parametrize("H,W,n,td", [(37, 23, 2, 0.3), (45, 70, 3, 0.3), (64, 64, 2, 0.0), (9, 15, 1, 0.0)])
@@ -290,3 +294,29 @@ def test_ppm_u16_path(cuda, sensitivity, basis):
         so2 = torch.empty(counts.shape[:3], dtype=torch.float32).pin_memory()
         eng.maps_from_host(host, thb, so2, chunk=1, scale=scale, big_endian=True)
         assert torch.equal(thb, out.thb.cpu())
+
+
+def test_estimate_sequence_pipelined(cuda, sensitivity, basis):
+    """The two-slot pipelined estimate_sequence returns exactly estimate_frame's
+    maps, in order, with the reference's error order (every earlier map is
+    yielded before a bad frame raises) -- pipeline.py:220-245."""
+    frames = [ox.RgbImage(synth.phantom_rgb_f32(48, 64, s, sensitivity, basis)) for s in range(5)]
+    cfg = ox.PipelineConfig(n_levels=2)
+    timings = []
+    maps = list(ox.estimate_sequence(frames, sensitivity, basis, cfg, timings=timings))
+    assert len(maps) == 5 and len(timings) == 5 and all(t >= 0 for t in timings)
+    for f, m in zip(frames, maps):
+        _, ref = ox.estimate_frame(f, sensitivity, basis, cfg)
+        assert np.array_equal(m.stacked(), ref.stacked())
+    bad = -np.array(frames[2].data)  # negative low-pass: flagged on the device (bayes.py:77-78)
+    seq = ox.estimate_sequence(frames[:2] + [ox.RgbImage(bad)] + frames[3:], sensitivity, basis, cfg)
+    got = [next(seq), next(seq)]
+    assert np.array_equal(got[1].stacked(), maps[1].stacked())
+    with pytest.raises(ox.ArgumentError):
+        next(seq)
+    seq = ox.estimate_sequence(frames[:3] + [ox.RgbImage(np.ones((48, 66, 3)))], sensitivity, basis, cfg)
+    assert len([next(seq) for _ in range(3)]) == 3
+    with pytest.raises(ox.DataError, match="mid-stream"):
+        next(seq)
+    with pytest.raises(ox.ArgumentError, match="smaller"):
+        list(ox.estimate_sequence([ox.RgbImage(np.ones((2, 2, 3)))], sensitivity, basis, cfg))
