@@ -32,9 +32,11 @@
 // fp32 path: HBM traffic is the frame read twice, the per-block spectra
 // (8 B/band/coefficient) once, and the maps written once.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "oxm_em.cuh"
+#include "oxm_tma.cuh"
 
 namespace oxm {
 namespace {
@@ -198,6 +200,249 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
       xinit[nll + idx] = x1;
       xinit[2 * nll + idx] = x2;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged low-pass kernel (fp32 frames, one pass of n <= 3 levels): the
+// same outputs as ll_kernel<PlainSrc<float>, NLV, true>, bit for bit.
+//
+// The batch is viewed as one 2D plane of B*H rows x 3W floats.  A CTA owns a
+// tile of TY x TX low-pass blocks (TY 2^n rows x TX 2^n pixels), staged into
+// shared memory by one cp.async.bulk.tensor per tile, double-buffered: while
+// the CTA reduces tile i, the TMA unit streams tile i + 1 (persistent grid,
+// tiles strided by gridDim).  Each thread then owns one low-pass coefficient:
+// interior blocks read their rows as conflict-free vector loads with
+// compile-time offsets; edge blocks (a tile hanging over the frame) take the
+// reference's per-level edge replication through clamped coordinates, which
+// always stay inside the tile.  Rows of a tile that belong to the next frame
+// (or lie past the batch, zero-filled) are never read.  A sample is
+// non-finite iff the fp64 low-pass sum over the block is (fp32 inputs cannot
+// overflow fp64), so the flag test is 3 compares per coefficient.
+template <int NLV>
+struct LlTma {
+  static constexpr int S = 1 << NLV;
+  static constexpr int kThreads = NLV == 3 ? 64 : 128;   // coefficients (threads) per tile
+  static constexpr int TX = NLV == 1 ? 32 : (NLV == 2 ? 16 : 8);
+  static constexpr int TY = kThreads / TX;
+  static constexpr int kRowF = TX * S * 3;                // floats per tile row (box inner dim, 192)
+  static constexpr int kRows = TY * S;
+  static constexpr int kTileF = kRowF * kRows;
+  static constexpr uint32_t kTileBytes = kTileF * 4;
+  static constexpr size_t kSmem = 2 * (size_t)kTileBytes;
+};
+
+// level-K low-pass of an interior block whose origin sample (row 0, col 0,
+// channel c) is p: every offset a compile-time constant
+template <int K, int ROWF>
+struct LpInterior {
+  __device__ __forceinline__ static double at(const float* p) {
+    constexpr int h = 1 << (K - 1);
+    const double a = LpInterior<K - 1, ROWF>::at(p);
+    const double b = LpInterior<K - 1, ROWF>::at(p + 3 * h);
+    const double c = LpInterior<K - 1, ROWF>::at(p + ROWF * h);
+    const double d = LpInterior<K - 1, ROWF>::at(p + ROWF * h + 3 * h);
+    return 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b), c), d);
+  }
+};
+template <int ROWF>
+struct LpInterior<0, ROWF> {
+  __device__ __forceinline__ static double at(const float* p) { return (double)*p; }
+};
+
+// level-K low-pass at level-K position (i, j) with the reference's per-level
+// edge replication (LowPass<> on a tile whose origin is frame pixel (r0, c0))
+template <int K, int ROWF>
+struct LpTile {
+  __device__ __forceinline__ static double at(const float* t, int r0, int c0, const LevelDims& d, int i, int j, int c) {
+    const int i1 = (int)min((int64_t)(2 * i + 1), d.h[K - 1] - 1);
+    const int j1 = (int)min((int64_t)(2 * j + 1), d.w[K - 1] - 1);
+    const double a = LpTile<K - 1, ROWF>::at(t, r0, c0, d, 2 * i, 2 * j, c);
+    const double b = LpTile<K - 1, ROWF>::at(t, r0, c0, d, 2 * i, j1, c);
+    const double cc = LpTile<K - 1, ROWF>::at(t, r0, c0, d, i1, 2 * j, c);
+    const double dd = LpTile<K - 1, ROWF>::at(t, r0, c0, d, i1, j1, c);
+    return 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b), cc), dd);
+  }
+};
+template <int ROWF>
+struct LpTile<0, ROWF> {
+  __device__ __forceinline__ static double at(const float* t, int r0, int c0, const LevelDims&, int i, int j, int c) {
+    return (double)t[(i - r0) * ROWF + (j - c0) * 3 + c];
+  }
+};
+
+template <int NLV>
+__global__ void __launch_bounds__(LlTma<NLV>::kThreads) ll_tma_kernel(
+    const __grid_constant__ DevOps ops, const __grid_constant__ CUtensorMap tmap, int64_t batch, LevelDims d,
+    double* __restrict__ ybar, int64_t nll, uint32_t* flags, double* __restrict__ xinit,
+    uint8_t* __restrict__ blkflag, int tiles_x, int tiles_y) {
+  using G = LlTma<NLV>;
+  extern __shared__ __align__(128) float tiles[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tid = threadIdx.x;
+  const int64_t per_frame = (int64_t)tiles_x * tiles_y;
+  const int64_t ntiles = batch * per_frame;
+  const int H0 = (int)d.h[0], W0 = (int)d.w[0], hL = (int)d.h[NLV], wL = (int)d.w[NLV];
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t, int s) {
+    if (t >= ntiles) return;
+    const int64_t f = t / per_frame;
+    const int r = (int)(t - f * per_frame);
+    const int ty = r / tiles_x, tx = r - ty * tiles_x;
+    mbar_expect_tx(&bar[s], G::kTileBytes);
+    tma_load_2d(tiles + s * G::kTileF, &tmap, tx * G::kRowF, (int)(f * H0) + ty * G::kRows, &bar[s]);
+  };
+  if (tid == 0) {
+    issue(blockIdx.x, 0);
+    issue(blockIdx.x + gridDim.x, 1);
+  }
+  const int ly = tid / G::TX, lx = tid - ly * G::TX;
+  const double inv = ldexp(1.0, -NLV);  // exact
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    const int s = it & 1;
+    const int64_t f = t / per_frame;
+    const int r = (int)(t - f * per_frame);
+    const int ty = r / tiles_x, tx = r - ty * tiles_x;
+    const int by = ty * G::TY + ly, bx = tx * G::TX + lx;
+    mbar_wait(&bar[s], (it >> 1) & 1);
+    const float* tile = tiles + s * G::kTileF;
+    if (by < hL && bx < wL) {
+      double ll[3];
+      const int py = by * G::S, px = bx * G::S;
+      if (py + G::S <= H0 && px + G::S <= W0) {
+        const float* p = tile + ly * G::S * G::kRowF + lx * G::S * 3;
+        if constexpr (NLV == 2) {
+          float v[4][12];
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const float4 w = *reinterpret_cast<const float4*>(p + rr * G::kRowF + 4 * q);
+              v[rr][4 * q] = w.x;
+              v[rr][4 * q + 1] = w.y;
+              v[rr][4 * q + 2] = w.z;
+              v[rr][4 * q + 3] = w.w;
+            }
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double l1[2][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const double a = v[2 * i][6 * j + c], b = v[2 * i][6 * j + 3 + c];
+                const double cc = v[2 * i + 1][6 * j + c], dd = v[2 * i + 1][6 * j + 3 + c];
+                l1[i][j] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b), cc), dd);
+              }
+            ll[c] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(l1[0][0], l1[0][1]), l1[1][0]), l1[1][1]);
+          }
+        } else if constexpr (NLV == 1) {
+          float v[2][6];
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+              const float2 w = *reinterpret_cast<const float2*>(p + rr * G::kRowF + 2 * q);
+              v[rr][2 * q] = w.x;
+              v[rr][2 * q + 1] = w.y;
+            }
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            ll[c] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn((double)v[0][c], (double)v[0][3 + c]), (double)v[1][c]),
+                                    (double)v[1][3 + c]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 3; ++c) ll[c] = LpInterior<NLV, G::kRowF>::at(p + c);
+        }
+      } else {
+        const int r0 = ty * G::kRows, c0 = tx * G::TX * G::S;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ll[c] = LpTile<NLV, G::kRowF>::at(tile, r0, c0, d, by, bx, c);
+      }
+      const int64_t idx = (f * hL + by) * wL + bx;
+      bool bad = false, neg = false;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        bad |= !isfinite(ll[c]);
+        ll[c] *= inv;
+        neg |= ll[c] < 0.0;
+        ybar[c * nll + idx] = ll[c];
+      }
+      if (flags && (bad || neg)) atomicOr(flags, (bad ? OXM_FLAG_NONFINITE : 0u) | (neg ? OXM_FLAG_NEGATIVE_LL : 0u));
+      if (blkflag) blkflag[idx] = 0;
+      if (xinit) {
+        double x0, x1, x2;
+        if (ops.L == 26)
+          start_fit<26>(ops, log_table_global(), ll[0], ll[1], ll[2], nullptr, x0, x1, x2);
+        else
+          start_fit<0>(ops, log_table_global(), ll[0], ll[1], ll[2], nullptr, x0, x1, x2);
+        xinit[idx] = x0;
+        xinit[nll + idx] = x1;
+        xinit[2 * nll + idx] = x2;
+      }
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0) {
+      fence_proxy_async();
+      issue(t + 2 * (int64_t)gridDim.x, s);
+    }
+  }
+}
+
+// TMA low-pass launch; returns false (nothing launched) when the frames
+// cannot be described by a tensor map -- the caller then runs ll_kernel
+template <int NLV>
+bool launch_ll_tma_n(const DevOps& ops, const float* frames, int64_t batch, const LevelDims& d, double* ybar,
+                     int64_t nll, uint32_t* flags, double* xinit, uint8_t* blkflag, cudaStream_t s) {
+  using G = LlTma<NLV>;
+  const int64_t H0 = d.h[0], W0 = d.w[0];
+  if (batch * H0 >= (int64_t(1) << 31) || 3 * W0 >= (int64_t(1) << 31)) return false;
+  CUtensorMap map;
+  if (!make_tmap_2d(&map, frames, false, (uint64_t)(3 * W0), (uint64_t)(batch * H0), (uint64_t)(12 * W0), G::kRowF,
+                    G::kRows))
+    return false;
+  auto kern = ll_tma_kernel<NLV>;
+  static bool attr_set = false;  // per template instance; the attribute is per function
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem) != cudaSuccess)
+      return false;
+    attr_set = true;
+  }
+  const int tiles_x = (int)ceil_div(d.w[NLV], G::TX), tiles_y = (int)ceil_div(d.h[NLV], G::TY);
+  const int64_t ntiles = batch * tiles_x * tiles_y;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::kThreads, G::kSmem) != cudaSuccess || per_sm < 1)
+    return false;
+  const int64_t grid = std::min<int64_t>(ntiles, (int64_t)device_sms() * per_sm);
+  kern<<<(unsigned)grid, G::kThreads, G::kSmem, s>>>(ops, map, batch, d, ybar, nll, flags, xinit, blkflag, tiles_x,
+                                                      tiles_y);
+  return true;
+}
+
+// OXM_LL_TMA=0 in the environment selects the per-thread-load ll_kernel
+// instead (A/B measurements; read once per process)
+inline bool ll_tma_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("OXM_LL_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool launch_ll_tma(const DevOps& ops, const float* frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll,
+                   uint32_t* flags, double* xinit, uint8_t* blkflag, cudaStream_t s) {
+  if (!ll_tma_enabled() || batch <= 0) return false;
+  switch (d.n) {
+    case 1: return launch_ll_tma_n<1>(ops, frames, batch, d, ybar, nll, flags, xinit, blkflag, s);
+    case 2: return launch_ll_tma_n<2>(ops, frames, batch, d, ybar, nll, flags, xinit, blkflag, s);
+    case 3: return launch_ll_tma_n<3>(ops, frames, batch, d, ybar, nll, flags, xinit, blkflag, s);
+    default: return false;
   }
 }
 
@@ -679,6 +924,10 @@ template <typename Src>
 int launch_ll(const DevOps& ops, const Src& frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll,
               uint32_t* flags, double* xinit, uint8_t* blkflag, cudaStream_t s) {
   const int n = d.n;
+  if constexpr (std::is_same<Src, PlainSrc<float>>::value) {
+    if (n <= 3 && launch_ll_tma(ops, frames.p, batch, d, ybar, nll, flags, xinit, blkflag, s))
+      return check_launch("hybrid_ll_tma");
+  }
   if (n <= 3) {
     launch_ll_pass<Src, true>(ops, frames, batch, d, n, ybar, nll, n, flags, xinit, blkflag, s);
     return check_launch("hybrid_ll");

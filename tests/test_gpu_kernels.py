@@ -48,6 +48,35 @@ def test_haar_fp32_within_1e6_of_plane_max(cuda, rng):
         assert np.max(np.abs(rec - img)) <= 1e-5 * np.max(np.abs(img))
 
 
+def test_haar_tma_tiles_fp64_bitwise(cuda, rng):
+    """RGB planes whose rows are 16-byte multiples take the TMA-tiled K1
+    (haar_fwd_tma_kernel): bit-identical to the oracle (= the reference) in
+    fp64, including edge tiles with per-level replication (odd heights, a
+    width that is not a tile multiple) and the chained second pass (n = 5);
+    non-finite samples anywhere in a tile -- interior, right / bottom edge --
+    raise like haar.py:133-134."""
+    for shape, n in [((1083, 1922, 3), 3), ((270, 482, 3), 2), ((99, 130, 3), 1), ((150, 202, 3), 5)]:
+        img = rng.normal(size=shape)
+        pyr = ox.forward(img, n)
+        ref = O.haar_forward(img, n)
+        for lv, rl in zip(pyr.levels, ref):
+            for name in ("lp", "dh", "dv", "dd"):
+                assert np.array_equal(getattr(lv, name), rl[name]), (shape, n, name)
+    for (r, c) in [(40, 37), (269, 483), (0, 0), (133, 300)]:
+        bad = rng.normal(size=(270, 484, 3))
+        bad[r, c, 1] = np.nan if r % 2 else np.inf
+        from paper_1706_07263_b200.haar import pyramid_device
+
+        with pytest.raises(ox.ArgumentError):
+            pyramid_device(torch.from_numpy(bad).to(cuda), 2)
+        with pytest.raises(ox.ArgumentError):
+            pyramid_device(torch.from_numpy(bad.astype(np.float32)).to(cuda), 2)
+    huge = np.full((64, 64, 3), 3.0e38, dtype=np.float32)  # finite, but an fp32 window sum overflows
+    from paper_1706_07263_b200.haar import pyramid_device
+
+    pyramid_device(torch.from_numpy(huge).to(cuda), 2)  # must not raise
+
+
 def test_haar_kats(cuda, rng):
     lv = ox.forward(np.full((2, 2), 3.5), 1).levels[0]
     assert lv.lp.shape == (1, 1) and lv.lp[0, 0] == 7.0

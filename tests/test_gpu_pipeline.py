@@ -145,6 +145,15 @@ def test_engine_small_and_odd(cuda, sensitivity, basis, H, W, n, td):
     _engine_vs_oracle(cuda, sensitivity, basis, frames, n)
 
 
+@pytest.mark.parametrize("H,W,n", [(1082, 1924, 2), (578, 724, 1), (1085, 1928, 3)])
+def test_engine_tma_edge_tiles(cuda, sensitivity, basis, H, W, n):
+    """Frames whose rows are 16-byte multiples take the TMA-staged low-pass
+    kernel (ll_tma_kernel); these sizes leave partial tiles and odd level
+    dimensions (per-level edge replication) at the right and bottom."""
+    frames = np.stack([synth.phantom_rgb_f32(H, W, s, sensitivity, basis) for s in (31,)])
+    _engine_vs_oracle(cuda, sensitivity, basis, frames, n)
+
+
 def test_engine_cfg2_stereo_pair(cuda, sensitivity, basis):
     # da Vinci SD: 720x576 per eye, two independent frames, n=1
     frames = np.stack([synth.phantom_rgb_f32(576, 720, s, sensitivity, basis) for s in (0, 1)])

@@ -65,6 +65,13 @@ def main():
     out["K1 haar_forward_f32 1080p n=2 C=3"] = timed(
         lambda i: lib.oxm_haar_forward_f32(frames[i].data_ptr(), H, W, C, n, planes[i].data_ptr(), flags.data_ptr(), s),
         4 * (H * W * C + nplanes * C))
+    planes64 = torch.empty((2, nplanes * C), dtype=torch.float64, device=dev)
+    frames64 = frames[:2].double().contiguous()
+    out["K1 haar_forward_f64 1080p n=2 C=3"] = timed(
+        lambda i: lib.oxm_haar_forward_f64(frames64[i % 2].data_ptr(), H, W, C, n, planes64[i % 2].data_ptr(),
+                                           flags.data_ptr(), s),
+        8 * (H * W * C + nplanes * C))
+    del planes64, frames64
     # K2: haar.inverse of a 26-band pyramid (the reference's spectral-domain inverse, pipeline.py:207)
     shapes = []
     prev = (H, W)
