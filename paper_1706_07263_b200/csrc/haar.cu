@@ -121,132 +121,155 @@ __global__ void __launch_bounds__(256) haar_fwd_kernel(const T* __restrict__ src
 }
 
 // ---------------------------------------------------------------------------
-// K1 with TMA-staged 2D tiles (3-channel HWC planes: RGB frames).  Same
-// per-thread work and the same arithmetic as haar_fwd_kernel (bit-identical
-// outputs), but the source samples come from shared memory: the plane is a 2D
-// tensor of h0 rows x 3 w0 elements, a CTA's tile of TY x TX coarsest blocks
-// (TY 2^NL rows x TX 2^NL pixels x 3 channels, 768 bytes per row) is brought
-// in by one cp.async.bulk.tensor, double-buffered across the tiles a
-// persistent CTA walks, and every thread reads its block's 2^NL x 2^NL
-// samples with compile-time offsets (interior blocks) or clamped offsets
-// (blocks at the right / bottom edge, whose replicated samples stay inside
-// the tile).  Thread t = (ly TX + lx) 3 + c owns channel c of block (ly, lx),
-// so output stores keep haar_fwd_kernel's warp-contiguous pattern.
+// K1 with TMA-staged 2D tiles in and out (3-channel HWC planes: RGB frames).
+// Same per-thread work and the same arithmetic as haar_fwd_kernel
+// (bit-identical outputs); only the data movement differs:
+//   in:  the plane is a 2D tensor of h0 rows x 3 w0 elements; a CTA's tile of
+//        TY x TX coarsest blocks (TY 2^NL rows x TX 2^NL pixels x 3 channels,
+//        768-byte rows) arrives by one cp.async.bulk.tensor load;
+//   out: every thread writes its coefficients into per-(level, plane) tiles
+//        in shared memory and one elected thread stores them with 4 NL
+//        cp.async.bulk.tensor stores (one tensor map per output plane; the
+//        hardware clips the parts of edge tiles outside a plane).
+// A persistent CTA walks tiles strided by gridDim; each thread copies its
+// block's samples to registers first, so the input buffer is released (and
+// the next tile's load issued) before the butterflies run.  Thread
+// t = (ly TX + lx) 3 + c owns channel c of block (ly, lx).  Interior blocks
+// read their samples at compile-time offsets, blocks at the right / bottom
+// edge through clamped ones (the reference's replication, inside the tile).
 template <typename T, int NL>
 struct FwdTma {
   static constexpr int S = 1 << NL;
-  static constexpr int TX = (sizeof(T) == 4 ? 64 : 32) / S;  // 768-byte tile rows
+  static constexpr int TX = (sizeof(T) == 4 ? 64 : 32) / S;  // 768-byte input tile rows
   static constexpr int TY = NL == 3 ? 8 : 128 / TX;
   static constexpr int kThreads = 3 * TX * TY;
   static constexpr int kRowE = TX * S * 3;
   static constexpr int kRows = TY * S;
   static constexpr int kTileE = kRowE * kRows;
   static constexpr uint32_t kTileBytes = kTileE * sizeof(T);
-  static constexpr size_t kSmem = 2 * (size_t)kTileBytes;
+  // output tile of level k (1..NL): (kRows >> k) rows x (kRowE >> k) elements, 4 planes each
+  __host__ __device__ static constexpr int out_elems(int k) { return (kRows >> k) * (kRowE >> k); }
+  __host__ __device__ static constexpr int out_offset(int k, int q) {  // elements from the staging base
+    int o = 0;
+    for (int l = 1; l < k; ++l) o += 4 * out_elems(l);
+    return o + q * out_elems(k);
+  }
+  static constexpr int kOutE = out_offset(NL + 1, 0);
+  static constexpr size_t kSmem = sizeof(T) * (size_t)(kTileE + kOutE);
+};
+
+struct FwdMaps {
+  CUtensorMap in;
+  CUtensorMap out[kMaxPass][4];  // level k+1, plane q (lp, dh, dv, dd)
 };
 
 template <typename T, int NL>
-__global__ void __launch_bounds__(FwdTma<T, NL>::kThreads) haar_fwd_tma_kernel(
-    const __grid_constant__ CUtensorMap tmap, FwdGeom g, T* __restrict__ out, uint32_t* flags, int tiles_x,
-    int tiles_y) {
+__global__ void __launch_bounds__(FwdTma<T, NL>::kThreads) haar_fwd_tma_kernel(const __grid_constant__ FwdMaps maps,
+                                                                             FwdGeom g, uint32_t* flags,
+                                                                             int tiles_x, int tiles_y) {
   using G = FwdTma<T, NL>;
   constexpr int S0 = G::S;
-  extern __shared__ __align__(128) unsigned char tile_raw[];
-  T* const tiles = reinterpret_cast<T*>(tile_raw);
-  __shared__ __align__(8) uint64_t bar[2];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* const tile = reinterpret_cast<T*>(smem_raw);
+  T* const stage = tile + G::kTileE;
+  __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   const int ntiles = tiles_x * tiles_y;
   const int H0 = (int)g.h[0], W0 = (int)g.w[0];
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    mbar_init(&bar, 1);
     mbar_fence_init();
   }
   __syncthreads();
-  auto issue = [&](int t, int s) {
+  auto issue = [&](int t) {
     if (t >= ntiles) return;
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
-    mbar_expect_tx(&bar[s], G::kTileBytes);
-    tma_load_2d(tiles + s * G::kTileE, &tmap, tx * G::kRowE, ty * G::kRows, &bar[s]);
+    mbar_expect_tx(&bar, G::kTileBytes);
+    tma_load_2d(tile, &maps.in, tx * G::kRowE, ty * G::kRows, &bar);
   };
-  if (tid == 0) {
-    issue(blockIdx.x, 0);
-    issue(blockIdx.x + gridDim.x, 1);
-  }
+  if (tid == 0) issue(blockIdx.x);
   const int c = tid % 3, blk = tid / 3;
   const int ly = blk / G::TX, lx = blk - ly * G::TX;
   bool bad = false;
   int it = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int s = it & 1;
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
     const int I = ty * G::TY + ly, J = tx * G::TX + lx;
-    mbar_wait(&bar[s], (it >> 1) & 1);
-    const T* tile = tiles + s * G::kTileE;
-    if (I < (int)g.h[NL] && J < (int)g.w[NL]) {
-      T p[S0][S0];
-      if (I * S0 + S0 <= H0 && J * S0 + S0 <= W0) {
-        const T* q = tile + (ly * S0) * G::kRowE + lx * S0 * 3 + c;
+    mbar_wait(&bar, it & 1);
+    T p[S0][S0];
+    if (I * S0 + S0 <= H0 && J * S0 + S0 <= W0) {
+      const T* q = tile + (ly * S0) * G::kRowE + lx * S0 * 3 + c;
 #pragma unroll
-        for (int r = 0; r < S0; ++r)
+      for (int r = 0; r < S0; ++r)
 #pragma unroll
-          for (int u = 0; u < S0; ++u) p[r][u] = q[r * G::kRowE + 3 * u];
-      } else {
-        const int r0 = ty * G::kRows, c0 = tx * G::TX * S0;
+        for (int u = 0; u < S0; ++u) p[r][u] = q[r * G::kRowE + 3 * u];
+    } else {
+      // clamped (edge) samples; blocks entirely past the plane read in-tile
+      // garbage that only lands in clipped parts of the output boxes
+      const int r0 = ty * G::kRows, c0 = tx * G::TX * S0;
 #pragma unroll
-        for (int r = 0; r < S0; ++r) {
-          const int row = min(I * S0 + r, H0 - 1) - r0;
+      for (int r = 0; r < S0; ++r) {
+        const int row = max(min(I * S0 + r, H0 - 1) - r0, 0);
 #pragma unroll
-          for (int u = 0; u < S0; ++u) p[r][u] = tile[row * G::kRowE + (min(J * S0 + u, W0 - 1) - c0) * 3 + c];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < NL; ++k) {
-        const int Sk = S0 >> k;
-        const int Sn = Sk >> 1;
-        const int br = I * Sk, bc = J * Sk;  // global position of p[0][0] at level k
-        const int hk = (int)g.h[k], wk = (int)g.w[k];
-        const int hn = (int)g.h[k + 1], wn = (int)g.w[k + 1];
-        T* const o0 = out + g.off[k + 1][0];
-        T* const o1 = out + g.off[k + 1][1];
-        T* const o2 = out + g.off[k + 1][2];
-        T* const o3 = out + g.off[k + 1][3];
-#pragma unroll
-        for (int i = 0; i < Sn; ++i) {
-#pragma unroll
-          for (int j = 0; j < Sn; ++j) {
-            const bool rowok = br + 2 * i + 1 < hk;
-            const bool colok = bc + 2 * j + 1 < wk;
-            const T a = p[2 * i][2 * j];
-            const T b = colok ? p[2 * i][2 * j + 1] : a;
-            const T cc = rowok ? p[2 * i + 1][2 * j] : a;
-            const T d = rowok ? (colok ? p[2 * i + 1][2 * j + 1] : cc) : b;
-            const T lp = T(0.5) * (((a + b) + cc) + d);
-            const T dh = T(0.5) * (((a + b) - cc) - d);
-            const T dv = T(0.5) * (((a - b) - cc) + d);
-            const T dd = T(0.5) * (((a - b) + cc) - d);
-            // level 1 sees every sample: its low-pass is finite iff its four inputs
-            // are (an overflowing fp32 sum is re-checked sample by sample)
-            if (k == 0 && !isfinite(lp)) bad |= !(isfinite(a) && isfinite(b) && isfinite(cc) && isfinite(d));
-            const int gi = (br >> 1) + i, gj = (bc >> 1) + j;
-            if (gi < hn && gj < wn) {
-              const int e = (gi * wn + gj) * 3 + c;
-              o0[e] = lp;
-              o1[e] = dh;
-              o2[e] = dv;
-              o3[e] = dd;
-            }
-            p[i][j] = lp;
-          }
-        }
+        for (int u = 0; u < S0; ++u) p[r][u] = tile[row * G::kRowE + max(min(J * S0 + u, W0 - 1) - c0, 0) * 3 + c];
       }
     }
-    __syncthreads();
+    if (tid == 0) tma_store_wait_read0();  // the previous tile's stores have read the staging tiles
+    __syncthreads();                        // input buffer consumed, staging buffer free
     if (tid == 0) {
       fence_proxy_async();
-      issue(t + 2 * gridDim.x, s);
+      issue(t + gridDim.x);
+    }
+    const bool valid = I < (int)g.h[NL] && J < (int)g.w[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+      const int Sk = S0 >> k;
+      const int Sn = Sk >> 1;
+      const int br = I * Sk, bc = J * Sk;  // global position of p[0][0] at level k
+      const int hk = (int)g.h[k], wk = (int)g.w[k];
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int orow = G::kRowE >> (k + 1);  // elements per staging row at level k+1
+      T* const s0 = stage + G::out_offset(k + 1, 0) + (ly * Sn) * orow + lx * Sn * 3 + c;
+      const int pl = G::out_elems(k + 1);
+#pragma unroll
+      for (int i = 0; i < Sn; ++i) {
+#pragma unroll
+        for (int j = 0; j < Sn; ++j) {
+          const bool rowok = br + 2 * i + 1 < hk;
+          const bool colok = bc + 2 * j + 1 < wk;
+          const T a = p[2 * i][2 * j];
+          const T b = colok ? p[2 * i][2 * j + 1] : a;
+          const T cc = rowok ? p[2 * i + 1][2 * j] : a;
+          const T d = rowok ? (colok ? p[2 * i + 1][2 * j + 1] : cc) : b;
+          const T lp = T(0.5) * (((a + b) + cc) + d);
+          const T dh = T(0.5) * (((a + b) - cc) - d);
+          const T dv = T(0.5) * (((a - b) - cc) + d);
+          const T dd = T(0.5) * (((a - b) + cc) - d);
+          // level 1 sees every sample: its low-pass is finite iff its four inputs
+          // are (an overflowing sum is re-checked sample by sample)
+          if (k == 0 && valid && !isfinite(lp)) bad |= !(isfinite(a) && isfinite(b) && isfinite(cc) && isfinite(d));
+          T* o = s0 + i * orow + 3 * j;
+          o[0] = lp;
+          o[pl] = dh;
+          o[2 * pl] = dv;
+          o[3 * pl] = dd;
+          p[i][j] = lp;
+        }
+      }
+    }
+    fence_proxy_async();  // staging writes -> visible to the TMA stores
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int k = 1; k <= NL; ++k)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tma_store_2d(&maps.out[k - 1][q], stage + G::out_offset(k, q), (tx * G::kRowE) >> k, (ty * G::kRows) >> k);
+      tma_store_commit();
     }
   }
+  if (tid == 0) tma_store_wait_all();
   if (flags && __syncthreads_or(bad) && tid == 0) atomicOr(flags, OXM_FLAG_NONFINITE);
 }
 
@@ -259,18 +282,23 @@ inline bool haar_tma_enabled() {
   return on;
 }
 
-// launches the TMA pass when the plane allows it (3 channels, 16-byte aligned
-// rows, 32-bit in-plane indices); false = not launched
+// launches the TMA pass when the planes allow it (3 channels, 16-byte aligned
+// rows and plane bases, 32-bit in-plane indices); false = not launched
 template <typename T, int NL>
 bool launch_fwd_tma(const T* src, const FwdGeom& g, T* out, uint32_t* flags, cudaStream_t stream) {
   using G = FwdTma<T, NL>;
   if (!haar_tma_enabled() || g.C != 3) return false;
-  if (g.h[0] * g.w[0] * 3 >= ((int64_t)1 << 31) || g.off[NL][3] + g.h[NL] * g.w[NL] * 3 >= ((int64_t)1 << 31))
+  if (g.h[0] * g.w[0] * 3 >= ((int64_t)1 << 31)) return false;
+  FwdMaps maps;
+  const bool f64 = sizeof(T) == 8;
+  if (!make_tmap_2d(&maps.in, src, f64, (uint64_t)(3 * g.w[0]), (uint64_t)g.h[0], (uint64_t)(3 * g.w[0] * sizeof(T)),
+                    G::kRowE, G::kRows))
     return false;
-  CUtensorMap map;
-  if (!make_tmap_2d(&map, src, sizeof(T) == 8, (uint64_t)(3 * g.w[0]), (uint64_t)g.h[0],
-                    (uint64_t)(3 * g.w[0] * sizeof(T)), G::kRowE, G::kRows))
-    return false;
+  for (int k = 1; k <= NL; ++k)
+    for (int q = 0; q < 4; ++q)
+      if (!make_tmap_2d(&maps.out[k - 1][q], out + g.off[k][q], f64, (uint64_t)(3 * g.w[k]), (uint64_t)g.h[k],
+                        (uint64_t)(3 * g.w[k] * sizeof(T)), G::kRowE >> k, G::kRows >> k))
+        return false;
   auto kern = haar_fwd_tma_kernel<T, NL>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -283,7 +311,7 @@ bool launch_fwd_tma(const T* src, const FwdGeom& g, T* out, uint32_t* flags, cud
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::kThreads, G::kSmem) != cudaSuccess || per_sm < 1)
     return false;
   const int64_t grid = std::min<int64_t>((int64_t)tiles_x * tiles_y, (int64_t)device_sms() * per_sm);
-  kern<<<(unsigned)grid, G::kThreads, G::kSmem, stream>>>(map, g, out, flags, tiles_x, tiles_y);
+  kern<<<(unsigned)grid, G::kThreads, G::kSmem, stream>>>(maps, g, flags, tiles_x, tiles_y);
   return true;
 }
 

@@ -204,50 +204,38 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------
-// TMA-staged low-pass kernel (fp32 frames, one pass of n <= 3 levels): the
+// TMA-staged low-pass kernel (fp32 frames, one pass of n <= 2 levels): the
 // same outputs as ll_kernel<PlainSrc<float>, NLV, true>, bit for bit.
 //
 // The batch is viewed as one 2D plane of B*H rows x 3W floats.  A CTA owns a
 // tile of TY x TX low-pass blocks (TY 2^n rows x TX 2^n pixels), staged into
-// shared memory by one cp.async.bulk.tensor per tile, double-buffered: while
-// the CTA reduces tile i, the TMA unit streams tile i + 1 (persistent grid,
-// tiles strided by gridDim).  Each thread then owns one low-pass coefficient:
-// interior blocks read their rows as conflict-free vector loads with
-// compile-time offsets; edge blocks (a tile hanging over the frame) take the
-// reference's per-level edge replication through clamped coordinates, which
-// always stay inside the tile.  Rows of a tile that belong to the next frame
-// (or lie past the batch, zero-filled) are never read.  A sample is
-// non-finite iff the fp64 low-pass sum over the block is (fp32 inputs cannot
-// overflow fp64), so the flag test is 3 compares per coefficient.
+// shared memory by one cp.async.bulk.tensor per tile.  Each thread owns one
+// low-pass coefficient: it reduces its block to the three fp64 low-pass
+// values straight out of shared memory -- interior blocks as conflict-free
+// vector loads with compile-time offsets, edge blocks (a tile hanging over
+// the frame) through clamped coordinates that reproduce the reference's
+// per-level edge replication and always stay inside the tile -- and then the
+// tile buffer is released: the elected thread issues the TMA for the CTA's
+// next tile (persistent grid, tiles strided by gridDim) while the warps run
+// the fp64 start fit (26 table logs per coefficient) and the stores.  One
+// buffer per CTA keeps 8 CTAs resident per SM for that fp64 phase.  Rows of
+// a tile that belong to the next frame (or lie past the batch, zero-filled)
+// are never read.  A sample is non-finite iff the fp64 low-pass sum over its
+// block is (fp32 inputs cannot overflow fp64): 3 compares per coefficient.
 template <int NLV>
 struct LlTma {
+  static_assert(NLV == 1 || NLV == 2, "3-level passes keep the per-thread-load ll_kernel (64 samples x 3 channels "
+                                      "per thread do not fit a TMA tile pipeline's register budget)");
   static constexpr int S = 1 << NLV;
-  static constexpr int kThreads = NLV == 3 ? 64 : 128;   // coefficients (threads) per tile
-  static constexpr int TX = NLV == 1 ? 32 : (NLV == 2 ? 16 : 8);
+  static constexpr int kThreads = 128;   // coefficients (threads) per tile
+  static constexpr int TX = NLV == 1 ? 32 : 16;
   static constexpr int TY = kThreads / TX;
   static constexpr int kRowF = TX * S * 3;                // floats per tile row (box inner dim, 192)
   static constexpr int kRows = TY * S;
   static constexpr int kTileF = kRowF * kRows;
   static constexpr uint32_t kTileBytes = kTileF * 4;
-  static constexpr size_t kSmem = 2 * (size_t)kTileBytes;
-};
-
-// level-K low-pass of an interior block whose origin sample (row 0, col 0,
-// channel c) is p: every offset a compile-time constant
-template <int K, int ROWF>
-struct LpInterior {
-  __device__ __forceinline__ static double at(const float* p) {
-    constexpr int h = 1 << (K - 1);
-    const double a = LpInterior<K - 1, ROWF>::at(p);
-    const double b = LpInterior<K - 1, ROWF>::at(p + 3 * h);
-    const double c = LpInterior<K - 1, ROWF>::at(p + ROWF * h);
-    const double d = LpInterior<K - 1, ROWF>::at(p + ROWF * h + 3 * h);
-    return 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b), c), d);
-  }
-};
-template <int ROWF>
-struct LpInterior<0, ROWF> {
-  __device__ __forceinline__ static double at(const float* p) { return (double)*p; }
+  static constexpr size_t kSmem = (size_t)kTileBytes;
+  static constexpr int kMinBlocks = NLV == 1 ? 12 : 8;
 };
 
 // level-K low-pass at level-K position (i, j) with the reference's per-level
@@ -272,48 +260,43 @@ struct LpTile<0, ROWF> {
 };
 
 template <int NLV>
-__global__ void __launch_bounds__(LlTma<NLV>::kThreads) ll_tma_kernel(
+__global__ void __launch_bounds__(LlTma<NLV>::kThreads, LlTma<NLV>::kMinBlocks) ll_tma_kernel(
     const __grid_constant__ DevOps ops, const __grid_constant__ CUtensorMap tmap, int64_t batch, LevelDims d,
     double* __restrict__ ybar, int64_t nll, uint32_t* flags, double* __restrict__ xinit,
     uint8_t* __restrict__ blkflag, int tiles_x, int tiles_y) {
   using G = LlTma<NLV>;
-  extern __shared__ __align__(128) float tiles[];
-  __shared__ __align__(8) uint64_t bar[2];
+  extern __shared__ __align__(128) float tile[];
+  __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x;
   const int64_t per_frame = (int64_t)tiles_x * tiles_y;
   const int64_t ntiles = batch * per_frame;
   const int H0 = (int)d.h[0], W0 = (int)d.w[0], hL = (int)d.h[NLV], wL = (int)d.w[NLV];
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    mbar_init(&bar, 1);
     mbar_fence_init();
   }
   __syncthreads();
-  auto issue = [&](int64_t t, int s) {
+  auto issue = [&](int64_t t) {
     if (t >= ntiles) return;
     const int64_t f = t / per_frame;
     const int r = (int)(t - f * per_frame);
     const int ty = r / tiles_x, tx = r - ty * tiles_x;
-    mbar_expect_tx(&bar[s], G::kTileBytes);
-    tma_load_2d(tiles + s * G::kTileF, &tmap, tx * G::kRowF, (int)(f * H0) + ty * G::kRows, &bar[s]);
+    mbar_expect_tx(&bar, G::kTileBytes);
+    tma_load_2d(tile, &tmap, tx * G::kRowF, (int)(f * H0) + ty * G::kRows, &bar);
   };
-  if (tid == 0) {
-    issue(blockIdx.x, 0);
-    issue(blockIdx.x + gridDim.x, 1);
-  }
+  if (tid == 0) issue(blockIdx.x);
   const int ly = tid / G::TX, lx = tid - ly * G::TX;
   const double inv = ldexp(1.0, -NLV);  // exact
   int it = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-    const int s = it & 1;
     const int64_t f = t / per_frame;
     const int r = (int)(t - f * per_frame);
     const int ty = r / tiles_x, tx = r - ty * tiles_x;
     const int by = ty * G::TY + ly, bx = tx * G::TX + lx;
-    mbar_wait(&bar[s], (it >> 1) & 1);
-    const float* tile = tiles + s * G::kTileF;
-    if (by < hL && bx < wL) {
-      double ll[3];
+    const bool mine = by < hL && bx < wL;
+    mbar_wait(&bar, it & 1);
+    double ll[3] = {0.0, 0.0, 0.0};
+    if (mine) {
       const int py = by * G::S, px = bx * G::S;
       if (py + G::S <= H0 && px + G::S <= W0) {
         const float* p = tile + ly * G::S * G::kRowF + lx * G::S * 3;
@@ -356,15 +339,19 @@ __global__ void __launch_bounds__(LlTma<NLV>::kThreads) ll_tma_kernel(
           for (int c = 0; c < 3; ++c)
             ll[c] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn((double)v[0][c], (double)v[0][3 + c]), (double)v[1][c]),
                                     (double)v[1][3 + c]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < 3; ++c) ll[c] = LpInterior<NLV, G::kRowF>::at(p + c);
         }
       } else {
         const int r0 = ty * G::kRows, c0 = tx * G::TX * G::S;
 #pragma unroll
         for (int c = 0; c < 3; ++c) ll[c] = LpTile<NLV, G::kRowF>::at(tile, r0, c0, d, by, bx, c);
       }
+    }
+    __syncthreads();  // every thread has its block in registers: the buffer is free
+    if (tid == 0) {
+      fence_proxy_async();
+      issue(t + gridDim.x);
+    }
+    if (mine) {
       const int64_t idx = (f * hL + by) * wL + bx;
       bool bad = false, neg = false;
 #pragma unroll
@@ -386,11 +373,6 @@ __global__ void __launch_bounds__(LlTma<NLV>::kThreads) ll_tma_kernel(
         xinit[nll + idx] = x1;
         xinit[2 * nll + idx] = x2;
       }
-    }
-    __syncthreads();  // every thread is done with stage s
-    if (tid == 0) {
-      fence_proxy_async();
-      issue(t + 2 * (int64_t)gridDim.x, s);
     }
   }
 }
@@ -441,7 +423,6 @@ bool launch_ll_tma(const DevOps& ops, const float* frames, int64_t batch, const 
   switch (d.n) {
     case 1: return launch_ll_tma_n<1>(ops, frames, batch, d, ybar, nll, flags, xinit, blkflag, s);
     case 2: return launch_ll_tma_n<2>(ops, frames, batch, d, ybar, nll, flags, xinit, blkflag, s);
-    case 3: return launch_ll_tma_n<3>(ops, frames, batch, d, ybar, nll, flags, xinit, blkflag, s);
     default: return false;
   }
 }
@@ -627,26 +608,36 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
       any_fb |= !(vmin[r][0] >= thr) || (two && !(vmin[r][1] >= thr));
     }
   }
-  // cancellation guard: queue pixels for the fp64 fixup kernel (rare)
-  const unsigned active = __activemask();
+  // cancellation guard: queue pixels for the fp64 fixup kernel (rare).  One
+  // atomic per warp; each thread's pixels land contiguously in lane order, so
+  // the pixels of one low-pass block (adjacent lanes) are adjacent in the list
+  // and the fixup kernels' warps share its spectrum / ybar rows through L1
+  // instead of re-reading them from DRAM per pixel.
+  const unsigned active = __activemask();  // a prefix of the warp (threads past the right edge returned)
   if (__any_sync(active, any_fb)) {
     const int lane = threadIdx.x & 31;
+    unsigned mask = 0;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const bool need = r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr);
-        const unsigned m = __ballot_sync(active, need);
-        if (m) {
-          const int leader = __ffs(m) - 1;
-          uint32_t base = 0;
-          if (lane == leader) base = atomicAdd(fb_count, (uint32_t)__popc(m));
-          base = __shfl_sync(active, base, leader);
-          if (need)
-            fb_list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((f * g.H + row0 + r) * g.W + col + c);
-        }
-      }
+      for (int c = 0; c < 2; ++c)
+        if (r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr)) mask |= 1u << (2 * r + c);
+    const unsigned cnt = __popc(mask);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(active, incl, o);
+      if (lane >= o) incl += v;
     }
+    const unsigned total = __shfl_sync(active, incl, 31 - __clz(active));
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(fb_count, total);
+    uint32_t pos = __shfl_sync(active, base, 0) + incl - cnt;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        if (mask & (1u << (2 * r + c))) fb_list[pos++] = (uint32_t)((f * g.H + row0 + r) * g.W + col + c);
   }
 }
 
