@@ -227,8 +227,6 @@ __global__ void __launch_bounds__(FwdTma<T, NL>::kThreads) haar_fwd_tma_kernel(c
       const int Sn = Sk >> 1;
       const int br = I * Sk, bc = J * Sk;  // global position of p[0][0] at level k
       const int hk = (int)g.h[k], wk = (int)g.w[k];
-      constexpr int dummy = 0;
-      (void)dummy;
       const int orow = G::kRowE >> (k + 1);  // elements per staging row at level k+1
       T* const s0 = stage + G::out_offset(k + 1, 0) + (ly * Sn) * orow + lx * Sn * 3 + c;
       const int pl = G::out_elems(k + 1);

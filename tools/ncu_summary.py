@@ -12,7 +12,8 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active',
         'sm__warps_active.avg.pct_of_peak_sustained_active', 'smsp__issue_active.avg.pct_of_peak_sustained_active',
         'smsp__thread_inst_executed_per_inst_executed.ratio', 'smsp__inst_executed.sum',
-        'launch__registers_per_thread', 'launch__grid_size', 'dram__throughput.avg.pct_of_peak_sustained_elapsed']
+        'launch__registers_per_thread', 'launch__grid_size', 'dram__throughput.avg.pct_of_peak_sustained_elapsed',
+        'smsp__inst_executed_pipe_fp64.sum', 'sm__inst_executed_pipe_fp64.sum', 'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum']
 
 
 def main():
