@@ -642,18 +642,19 @@ def run_ours(args):
                "peak_source": "fp64 DFMA probe (oxm_probe_fp64_fma) in this run: one DFMA per lane per pipe slot",
                "kernels": "em_persistent_kernel (fp64 tail)",
                "work": f"{emc['tail_fits']} fp64 fits (incl. {emc['restarts']} exact-mode restarts) x "
-                       f"{FP64_INST_PER_FIT} fp64-pipe instructions per fit (DFMA/DADD/DMUL/DSETP, counted in the "
-                       f"SASS of the fit step: tools/sass_stats.py --em-fit)",
+                       f"{FP64_INST_PER_FIT} fp64-pipe thread instructions per fit (DFMA/DADD/DMUL/DSETP; ncu "
+                       f"SASS counts of this batch's tail launch / its fits, profiles/r02_em_tail_sass_counts.txt)",
                "flops": {"achieved": emc["tail_fits"] * FLOPS_PER_FIT / stage_s[2] / 1e12,
                          "peak": 2 * fp64_rate / 1e12, "unit": "TFLOP/s",
-                         "per_fit": FLOPS_PER_FIT, "note": "FMA = 2 flops, DADD/DMUL = 1, compares 0"}},
+                         "per_fit": FLOPS_PER_FIT, "note": "FMA = 2 flops, DADD/DMUL = 1, compares 0 (same counts)"}},
         "px_f32_kernel": {"bound": "xu", "achieved": px_lg2 / stage_s[3] / 1e12, "peak": peaks["mufu_lg2"] / 1e12,
                           "unit": "Tlg2/s", "peak_source": "MUFU lg2 probe (oxm_probe_mufu_lg2) in this run",
                           "kernels": "px_f32_kernel", "work": f"{px} px x 26 lg2"},
         "fixup": {"bound": "latency", "achieved": None, "peak": None, "unit": None,
-                  "kernels": "px_fallback_kernel (classify) + em_exact_kernel + px_fallback_kernel (deferred)",
-                  "note": f"fp64 recompute of {emc['queued_px']} queued pixels; all-fp64 EM of "
-                          f"{emc['exact_blocks']} blocks"},
+                  "kernels": "exact pass (em_persistent_kernel on the block list) + px_fallback_kernel (deferred)",
+                  "note": f"all-fp64 EM of {emc['exact_blocks']} blocks, then fp64 recompute of "
+                          f"{emc['deferred_px']} deferred pixels (of {emc['queued_px']} fallback pixels; "
+                          f"the rest are finished in place by px_f32_kernel)"},
     }
     for k, r in rooflines.items():
         r["ms"] = stage_t[k] * 1e3
@@ -699,19 +700,24 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-# EM tail work per fp64 fit, from the code's actual arithmetic:
-# per band 11 fp64-pipe instructions in phase A (exp argument 2 DFMA; exp:
-# DADD + 3 DFMA + DMUL + DFMA; C e 3 DFMA) and 15 in phase B (e + G r 3 DFMA,
-# eps clamp DSETP, log: DFMA + 3 DFMA + DMUL + 2 DFMA + DADD, fit 3 DFMA), x 26
-# bands, + 20 per step (residual, step / norm test).  Flops count FMA = 2.
-FP64_INST_PER_FIT = 26 * 26 + 20
-FLOPS_PER_FIT = 46 * 26 + 16
+# EM tail work per fp64 fit, measured rather than assumed: ncu's
+# SASS-level thread-instruction counts of the tail launch of this exact bench
+# batch (64 frames, profiles/r02_em_tail_sass_counts.txt) divided by its
+# 30,287,354 fits -- DFMA 581.8 + DADD 66.5 + DMUL 63.2 + DSETP 37.6 = 749.1
+# fp64-pipe instructions per fit, 1293 flops (FMA = 2).  Per band that is the
+# exp (DADD + 3 DFMA + DMUL + DFMA), its argument (2 DFMA), C e (3 DFMA),
+# e + G r (3 DFMA), the eps clamp (DSETP), the table log (DFMA + 3 DFMA + DMUL
+# + 2 DFMA + DADD) and the fit (3 DFMA), plus per-step norms and the write-out's
+# re-formed spectra.  `frac` = fp64-pipe instructions issued / the DFMA probe's
+# rate, the quantity ncu reports as sm__inst_executed_pipe_fp64.
+FP64_INST_PER_FIT = 749.1
+FLOPS_PER_FIT = 1293.2
 MUFU_PER_LEAD_FIT = 2 * 26  # fp32 lead-in: one ex2 and one lg2 per band
 CPU_OTHER_FRAMES = 3   # frames for the slower reference thread setting (threads=1, BLAS=nproc)
 DROPIN_SEQ_FRAMES = 6
-# kernels launched per step: zero_counters, ll (+ fit #1), em_lead, em_persistent (tail), px,
-# px_fallback (classify), em_exact, px_fallback (deferred)
-HybridMapLaunches = 8
+# kernels launched per step: zero_counters, ll_tma (+ fit #1), em_lead, em_persistent (tail),
+# px_f32 (+ in-warp fp64 fallback), exact pass, px_fallback (deferred)
+HybridMapLaunches = 7
 
 
 def spawn_ranks(args) -> int:

@@ -181,8 +181,8 @@ OXM_API int oxm_expected_spectrum_f64(const oxm_ctx* ctx, const double* x, int64
  * Outputs are planar (batch, H, W); fits is (batch, ceil(H/2^n), ceil(W/2^n)).
  * stage_events: NULL, or 6 cudaEvent_t recorded on `stream` before the
  * low-pass kernel, before the EM's fp32 lead-in, before its fp64 kernel,
- * before the per-pixel kernel, before the fp64 pixel fixup (fallback
- * classification, exact-block EM, deferred pixels) and after it (live
+ * before the per-pixel kernel (which also finishes most fp64-fallback pixels
+ * in place), before the fixup (exact-block EM, deferred pixels) and after it (live
  * per-kernel timing for the roofline report; with no lead-in, events 1 and 2
  * coincide). */
 OXM_API size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, int64_t height,
@@ -190,8 +190,9 @@ OXM_API size_t oxm_hybrid_workspace_bytes(const oxm_ctx* ctx, int64_t batch, int
 /* EM work counters of the last fp32-map launch that used `workspace` (same
  * geometry): out[0] fp32 fits of the lead-in, out[1] fp64 fits of the tail,
  * out[2] tail restarts in exact mode, out[3] low-pass blocks re-estimated
- * all-fp64 for the fp64 pixel fallback, out[4] pixels queued for the fp64
- * fallback (`out` holds 5 values).  Synchronises `stream`. */
+ * all-fp64 for the fp64 pixel fallback, out[4] pixels that took the fp64
+ * fallback, out[5] of those, the ones deferred to after the exact pass
+ * (`out` holds 6 values).  Synchronises `stream`. */
 OXM_API int oxm_hybrid_em_counters(const oxm_ctx* ctx, void* workspace, int64_t batch, int64_t height,
                                    int64_t width, int n_levels, uint64_t* out, void* stream);
 OXM_API int oxm_hybrid_maps_f32(const oxm_ctx* ctx, const float* frames, int64_t batch, int64_t height,

@@ -19,14 +19,13 @@
 //   4. px kernel      one thread per (2 columns, R rows of a block): rebuild
 //                     the 26-band spectrum in registers, MUFU lg2, 3x26 fit,
 //                     THb/SO2; pixels whose smallest band < fallback_below
-//                     are appended (warp-aggregated) to a list
-//   5. px_fallback_kernel<kFbClassify>  fp64 recompute of the queued pixels
-//                     (cancellation guard; ~0.4 % of textured pixels), except
-//                     the "sensitive" ones, whose blocks go to
-//   6. em_exact_kernel all-fp64 EM of those blocks (~1 % of them), then
-//   7. px_fallback_kernel<kFbDeferred>  the deferred pixels.
-// With the all-fp64 EM schedule (oxm_ctx_set_em_lead ratio <= 1) 2, 5-7
-// become one all-fp64 persistent EM and one fallback pass.  The fp64 variant
+//                     (cancellation guard, ~0.4 % of textured pixels) are
+//                     recomputed in fp64 by their warp right away, except the
+//                     "sensitive" ones, which are listed with their blocks for
+//   5. em exact pass  all-fp64 EM of those blocks (~1 % of them), then
+//   6. px_fallback_kernel  the deferred pixels.
+// With the all-fp64 EM schedule (oxm_ctx_set_em_lead ratio <= 1) 2 and 5-6
+// go: one all-fp64 persistent EM, every fallback pixel finished in 4.  The fp64 variant
 // (drop-in API): everything fp64, optional (H, W, L) cube, no fallback.
 // Neither the directional planes nor the 26-channel cube touch HBM on the
 // fp32 path: HBM traffic is the frame read twice, the per-block spectra
@@ -450,6 +449,18 @@ __device__ __forceinline__ void pixel_fit_f64(const DevOps& ops, SpecLoad spec, 
   x2 = -a2;
 }
 
+// Where the per-pixel kernel sends the pixels it does not finish itself
+// (the fp64 fallback's "sensitive" ones, see px_f32_kernel's tail).
+struct FbOut {
+  uint32_t* count;      // deferred pixels listed (fb list)
+  uint32_t* list;
+  uint8_t* blkflag;     // [nll] block marked for the exact pass
+  uint32_t* blk_list;   // marked blocks
+  uint32_t* blk_count;
+  uint32_t* queued;     // every pixel that took the fp64 fallback (statistics)
+  int classify;         // 1: EM precision schedule active (hi parts only, defer sensitive pixels)
+};
+
 struct PxGeom {
   int64_t H, W, hL, wL, nll;
   int n;
@@ -474,20 +485,23 @@ template <int KL, int R, bool PLANES, typename Src>
 #endif
 __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(const __grid_constant__ DevOps ops,
                                                             const Src frames, PxGeom g,
-                                                            const float* __restrict__ Shi, int Lp,
-                                                            const double* __restrict__ ybar, float* __restrict__ thb,
-                                                            float* __restrict__ so2, float* __restrict__ hbo,
-                                                            float* __restrict__ hb, float* __restrict__ off,
-                                                            uint32_t* __restrict__ fb_count, uint32_t* __restrict__ fb_list) {
+                                                            const float* __restrict__ Shi, const float* __restrict__ Slo,
+                                                            int Lp, const double* __restrict__ ybar,
+                                                            float* __restrict__ thb, float* __restrict__ so2,
+                                                            float* __restrict__ hbo, float* __restrict__ hb,
+                                                            float* __restrict__ off, FbOut fb) {
   constexpr int LM = BandCount<KL>::kMax;
   const int L = BandCount<KL>::get(ops);
   const int64_t f = blockIdx.z;
-  const int64_t col = 2 * ((int64_t)blockIdx.x * kPxThreads + threadIdx.x);  // first of the two columns
   const int bs = 1 << g.n;               // rows per low-pass block
   const int cpb = bs > R ? bs / R : 1;   // row chunks per block row (a power of two)
   const int64_t by = blockIdx.y >> (__ffs(cpb) - 1);
   const int64_t row0 = by * bs + (int64_t)(blockIdx.y & (cpb - 1)) * R;
-  if (col >= g.W) return;
+  // threads past the right edge stay (on the last even column, storing
+  // nothing) so that every warp is full for the cooperative fallback below
+  const int64_t col_raw = 2 * ((int64_t)blockIdx.x * kPxThreads + threadIdx.x);  // first of the two columns
+  const bool live = col_raw < g.W;
+  const int64_t col = live ? col_raw : ((g.W - 1) & ~int64_t(1));
   const bool two = col + 1 < g.W;
   const int nrow = (int)min64(min64(R, g.H - row0), (int64_t)bs);
   const int64_t bidx = (f * g.hL + by) * g.wL + (col >> g.n);
@@ -573,7 +587,7 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + r) * g.W + col;
-    if (r < nrow) {
+    if (live && r < nrow) {
       const float2 xo = make_float2(a0[r].x * cal, a0[r].y * cal), xd = make_float2(a1[r].x * cal, a1[r].y * cal);
       const float2 co = make_float2(fmaxf(xo.x, 0.f), fmaxf(xo.y, 0.f));
       const float2 t = make_float2(co.x + fmaxf(xd.x, 0.f), co.y + fmaxf(xd.y, 0.f));
@@ -608,94 +622,146 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
       any_fb |= !(vmin[r][0] >= thr) || (two && !(vmin[r][1] >= thr));
     }
   }
-  // cancellation guard: queue pixels for the fp64 fixup kernel (rare).  One
-  // atomic per warp; each thread's pixels land contiguously in lane order, so
-  // the pixels of one low-pass block (adjacent lanes) are adjacent in the list
-  // and the fixup kernels' warps share its spectrum / ybar rows through L1
-  // instead of re-reading them from DRAM per pixel.
-  const unsigned active = __activemask();  // a prefix of the warp (threads past the right edge returned)
-  if (__any_sync(active, any_fb)) {
+  // Cancellation guard (rare: ~0.4% of textured pixels, clustered): pixels
+  // with a band below fallback_below are recomputed in fp64 right here, by the
+  // whole warp -- lane l takes band l (its block spectrum, the reference's eps
+  // clamp, a table log), and the three fit sums are reduced with xor shuffles
+  // (every lane ends with the same bits).  The pixel's rgb, ybar and spectrum
+  // rows were just read by this warp, so they come from L1, not DRAM.  With
+  // the EM precision schedule (fb.classify) a pixel with a band in
+  // [eps / 2, exact_below) is "sensitive" to the schedule's ~1e-8 spectrum
+  // deviation (see px_fallback_kernel): it is listed for the deferred pass
+  // and its block for the all-fp64 exact pass instead.  Without the schedule
+  // the spectrum is hi + lo (fp64 to 48 bits) and every queued pixel is
+  // finished here.
+  if (__any_sync(0xffffffffu, any_fb)) {
     const int lane = threadIdx.x & 31;
     unsigned mask = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < 2; ++c)
-        if (r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr)) mask |= 1u << (2 * r + c);
-    const unsigned cnt = __popc(mask);
-    unsigned incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(active, incl, o);
-      if (lane >= o) incl += v;
+        if (live && r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr)) mask |= 1u << (2 * r + c);
+    const unsigned nq = __reduce_add_sync(0xffffffffu, __popc(mask));
+    if (lane == 0 && fb.queued) atomicAdd(fb.queued, nq);
+    // this lane's band row (indexed constant-bank reads: once per warp that needs them)
+    double T0 = 0.0, T1 = 0.0, T2 = 0.0, F0 = 0.0, F1 = 0.0, F2 = 0.0;
+    if (lane < L) {
+      T0 = ops.solve[lane][0];
+      T1 = ops.solve[lane][1];
+      T2 = ops.solve[lane][2];
+      F0 = ops.fitm[0][lane];
+      F1 = ops.fitm[1][lane];
+      F2 = ops.fitm[2][lane];
     }
-    const unsigned total = __shfl_sync(active, incl, 31 - __clz(active));
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(fb_count, total);
-    uint32_t pos = __shfl_sync(active, base, 0) + incl - cnt;
+    const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below, eps = ops.eps;
+    const double2* logt = log_table_global();
+    for (;;) {
+      const unsigned m = __ballot_sync(0xffffffffu, mask != 0);
+      if (!m) break;
+      const int owner = __ffs(m) - 1;
+      int bit = 0;
+      if (lane == owner) {
+        bit = __ffs(mask) - 1;
+        mask &= mask - 1;
+      }
+      bit = __shfl_sync(0xffffffffu, bit, owner);
+      const int64_t ocol = __shfl_sync(0xffffffffu, col, owner) + (bit & 1);
+      const int64_t p = (f * g.H + row0 + (bit >> 1)) * g.W + ocol;
+      const int64_t ob = (f * g.hL + by) * g.wL + (ocol >> g.n);
+      const double D0 = frames.at(3 * p) - ybar[ob];
+      const double D1 = frames.at(3 * p + 1) - ybar[g.nll + ob];
+      const double D2 = frames.at(3 * p + 2) - ybar[2 * g.nll + ob];
+      double a0s = 0.0, a1s = 0.0, a2s = 0.0;
+      bool sens = false;
+      for (int l = lane; l < L; l += 32) {
+        double t0 = T0, t1 = T1, t2 = T2, f0 = F0, f1 = F1, f2 = F2;
+        if (l >= 32) {  // band counts above 32 (generic-L builds)
+          t0 = ops.solve[l][0];
+          t1 = ops.solve[l][1];
+          t2 = ops.solve[l][2];
+          f0 = ops.fitm[0][l];
+          f1 = ops.fitm[1][l];
+          f2 = ops.fitm[2][l];
+        }
+        double S = (double)ldg(Shi + ob * Lp + l);
+        if (!fb.classify) S += (double)ldg(Slo + ob * Lp + l);
+        const double sp = fma(t2, D2, fma(t1, D1, fma(t0, D0, S)));
+        sens |= fb.classify && sp >= lo_b && sp < hi_b;
+        const double lg = log_tab(fmax(sp, eps), logt);
+        a0s = fma(f0, lg, a0s);
+        a1s = fma(f1, lg, a1s);
+        a2s = fma(f2, lg, a2s);
+      }
+      if (__any_sync(0xffffffffu, sens)) {  // defer: the exact pass re-estimates its block all-fp64
+        if (lane == owner) {
+          fb.list[atomicAdd(fb.count, 1u)] = (uint32_t)p;
+          unsigned* word = reinterpret_cast<unsigned*>(fb.blkflag + (ob & ~int64_t(3)));
+          const unsigned bitm = 1u << (8 * (unsigned)(ob & 3));
+          if (!(atomicOr(word, bitm) & bitm)) fb.blk_list[atomicAdd(fb.blk_count, 1u)] = (uint32_t)ob;
+        }
+        continue;
+      }
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        if (mask & (1u << (2 * r + c))) fb_list[pos++] = (uint32_t)((f * g.H + row0 + r) * g.W + col + c);
+      for (int o = 16; o > 0; o >>= 1) {
+        a0s += __shfl_xor_sync(0xffffffffu, a0s, o);
+        a1s += __shfl_xor_sync(0xffffffffu, a1s, o);
+        a2s += __shfl_xor_sync(0xffffffffu, a2s, o);
+      }
+      if (lane == owner) {  // the owner also made this pixel's fp32 stores: program order
+        const float xo = (float)(-a0s * g.cal), xd = (float)(-a1s * g.cal);
+        const float co = fmaxf(xo, 0.f);
+        const float t = co + fmaxf(xd, 0.f);
+        thb[p] = t;
+        so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
+        if constexpr (PLANES) {
+          hbo[p] = xo;
+          hb[p] = xd;
+          off[p] = (float)(-a2s);
+        }
+      }
+    }
   }
 }
 
-// fp64 recompute of the queued pixels (~0.4% of them): kFbLanes (2) threads per
-// pixel, each taking every kFbLanes-th band, partial fit sums reduced with
-// two shuffles; grid-stride over the device-side count.  Each thread issues
-// its loads (rgb, ybar, its part of the hi/lo spectrum row) together and uses
-// the table log (~1 ulp; the argument is clamped at eps > 0 first, as the
-// reference does).  Operators are staged in shared memory by CTAs that have
-// work (the per-lane band index would serialise constant-bank reads).
-//
-// With the EM's fp32 lead-in (em_lead_kernel) the block spectra differ from
-// the all-fp64 ones by ~1e-8 relative, and a queued pixel amplifies that by
-// |S| / s_l through log s_l for every band s_l = S_l + solve (rgb - ybar)
-// that is small but not clamped.  Bands below eps / 2 are clamped to eps
-// either way, so a pixel is "sensitive" when some band lies in
-// [eps / 2, exact_below).  Modes:
-//   kFbAll       recompute every queued pixel (all-fp64 EM schedule);
-//   kFbClassify  recompute the insensitive ones (~85% of textured queues are
-//                clamped-only); for a sensitive one, tag its list entry
-//                (kDeferTag) and append its low-pass block (once) to the
-//                exact list that em_exact_kernel re-estimates all-fp64;
-//   kFbDeferred  recompute the tagged entries (after the exact pass).
-// Each pixel is written exactly once, from spectra that no kernel modifies
-// while it is classified: the output does not depend on scheduling.
+// fp64 recompute of the deferred pixels -- the "sensitive" fallback pixels
+// px_f32_kernel listed -- after the exact pass has re-estimated their blocks
+// all-fp64 (hi + lo spectrum parts).  With the EM's fp32 lead-in the block
+// spectra differ from the all-fp64 ones by ~1e-8 relative, and a fallback
+// pixel amplifies that by |S| / s_l through log s_l for every band
+// s_l = S_l + solve (rgb - ybar) that is small but not clamped; bands below
+// eps / 2 are clamped to eps either way, so only pixels with a band in
+// [eps / 2, exact_below) wait for the exact pass (~15% of textured fallback
+// pixels).  kFbLanes (2) threads per pixel, each taking every kFbLanes-th
+// band, partial fit sums reduced with shuffles; grid-stride over the
+// device-side count; table log (~1 ulp) after the reference's eps clamp.
+// Operators are staged in shared memory by CTAs that have work (the per-lane
+// band index would serialise constant-bank reads).  Every pixel is written
+// exactly once after the exact pass, from spectra no kernel modifies any
+// more: the output does not depend on scheduling.
 #ifndef OXM_FB_LANES
 #define OXM_FB_LANES 2
 #endif
-constexpr int kFbLanes = OXM_FB_LANES;  // threads per queued pixel (1, 2 or 4)
+constexpr int kFbLanes = OXM_FB_LANES;  // threads per deferred pixel (1, 2 or 4)
 #ifndef OXM_FB_CTAS_PER_SM
 #define OXM_FB_CTAS_PER_SM 32
 #endif
-constexpr uint32_t kDeferTag = 0x80000000u;
-enum FbMode { kFbAll, kFbClassify, kFbDeferred };
-template <int KL, typename Src, int MODE>
+template <int KL, typename Src>
 __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_constant__ DevOps ops,
                                                                  const Src frames, PxGeom g,
                                                                  const float* __restrict__ Shi,
                                                                  const float* __restrict__ Slo, int Lp,
                                                                  const double* __restrict__ ybar,
                                                                  const uint32_t* __restrict__ fb_count,
-                                                                 uint32_t* __restrict__ fb_list,
+                                                                 const uint32_t* __restrict__ fb_list,
                                                                  float* __restrict__ thb, float* __restrict__ so2,
                                                                  float* __restrict__ hbo, float* __restrict__ hb,
-                                                                 float* __restrict__ off, uint8_t* __restrict__ blkflag,
-                                                                 uint32_t* __restrict__ blk_list,
-                                                                 uint32_t* __restrict__ blk_count) {
+                                                                 float* __restrict__ off) {
   __shared__ double T[kMaxBands][3], F[3][kMaxBands];
   constexpr int kPerCta = kFbThreads / kFbLanes;
   const uint32_t cnt = *fb_count;
   if ((int64_t)blockIdx.x * kPerCta >= cnt) return;  // whole CTA idle: skip the staging
   const int64_t stride = (int64_t)gridDim.x * kPerCta;
-  if constexpr (MODE == kFbDeferred) {  // most CTAs hold no deferred entry: skip the staging too
-    bool any = false;
-    for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride)
-      any |= (fb_list[i] & kDeferTag) != 0;
-    if (!__syncthreads_or(any)) return;
-  }
   const int L = ops.L;
   for (int q = threadIdx.x; q < 3 * L; q += kFbThreads) {
     T[q / 3][q % 3] = ops.solve[q / 3][q % 3];
@@ -706,17 +772,11 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
   // pixel indices are < 2^32 (checked at launch): 32-bit index arithmetic
   const uint32_t plane = (uint32_t)(g.H * g.W), W = (uint32_t)g.W;
   const double2* logt = log_table_global();
-  // the loop bound is uniform over each group of kFbLanes lanes (shuffles below)
-  const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below;
   // group collectives use the group's own lanes: other groups of the warp may
-  // have left the loop or skipped this entry
+  // have left the loop
   const unsigned grp = ((1u << kFbLanes) - 1u) << ((threadIdx.x & 31) & ~(kFbLanes - 1));
   for (int64_t i = (int64_t)blockIdx.x * kPerCta + threadIdx.x / kFbLanes; i < cnt; i += stride) {
-    uint32_t p = fb_list[i];
-    if constexpr (MODE == kFbDeferred) {
-      if (!(p & kDeferTag)) continue;  // group-uniform
-      p &= ~kDeferTag;
-    }
+    const uint32_t p = fb_list[i];
     const uint32_t f = p / plane;
     const uint32_t rem = p - f * plane;
     const uint32_t row = rem / W, col = rem - row * W;
@@ -727,36 +787,14 @@ __global__ void __launch_bounds__(kFbThreads) px_fallback_kernel(const __grid_co
     const float* hi = Shi + bidx * Lp;
     const float* lo = Slo + bidx * Lp;
     constexpr int kPer = (BandCount<KL>::kMax + kFbLanes - 1) / kFbLanes;
-    double sp[kPer];
-    bool sens = false;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int l = sub + kFbLanes * k;
-      if (l < L) {
-        // classify: the tail stored hi parts only (insensitive pixels need no more; the
-        // sensitive ones are recomputed from the exact pass's hi + lo)
-        const double S = MODE == kFbClassify ? (double)ldg(hi + l) : (double)ldg(hi + l) + (double)ldg(lo + l);
-        sp[k] = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
-        sens |= sp[k] >= lo_b && sp[k] < hi_b;
-      }
-    }
-    if constexpr (MODE == kFbClassify) {
-      if (__ballot_sync(grp, sens)) {  // this group's pixel: defer to the exact pass
-        if (sub == 0) {
-          fb_list[i] = p | kDeferTag;
-          unsigned* word = reinterpret_cast<unsigned*>(blkflag + (bidx & ~int64_t(3)));
-          const unsigned bit = 1u << (8 * (unsigned)(bidx & 3));
-          if (!(atomicOr(word, bit) & bit)) blk_list[atomicAdd(blk_count, 1u)] = (uint32_t)bidx;
-        }
-        continue;
-      }
-    }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
       const int l = sub + kFbLanes * k;
       if (l < L) {
-        const double lg = log_tab(fmax(sp[k], ops.eps), logt);
+        const double S = (double)ldg(hi + l) + (double)ldg(lo + l);
+        const double sp = fma(T[l][2], D2, fma(T[l][1], D1, fma(T[l][0], D0, S)));
+        const double lg = log_tab(fmax(sp, ops.eps), logt);
         a0 = fma(F[0][l], lg, a0);
         a1 = fma(F[1][l], lg, a1);
         a2 = fma(F[2][l], lg, a2);
@@ -848,6 +886,7 @@ struct Workspace {
   unsigned long long* em_stats;   // [3] EM work counters (same block, EmIO::stats)
   unsigned long long* sel_work;   // chunk counter of the exact-block EM pass (same block)
   uint32_t* blk_count;            // number of exact blocks (same block)
+  uint32_t* queued;               // pixels that took the fp64 fallback (same block)
   uint8_t* blk_flag;              // [nll] block marked for the exact pass (zeroed by ll_kernel)
   uint32_t* blk_list;             // [nll] marked blocks
   uint32_t* fb_list;
@@ -891,6 +930,7 @@ Workspace carve(void* ws, int L, int64_t nll) {
   w.lead_work = reinterpret_cast<unsigned long long*>(p + 192);
   w.em_stats = reinterpret_cast<unsigned long long*>(p + 8);
   w.blk_count = reinterpret_cast<uint32_t*>(p + 4);
+  w.queued = reinterpret_cast<uint32_t*>(p + 32);
   w.sel_work = reinterpret_cast<unsigned long long*>(p + 200);
   w.fb_list = reinterpret_cast<uint32_t*>(p + 256);
   return w;
@@ -997,11 +1037,11 @@ int launch_em_soa(const DevOps& ops, const double* ybar, int64_t nll, const Work
 
 template <int KL, bool PLANES, typename Src>
 void launch_px_rows(const DevOps& ops, const Src& frames, const PxGeom& g, dim3 grid, int R, const Workspace& w,
-                    float* thb, float* so2, float* hbo, float* hb, float* off, cudaStream_t s) {
+                    float* thb, float* so2, float* hbo, float* hb, float* off, const FbOut& fb, cudaStream_t s) {
   if (R == 2)
-    px_f32_kernel<KL, 2, PLANES, Src><<<grid, kPxThreads, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list);
+    px_f32_kernel<KL, 2, PLANES, Src><<<grid, kPxThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, thb, so2, hbo, hb, off, fb);
   else
-    px_f32_kernel<KL, 4, PLANES, Src><<<grid, kPxThreads, 0, s>>>(ops, frames, g, w.Shi, w.Lp, w.ybar, thb, so2, hbo, hb, off, w.fb_count, w.fb_list);
+    px_f32_kernel<KL, 4, PLANES, Src><<<grid, kPxThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, thb, so2, hbo, hb, off, fb);
 }
 
 template <int KL, typename Src>
@@ -1020,24 +1060,16 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
   const int64_t cpb = bs > R ? bs / R : 1;
   dim3 grid((unsigned)ceil_div(g.W, 2 * kPxThreads), (unsigned)(g.hL * cpb), (unsigned)batch);
   if (g.hL * cpb > 65535 || batch > 65535) return OXM_ERR_ARGUMENT;
+  const bool classify = exact_blocks_active(ops);
+  const FbOut fb{w.fb_count, w.fb_list, w.blk_flag, w.blk_list, w.blk_count, w.queued, classify ? 1 : 0};
   if (planes)
-    launch_px_rows<KL, true>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
+    launch_px_rows<KL, true>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, fb, s);
   else
-    launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, s);
+    launch_px_rows<KL, false>(ops, frames, g, grid, R, w, thb, so2, hbo, hb, off, fb, s);
   int st = check_launch("hybrid_px_f32");
   if (st) return st;
   if (fixup_ev) cudaEventRecord(fixup_ev, s);
-  const unsigned fb_grid = (unsigned)device_sms() * OXM_FB_CTAS_PER_SM;
-  if (!exact_blocks_active(ops)) {
-    px_fallback_kernel<KL, Src, kFbAll><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
-                                                                  w.fb_list, thb, so2, hbo, hb, off, nullptr, nullptr,
-                                                                  nullptr);
-    return check_launch("hybrid_fallback");
-  }
-  px_fallback_kernel<KL, Src, kFbClassify><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar,
-                                                                     w.fb_count, w.fb_list, thb, so2, hbo, hb, off,
-                                                                     w.blk_flag, w.blk_list, w.blk_count);
-  if ((st = check_launch("hybrid_fallback_classify"))) return st;
+  if (!classify) return OXM_OK;  // every fallback pixel was finished by px_f32_kernel
   EmIO io{};
   io.y = w.ybar;
   io.y_soa = 1;
@@ -1052,9 +1084,9 @@ int launch_px_f32(const DevOps& ops, const Src& frames, const PxGeom& g, int64_t
   io.sel = w.blk_list;
   io.sel_count = w.blk_count;
   if ((st = launch_em_selected<26, SpecOut::kAosF32HiLo>(ops, io, s))) return st;
-  px_fallback_kernel<KL, Src, kFbDeferred><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar,
-                                                                     w.fb_count, w.fb_list, thb, so2, hbo, hb, off,
-                                                                     nullptr, nullptr, nullptr);
+  const unsigned fb_grid = (unsigned)device_sms() * OXM_FB_CTAS_PER_SM;
+  px_fallback_kernel<KL, Src><<<fb_grid, kFbThreads, 0, s>>>(ops, frames, g, w.Shi, w.Slo, w.Lp, w.ybar, w.fb_count,
+                                                             w.fb_list, thb, so2, hbo, hb, off);
   return check_launch("hybrid_fallback");
 }
 
@@ -1082,13 +1114,14 @@ int hybrid_prologue(const oxm_ctx* ctx, const void* frames, int64_t batch, int64
 
 // fallback + EM chunk counter reset, ordered before the low-pass kernel
 __global__ void zero_counters(uint32_t* fb, unsigned long long* em, unsigned long long* lead,
-                              unsigned long long* stats, unsigned long long* sel, uint32_t* blk) {
+                              unsigned long long* stats, unsigned long long* sel, uint32_t* blk, uint32_t* queued) {
   *fb = 0u;
   *em = 0ull;
   *lead = 0ull;
   stats[0] = stats[1] = stats[2] = 0ull;
   *sel = 0ull;
   *blk = 0u;
+  *queued = 0u;
 }
 
 }  // namespace
@@ -1104,13 +1137,15 @@ extern "C" int oxm_hybrid_em_counters(const oxm_ctx* ctx, void* workspace, int64
   const Workspace w = carve(workspace, ctx->ops.L, batch * d.h[n_levels] * d.w[n_levels]);
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
-  uint32_t blk = 0, queued = 0;
+  uint32_t blk = 0, queued = 0, deferred = 0;
   cudaError_t err = cudaMemcpyAsync(out, w.em_stats, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
   if (err == cudaSuccess) err = cudaMemcpyAsync(&blk, w.blk_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-  if (err == cudaSuccess) err = cudaMemcpyAsync(&queued, w.fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&queued, w.queued, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+  if (err == cudaSuccess) err = cudaMemcpyAsync(&deferred, w.fb_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
   if (err == cudaSuccess) err = cudaStreamSynchronize(s);
   out[3] = blk;
   out[4] = queued;
+  out[5] = deferred;
   if (err != cudaSuccess) {
     set_last_error("oxm_hybrid_em_counters", err);
     return OXM_ERR_CUDA;
@@ -1138,12 +1173,12 @@ int hybrid_maps(const oxm_ctx* ctx, const void* raw, const Src& src, int64_t bat
   int st = hybrid_prologue(ctx, raw, batch, height, width, n_levels, workspace, workspace_bytes_, d, nll, w);
   if (st) return st;
   if (batch == 0) return OXM_OK;
-  // the fallback list stores 31-bit pixel indices (+ kDeferTag)
-  if (batch * height * width >= (int64_t)kDeferTag) return OXM_ERR_ARGUMENT;
+  // the fallback list and its kernel use 32-bit pixel indices
+  if (batch * height * width >= ((int64_t)1 << 32)) return OXM_ERR_ARGUMENT;
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work, w.lead_work, w.em_stats, w.sel_work, w.blk_count);
+  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work, w.lead_work, w.em_stats, w.sel_work, w.blk_count, w.queued);
   if ((st = launch_ll(ctx->ops, src, batch, d, w.ybar, nll, flags, w.xinit, w.blk_flag, s))) return st;
   mark(ev, 1, s);
   if (fits) w.fits_out = fits;
@@ -1217,7 +1252,7 @@ extern "C" int oxm_hybrid_frame_f64(const oxm_ctx* ctx, const double* frames, in
   DeviceGuard dg(ctx->device);
   cudaStream_t s = as_stream(stream);
   mark(ev, 0, s);
-  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work, w.lead_work, w.em_stats, w.sel_work, w.blk_count);
+  zero_counters<<<1, 1, 0, s>>>(w.fb_count, w.em_work, w.lead_work, w.em_stats, w.sel_work, w.blk_count, w.queued);
   if ((st = launch_ll(ctx->ops, PlainSrc<double>{frames}, batch, d, w.ybar, nll, flags, w.xinit, nullptr, s))) return st;
   mark(ev, 1, s);
   mark(ev, 2, s);  // no fp32 lead-in on the fp64 path

@@ -63,9 +63,9 @@ class MapBatch:
 class HybridMapEngine:
     """Hybrid estimator for (B, H, W, 3) float32 frame batches on one GPU."""
 
-    # zero_counters, ll_kernel (+ EM fit #1), em_lead_kernel, em_persistent_kernel (tail),
-    # px_f32_kernel, px_fallback_kernel (classify), em_exact_kernel, px_fallback_kernel (deferred)
-    KERNELS_PER_RUN = 8
+    # zero_counters, ll_tma_kernel (+ EM fit #1), em_lead_kernel, em_persistent_kernel (tail),
+    # px_f32_kernel (+ in-warp fp64 fallback), exact pass (em_persistent / em_exact), px_fallback_kernel (deferred)
+    KERNELS_PER_RUN = 7
 
     def __init__(
         self,
@@ -129,17 +129,18 @@ class HybridMapEngine:
     def em_counters(self, batch: int, height: int, width: int) -> dict:
         """EM work of the last launch of this geometry: fp32 lead-in fits,
         fp64 tail fits, exact-mode restarts, blocks re-estimated all-fp64 for
-        the pixel fallback, pixels queued for the fp64 fallback (synchronises
-        the current stream)."""
+        the pixel fallback, pixels that took the fp64 fallback and, of those,
+        the ones deferred to after the exact pass (synchronises the current
+        stream)."""
         import ctypes
 
-        out = (ctypes.c_uint64 * 5)()
+        out = (ctypes.c_uint64 * 6)()
         st = self._lib.oxm_hybrid_em_counters(self.ctx.handle, ptr(self._workspace(self.workspace_bytes(batch, height, width))),
                                               batch, height, width, self.cfg.n_levels, out,
                                               stream_handle(None))
         _native.check(st, "em_counters")
         return {"lead_fits": int(out[0]), "tail_fits": int(out[1]), "restarts": int(out[2]),
-                "exact_blocks": int(out[3]), "queued_px": int(out[4])}
+                "exact_blocks": int(out[3]), "queued_px": int(out[4]), "deferred_px": int(out[5])}
 
     # ---- device-resident path ---------------------------------------------
     def launch(self, frames: torch.Tensor, out: MapBatch, *, stream: torch.cuda.Stream | None = None,

@@ -120,7 +120,7 @@ def test_set_em_lead_validation(cuda, sensitivity, basis):
     assert lib.oxm_ctx_set_em_lead(h, -1.0, 0.01, 0.0) == bad
     assert lib.oxm_ctx_set_em_lead(h, 16.0, 0.01, -1.0) == bad
     assert lib.oxm_ctx_set_em_lead(None, 16.0, 0.01, 0.0) == bad
-    out = (ctypes.c_uint64 * 5)()
+    out = (ctypes.c_uint64 * 6)()
     assert lib.oxm_hybrid_em_counters(None, None, 1, 8, 8, 1, out, None) == bad
 
 
