@@ -221,12 +221,17 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
 // a tile that belong to the next frame (or lie past the batch, zero-filled)
 // are never read.  A sample is non-finite iff the fp64 low-pass sum over its
 // block is (fp32 inputs cannot overflow fp64): 3 compares per coefficient.
+#ifndef OXM_LL_TMA_THREADS
+#define OXM_LL_TMA_THREADS 32
+#endif
 template <int NLV>
 struct LlTma {
   static_assert(NLV == 1 || NLV == 2, "3-level passes keep the per-thread-load ll_kernel (64 samples x 3 channels "
                                       "per thread do not fit a TMA tile pipeline's register budget)");
   static constexpr int S = 1 << NLV;
-  static constexpr int kThreads = 128;   // coefficients (threads) per tile
+  // one warp per CTA and per tile: the tile hand-off needs only __syncwarp,
+  // so warps never wait for each other (32 CTAs = 32 warps per SM)
+  static constexpr int kThreads = OXM_LL_TMA_THREADS;  // coefficients (threads) per tile
   static constexpr int TX = NLV == 1 ? 32 : 16;
   static constexpr int TY = kThreads / TX;
   static constexpr int kRowF = TX * S * 3;                // floats per tile row (box inner dim, 192)
@@ -234,7 +239,7 @@ struct LlTma {
   static constexpr int kTileF = kRowF * kRows;
   static constexpr uint32_t kTileBytes = kTileF * 4;
   static constexpr size_t kSmem = (size_t)kTileBytes;
-  static constexpr int kMinBlocks = NLV == 1 ? 12 : 8;
+  static constexpr int kMinBlocks = (NLV == 1 ? 1536 : 1024) / kThreads > 32 ? 32 : (NLV == 1 ? 1536 : 1024) / kThreads;
 };
 
 // level-K low-pass at level-K position (i, j) with the reference's per-level
@@ -345,7 +350,7 @@ __global__ void __launch_bounds__(LlTma<NLV>::kThreads, LlTma<NLV>::kMinBlocks) 
         for (int c = 0; c < 3; ++c) ll[c] = LpTile<NLV, G::kRowF>::at(tile, r0, c0, d, by, bx, c);
       }
     }
-    __syncthreads();  // every thread has its block in registers: the buffer is free
+    if constexpr (G::kThreads == 32) __syncwarp(); else __syncthreads();  // blocks in registers: buffer free
     if (tid == 0) {
       fence_proxy_async();
       issue(t + gridDim.x);
@@ -451,6 +456,8 @@ __device__ __forceinline__ void pixel_fit_f64(const DevOps& ops, SpecLoad spec, 
 
 // Where the per-pixel kernel sends the pixels it does not finish itself
 // (the fp64 fallback's "sensitive" ones, see px_f32_kernel's tail).
+constexpr int kFbBandCap = 32;  // band rows staged per warp by the in-kernel fp64 fallback
+
 struct FbOut {
   uint32_t* count;      // deferred pixels listed (fb list)
   uint32_t* list;
@@ -623,19 +630,23 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
     }
   }
   // Cancellation guard (rare: ~0.4% of textured pixels, clustered): pixels
-  // with a band below fallback_below are recomputed in fp64 right here, by the
-  // whole warp -- lane l takes band l (its block spectrum, the reference's eps
-  // clamp, a table log), and the three fit sums are reduced with xor shuffles
-  // (every lane ends with the same bits).  The pixel's rgb, ybar and spectrum
-  // rows were just read by this warp, so they come from L1, not DRAM.  With
-  // the EM precision schedule (fb.classify) a pixel with a band in
+  // with a band below fallback_below are recomputed in fp64 right here by
+  // their warp, four at a time: lane group g (8 lanes) takes the pending pixel
+  // of the g-th lane that has one, each lane of the group 4 of its bands (the
+  // block spectrum, the reference's eps clamp, a table log), and the three fit
+  // sums are reduced with xor shuffles inside the group (all 8 lanes end with
+  // the same bits).  The pixel's rgb, ybar and spectrum rows were just read
+  // by this warp, so they come from L1, not DRAM; the band rows of the
+  // operators are staged per warp in shared memory on first use.  With the
+  // EM precision schedule (fb.classify) a pixel with a band in
   // [eps / 2, exact_below) is "sensitive" to the schedule's ~1e-8 spectrum
   // deviation (see px_fallback_kernel): it is listed for the deferred pass
   // and its block for the all-fp64 exact pass instead.  Without the schedule
-  // the spectrum is hi + lo (fp64 to 48 bits) and every queued pixel is
-  // finished here.
+  // the spectrum is hi + lo (fp64 to 48 bits) and every pixel is finished here.
   if (__any_sync(0xffffffffu, any_fb)) {
-    const int lane = threadIdx.x & 31;
+    __shared__ double rows[kPxThreads / 32][kFbBandCap][6];  // per warp: solve row, fit column
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = lane >> 3, sub = lane & 7;
     unsigned mask = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r)
@@ -644,80 +655,91 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
         if (live && r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr)) mask |= 1u << (2 * r + c);
     const unsigned nq = __reduce_add_sync(0xffffffffu, __popc(mask));
     if (lane == 0 && fb.queued) atomicAdd(fb.queued, nq);
-    // this lane's band row (indexed constant-bank reads: once per warp that needs them)
-    double T0 = 0.0, T1 = 0.0, T2 = 0.0, F0 = 0.0, F1 = 0.0, F2 = 0.0;
-    if (lane < L) {
-      T0 = ops.solve[lane][0];
-      T1 = ops.solve[lane][1];
-      T2 = ops.solve[lane][2];
-      F0 = ops.fitm[0][lane];
-      F1 = ops.fitm[1][lane];
-      F2 = ops.fitm[2][lane];
+    __syncwarp();  // orders every lane's fp32 map stores before the fp64 rewrites below
+    double(*rw)[6] = rows[warp];
+    const bool staged = L <= kFbBandCap;
+    if (staged) {
+      for (int q = lane; q < 6 * L; q += 32) {
+        const int l = q / 6, k = q - 6 * l;
+        rw[l][k] = k < 3 ? ops.solve[l][k] : ops.fitm[k - 3][l];
+      }
+      __syncwarp();
     }
     const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below, eps = ops.eps;
     const double2* logt = log_table_global();
+    const uint32_t W32 = (uint32_t)g.W;
+    const unsigned lt = (1u << lane) - 1u;
     for (;;) {
       const unsigned m = __ballot_sync(0xffffffffu, mask != 0);
       if (!m) break;
-      const int owner = __ffs(m) - 1;
-      int bit = 0;
-      if (lane == owner) {
-        bit = __ffs(mask) - 1;
-        mask &= mask - 1;
-      }
-      bit = __shfl_sync(0xffffffffu, bit, owner);
-      const int64_t ocol = __shfl_sync(0xffffffffu, col, owner) + (bit & 1);
-      const int64_t p = (f * g.H + row0 + (bit >> 1)) * g.W + ocol;
+      // group g serves the lane holding the g-th set bit of m (if any)
+      const int owner = (int)__fns(m, 0, grp + 1);
+      const bool act = owner < 32;
+      const int own = act ? owner : 0;
+      const int b0 = mask ? __ffs(mask) - 1 : 0;
+      const int bit = __shfl_sync(0xffffffffu, b0, own);
+      const uint32_t ocol = (uint32_t)__shfl_sync(0xffffffffu, (int)col, own) + (bit & 1);
+      if (mask && __popc(m & lt) < 4) mask &= mask - 1;  // this lane's pixel is taken this pass
+      const uint32_t p = ((uint32_t)f * (uint32_t)g.H + (uint32_t)row0 + (uint32_t)(bit >> 1)) * W32 + ocol;
       const int64_t ob = (f * g.hL + by) * g.wL + (ocol >> g.n);
-      const double D0 = frames.at(3 * p) - ybar[ob];
-      const double D1 = frames.at(3 * p + 1) - ybar[g.nll + ob];
-      const double D2 = frames.at(3 * p + 2) - ybar[2 * g.nll + ob];
       double a0s = 0.0, a1s = 0.0, a2s = 0.0;
       bool sens = false;
-      for (int l = lane; l < L; l += 32) {
-        double t0 = T0, t1 = T1, t2 = T2, f0 = F0, f1 = F1, f2 = F2;
-        if (l >= 32) {  // band counts above 32 (generic-L builds)
-          t0 = ops.solve[l][0];
-          t1 = ops.solve[l][1];
-          t2 = ops.solve[l][2];
-          f0 = ops.fitm[0][l];
-          f1 = ops.fitm[1][l];
-          f2 = ops.fitm[2][l];
+      if (act) {
+        const double D0 = frames.at(3 * (int64_t)p) - ybar[ob];
+        const double D1 = frames.at(3 * (int64_t)p + 1) - ybar[g.nll + ob];
+        const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + ob];
+        for (int l = sub; l < L; l += 8) {
+          double t0, t1, t2, f0, f1, f2;
+          if (staged) {
+            t0 = rw[l][0];
+            t1 = rw[l][1];
+            t2 = rw[l][2];
+            f0 = rw[l][3];
+            f1 = rw[l][4];
+            f2 = rw[l][5];
+          } else {
+            t0 = ops.solve[l][0];
+            t1 = ops.solve[l][1];
+            t2 = ops.solve[l][2];
+            f0 = ops.fitm[0][l];
+            f1 = ops.fitm[1][l];
+            f2 = ops.fitm[2][l];
+          }
+          double S = (double)ldg(Shi + ob * Lp + l);
+          if (!fb.classify) S += (double)ldg(Slo + ob * Lp + l);
+          const double sp = fma(t2, D2, fma(t1, D1, fma(t0, D0, S)));
+          sens |= fb.classify && sp >= lo_b && sp < hi_b;
+          const double lg = log_tab(fmax(sp, eps), logt);
+          a0s = fma(f0, lg, a0s);
+          a1s = fma(f1, lg, a1s);
+          a2s = fma(f2, lg, a2s);
         }
-        double S = (double)ldg(Shi + ob * Lp + l);
-        if (!fb.classify) S += (double)ldg(Slo + ob * Lp + l);
-        const double sp = fma(t2, D2, fma(t1, D1, fma(t0, D0, S)));
-        sens |= fb.classify && sp >= lo_b && sp < hi_b;
-        const double lg = log_tab(fmax(sp, eps), logt);
-        a0s = fma(f0, lg, a0s);
-        a1s = fma(f1, lg, a1s);
-        a2s = fma(f2, lg, a2s);
       }
-      if (__any_sync(0xffffffffu, sens)) {  // defer: the exact pass re-estimates its block all-fp64
-        if (lane == owner) {
-          fb.list[atomicAdd(fb.count, 1u)] = (uint32_t)p;
-          unsigned* word = reinterpret_cast<unsigned*>(fb.blkflag + (ob & ~int64_t(3)));
-          const unsigned bitm = 1u << (8 * (unsigned)(ob & 3));
-          if (!(atomicOr(word, bitm) & bitm)) fb.blk_list[atomicAdd(fb.blk_count, 1u)] = (uint32_t)ob;
-        }
-        continue;
-      }
+      const bool gsens = ((__ballot_sync(0xffffffffu, sens) >> (8 * grp)) & 0xffu) != 0;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
+      for (int o = 4; o > 0; o >>= 1) {
         a0s += __shfl_xor_sync(0xffffffffu, a0s, o);
         a1s += __shfl_xor_sync(0xffffffffu, a1s, o);
         a2s += __shfl_xor_sync(0xffffffffu, a2s, o);
       }
-      if (lane == owner) {  // the owner also made this pixel's fp32 stores: program order
-        const float xo = (float)(-a0s * g.cal), xd = (float)(-a1s * g.cal);
-        const float co = fmaxf(xo, 0.f);
-        const float t = co + fmaxf(xd, 0.f);
-        thb[p] = t;
-        so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
-        if constexpr (PLANES) {
-          hbo[p] = xo;
-          hb[p] = xd;
-          off[p] = (float)(-a2s);
+      if (act && sub == 0) {
+        if (gsens) {  // defer: the exact pass re-estimates its block all-fp64
+          fb.list[atomicAdd(fb.count, 1u)] = p;
+          unsigned* word = reinterpret_cast<unsigned*>(fb.blkflag + (ob & ~int64_t(3)));
+          const unsigned bitm = 1u << (8 * (unsigned)(ob & 3));
+          if (!(atomicOr(word, bitm) & bitm)) fb.blk_list[atomicAdd(fb.blk_count, 1u)] = (uint32_t)ob;
+        } else {
+          // overwrites the owner lane's fp32 stores (ordered by the __syncwarp above)
+          const float xo = (float)(-a0s * g.cal), xd = (float)(-a1s * g.cal);
+          const float co = fmaxf(xo, 0.f);
+          const float t = co + fmaxf(xd, 0.f);
+          thb[p] = t;
+          so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
+          if constexpr (PLANES) {
+            hbo[p] = xo;
+            hb[p] = xd;
+            off[p] = (float)(-a2s);
+          }
         }
       }
     }

@@ -22,7 +22,16 @@ import torch
 
 from . import _native
 from .bayes import BayesConfig, LowPassBlock, em_device, em_operator_set, fit_device
-from .core import ChromophoreBasis, CameraSensitivity, ConcentrationMap, RgbImage, SpectralCube, check_grids
+from .core import (
+    CameraSensitivity,
+    ChromophoreBasis,
+    ConcentrationMap,
+    RgbImage,
+    SpectralCube,
+    check_grids,
+    trusted_cube,
+    trusted_map,
+)
 from .device import download, ptr, require_cuda, stream_handle, upload
 from .errors import ArgumentError, DataError
 from .haar import level_dims
@@ -183,12 +192,12 @@ def estimate_frame(
             stats.update(bayes_coefficients=0, tikhonov_coefficients=n_lp + n_dir)
         return cube, _map_from_planes(download(x), H, W)
 
-    # hybrid
+    # hybrid (outputs come straight from the kernels: no host-side re-validation)
     ops = _hybrid_operators(sensitivity, basis, cfg)
     out = hybrid_device(upload(frame.data[None], torch.float64, dev), ops, cfg.n_levels, cal)
-    cube = SpectralCube(grid=grid, data=download(out["cube"][0]))
+    cube = trusted_cube(grid, download(out["cube"][0]))
     xs = download(out["x"][:, 0])
-    cmap = ConcentrationMap(hbo=xs[0], hb=xs[1], offset=xs[2])
+    cmap = trusted_map(xs[0], xs[1], xs[2])
     if stats is not None:
         stats.update(bayes_coefficients=n_lp, tikhonov_coefficients=n_dir)
     return cube, cmap
@@ -326,4 +335,4 @@ class _SequenceRunner:
         if f & _native.FLAG_NEGATIVE_LL:
             raise ArgumentError("low-pass coefficients must be finite and non-negative")
         xs = sl["h_x"].numpy()[:, 0]
-        return ConcentrationMap(hbo=xs[0].copy(), hb=xs[1].copy(), offset=xs[2].copy()), t_sub
+        return trusted_map(xs[0].copy(), xs[1].copy(), xs[2].copy()), t_sub

@@ -65,6 +65,17 @@ def main():
     out["K1 haar_forward_f32 1080p n=2 C=3"] = timed(
         lambda i: lib.oxm_haar_forward_f32(frames[i].data_ptr(), H, W, C, n, planes[i].data_ptr(), flags.data_ptr(), s),
         4 * (H * W * C + nplanes * C))
+    # K1 at 4K (BASELINE config 5 frame size, 3 levels): the same kernel on a 4x larger plane
+    H4, W4, n4 = 2160, 3840, 3
+    dims4 = level_dims(H4, W4, n4)
+    np4 = sum(4 * h * w for h, w in dims4)
+    f4 = torch.rand((2, H4, W4, C), dtype=torch.float32, device=dev)
+    pl4 = torch.empty((2, np4 * C), dtype=torch.float32, device=dev)
+    out["K1 haar_forward_f32 4K n=3 C=3"] = timed(
+        lambda i: lib.oxm_haar_forward_f32(f4[i % 2].data_ptr(), H4, W4, C, n4, pl4[i % 2].data_ptr(),
+                                           flags.data_ptr(), s),
+        4 * (H4 * W4 * C + np4 * C))
+    del f4, pl4
     planes64 = torch.empty((2, nplanes * C), dtype=torch.float64, device=dev)
     frames64 = frames[:2].double().contiguous()
     out["K1 haar_forward_f64 1080p n=2 C=3"] = timed(
