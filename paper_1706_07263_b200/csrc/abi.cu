@@ -124,6 +124,25 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
         delete c;
         return OXM_ERR_NUMERICAL;
       }
+  {
+    double rows[kMaxBands * 8] = {};
+    for (int l = 0; l < L; ++l)
+      for (int k = 0; k < 3; ++k) {
+        rows[8 * l + k] = d.solve[l][k];
+        rows[8 * l + 3 + k] = d.fitm[k][l];
+      }
+    DeviceGuard dg(device);
+    void* dev = nullptr;
+    cudaError_t err = cudaMalloc(&dev, sizeof(double) * 8 * (size_t)L);
+    if (err == cudaSuccess) err = cudaMemcpy(dev, rows, sizeof(double) * 8 * (size_t)L, cudaMemcpyHostToDevice);
+    if (err != cudaSuccess) {
+      set_last_error("oxm_ctx_create band rows", err);
+      if (dev) cudaFree(dev);
+      delete c;
+      return OXM_ERR_CUDA;
+    }
+    d.band_rows = static_cast<const double*>(dev);
+  }
   *out = c;
   return OXM_OK;
 }
@@ -136,6 +155,10 @@ extern "C" int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, dou
 }
 
 extern "C" int oxm_ctx_destroy(oxm_ctx* ctx) {
+  if (ctx && ctx->ops.band_rows) {
+    DeviceGuard dg(ctx->device);
+    cudaFree(const_cast<double*>(ctx->ops.band_rows));
+  }
   delete ctx;
   return OXM_OK;
 }

@@ -456,8 +456,6 @@ __device__ __forceinline__ void pixel_fit_f64(const DevOps& ops, SpecLoad spec, 
 
 // Where the per-pixel kernel sends the pixels it does not finish itself
 // (the fp64 fallback's "sensitive" ones, see px_f32_kernel's tail).
-constexpr int kFbBandCap = 32;  // band rows staged per warp by the in-kernel fp64 fallback
-
 struct FbOut {
   uint32_t* count;      // deferred pixels listed (fb list)
   uint32_t* list;
@@ -637,15 +635,14 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   // sums are reduced with xor shuffles inside the group (all 8 lanes end with
   // the same bits).  The pixel's rgb, ybar and spectrum rows were just read
   // by this warp, so they come from L1, not DRAM; the band rows of the
-  // operators are staged per warp in shared memory on first use.  With the
+  // operators' band rows come from a 64-byte-per-band device copy (L1).  With the
   // EM precision schedule (fb.classify) a pixel with a band in
   // [eps / 2, exact_below) is "sensitive" to the schedule's ~1e-8 spectrum
   // deviation (see px_fallback_kernel): it is listed for the deferred pass
   // and its block for the all-fp64 exact pass instead.  Without the schedule
   // the spectrum is hi + lo (fp64 to 48 bits) and every pixel is finished here.
   if (__any_sync(0xffffffffu, any_fb)) {
-    __shared__ double rows[kPxThreads / 32][kFbBandCap][6];  // per warp: solve row, fit column
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const int grp = lane >> 3, sub = lane & 7;
     unsigned mask = 0;
 #pragma unroll
@@ -656,15 +653,7 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
     const unsigned nq = __reduce_add_sync(0xffffffffu, __popc(mask));
     if (lane == 0 && fb.queued) atomicAdd(fb.queued, nq);
     __syncwarp();  // orders every lane's fp32 map stores before the fp64 rewrites below
-    double(*rw)[6] = rows[warp];
-    const bool staged = L <= kFbBandCap;
-    if (staged) {
-      for (int q = lane; q < 6 * L; q += 32) {
-        const int l = q / 6, k = q - 6 * l;
-        rw[l][k] = k < 3 ? ops.solve[l][k] : ops.fitm[k - 3][l];
-      }
-      __syncwarp();
-    }
+    const double2* rows = reinterpret_cast<const double2*>(ops.band_rows);  // 4 double2 per band
     const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below, eps = ops.eps;
     const double2* logt = log_table_global();
     const uint32_t W32 = (uint32_t)g.W;
@@ -689,22 +678,8 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
         const double D1 = frames.at(3 * (int64_t)p + 1) - ybar[g.nll + ob];
         const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + ob];
         for (int l = sub; l < L; l += 8) {
-          double t0, t1, t2, f0, f1, f2;
-          if (staged) {
-            t0 = rw[l][0];
-            t1 = rw[l][1];
-            t2 = rw[l][2];
-            f0 = rw[l][3];
-            f1 = rw[l][4];
-            f2 = rw[l][5];
-          } else {
-            t0 = ops.solve[l][0];
-            t1 = ops.solve[l][1];
-            t2 = ops.solve[l][2];
-            f0 = ops.fitm[0][l];
-            f1 = ops.fitm[1][l];
-            f2 = ops.fitm[2][l];
-          }
+          const double2 r01 = ldg(rows + 4 * l), r23 = ldg(rows + 4 * l + 1), r45 = ldg(rows + 4 * l + 2);
+          const double t0 = r01.x, t1 = r01.y, t2 = r23.x, f0 = r23.y, f1 = r45.x, f2 = r45.y;
           double S = (double)ldg(Shi + ob * Lp + l);
           if (!fb.classify) S += (double)ldg(Slo + ob * Lp + l);
           const double sp = fma(t2, D2, fma(t1, D1, fma(t0, D0, S)));

@@ -41,6 +41,10 @@ struct DevOps {
   double sens[3][kMaxBands];   // camera matrix C, core.py:112-131
   double gain[kMaxBands][3];   // N^-1 C^T, N = C^T C + beta D2^T D2 (bayes.py:117-129)
   double xis[kMaxBands][2];    // xi[:, 0:2] * 256/ln2: EM exp arguments pre-scaled (oxm_math.cuh)
+  // device copy of the per-band rows {solve[l][0..2], fitm[0..2][l], 0, 0}
+  // (L x 8 doubles, 64 B per band): code that indexes bands by lane reads
+  // them with coalesced loads instead of serialised indexed constant loads
+  const double* band_rows;
 };
 
 struct oxm_ctx_impl {
