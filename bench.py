@@ -615,7 +615,7 @@ def run_ours(args):
     parity["schedule"] = sched
     dropin = None
     if world == 1 and not args.no_dropin:
-        dropin = dropin_record(sample, n, min(DROPIN_SEQ_FRAMES, len(sample)))
+        dropin = dropin_record(frames[:DROPIN_SEQ_FRAMES].cpu().numpy(), n, DROPIN_SEQ_FRAMES)
 
     peaks = probe_peaks(lib, torch, dev)
     mp = ROOT / "MEASURED_PEAKS.json"
@@ -714,7 +714,7 @@ FP64_INST_PER_FIT = 749.1
 FLOPS_PER_FIT = 1293.2
 MUFU_PER_LEAD_FIT = 2 * 26  # fp32 lead-in: one ex2 and one lg2 per band
 CPU_OTHER_FRAMES = 3   # frames for the slower reference thread setting (threads=1, BLAS=nproc)
-DROPIN_SEQ_FRAMES = 6
+DROPIN_SEQ_FRAMES = 8
 # kernels launched per step: zero_counters, ll_tma (+ fit #1), em_lead, em_persistent (tail),
 # px_f32 (+ in-warp fp64 fallback), exact pass, px_fallback (deferred)
 HybridMapLaunches = 7

@@ -629,92 +629,97 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   }
   // Cancellation guard (rare: ~0.4% of textured pixels, clustered): pixels
   // with a band below fallback_below are recomputed in fp64 right here by
-  // their warp, four at a time: lane group g (8 lanes) takes the pending pixel
-  // of the g-th lane that has one, each lane of the group 4 of its bands (the
-  // block spectrum, the reference's eps clamp, a table log), and the three fit
-  // sums are reduced with xor shuffles inside the group (all 8 lanes end with
-  // the same bits).  The pixel's rgb, ybar and spectrum rows were just read
-  // by this warp, so they come from L1, not DRAM; the band rows of the
-  // operators' band rows come from a 64-byte-per-band device copy (L1).  With the
-  // EM precision schedule (fb.classify) a pixel with a band in
+  // their warp.  The warp's pending pixels are first packed into a per-warp
+  // list in shared memory (a lane can hold up to 2R of them), then lane group
+  // g (8 lanes) takes list entries g, g + 4, ...: each lane of the group 4 of
+  // the pixel's bands (the block spectrum, the reference's eps clamp, a table
+  // log), the three fit sums reduced with xor shuffles inside the group (all 8
+  // lanes end with the same bits).  The pixel's rgb, ybar and spectrum rows
+  // were just read by this warp, so they come from L1, not DRAM; the
+  // operators' band rows come from a 64-byte-per-band device copy (L1).  With
+  // the EM precision schedule (fb.classify) a pixel with a band in
   // [eps / 2, exact_below) is "sensitive" to the schedule's ~1e-8 spectrum
-  // deviation (see px_fallback_kernel): it is listed for the deferred pass
-  // and its block for the all-fp64 exact pass instead.  Without the schedule
-  // the spectrum is hi + lo (fp64 to 48 bits) and every pixel is finished here.
+  // deviation (see px_fallback_kernel): it is listed for the deferred pass and
+  // its block for the all-fp64 exact pass instead.  Without the schedule the
+  // spectrum is hi + lo (fp64 to 48 bits) and every pixel is finished here.
   if (__any_sync(0xffffffffu, any_fb)) {
+    __shared__ uint32_t pend[kPxThreads / 32][32 * 2 * R];  // (row << 24) | column, per warp
     const int lane = threadIdx.x & 31;
-    const int grp = lane >> 3, sub = lane & 7;
+    uint32_t* lst = pend[threadIdx.x >> 5];
     unsigned mask = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < 2; ++c)
         if (live && r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr)) mask |= 1u << (2 * r + c);
-    const unsigned nq = __reduce_add_sync(0xffffffffu, __popc(mask));
-    if (lane == 0 && fb.queued) atomicAdd(fb.queued, nq);
-    __syncwarp();  // orders every lane's fp32 map stores before the fp64 rewrites below
+    const unsigned cnt = __popc(mask);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane == 31 && fb.queued) atomicAdd(fb.queued, total);
+    unsigned pos = incl - cnt;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+        if (mask & (1u << (2 * r + c))) lst[pos++] = ((uint32_t)r << 24) | (uint32_t)(col + c);
+    __syncwarp();  // the list, and every lane's fp32 map stores before the fp64 rewrites below
+    const int grp = lane >> 3, sub = lane & 7;
+    const unsigned gm = 0xffu << (8 * grp);
     const double2* rows = reinterpret_cast<const double2*>(ops.band_rows);  // 4 double2 per band
     const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below, eps = ops.eps;
     const double2* logt = log_table_global();
-    const uint32_t W32 = (uint32_t)g.W;
-    const unsigned lt = (1u << lane) - 1u;
-    for (;;) {
-      const unsigned m = __ballot_sync(0xffffffffu, mask != 0);
-      if (!m) break;
-      // group g serves the lane holding the g-th set bit of m (if any)
-      const int owner = (int)__fns(m, 0, grp + 1);
-      const bool act = owner < 32;
-      const int own = act ? owner : 0;
-      const int b0 = mask ? __ffs(mask) - 1 : 0;
-      const int bit = __shfl_sync(0xffffffffu, b0, own);
-      const uint32_t ocol = (uint32_t)__shfl_sync(0xffffffffu, (int)col, own) + (bit & 1);
-      if (mask && __popc(m & lt) < 4) mask &= mask - 1;  // this lane's pixel is taken this pass
-      const uint32_t p = ((uint32_t)f * (uint32_t)g.H + (uint32_t)row0 + (uint32_t)(bit >> 1)) * W32 + ocol;
+    const uint32_t W32 = (uint32_t)g.W, prow = (uint32_t)(f * g.H + row0);
+    for (unsigned k = grp; k < total; k += 4) {  // group-uniform trip count
+      const uint32_t e = lst[k];
+      const uint32_t ocol = e & 0xffffffu;
+      const uint32_t p = (prow + (e >> 24)) * W32 + ocol;
       const int64_t ob = (f * g.hL + by) * g.wL + (ocol >> g.n);
+      const double D0 = frames.at(3 * (int64_t)p) - ybar[ob];
+      const double D1 = frames.at(3 * (int64_t)p + 1) - ybar[g.nll + ob];
+      const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + ob];
       double a0s = 0.0, a1s = 0.0, a2s = 0.0;
       bool sens = false;
-      if (act) {
-        const double D0 = frames.at(3 * (int64_t)p) - ybar[ob];
-        const double D1 = frames.at(3 * (int64_t)p + 1) - ybar[g.nll + ob];
-        const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + ob];
-        for (int l = sub; l < L; l += 8) {
-          const double2 r01 = ldg(rows + 4 * l), r23 = ldg(rows + 4 * l + 1), r45 = ldg(rows + 4 * l + 2);
-          const double t0 = r01.x, t1 = r01.y, t2 = r23.x, f0 = r23.y, f1 = r45.x, f2 = r45.y;
-          double S = (double)ldg(Shi + ob * Lp + l);
-          if (!fb.classify) S += (double)ldg(Slo + ob * Lp + l);
-          const double sp = fma(t2, D2, fma(t1, D1, fma(t0, D0, S)));
-          sens |= fb.classify && sp >= lo_b && sp < hi_b;
-          const double lg = log_tab(fmax(sp, eps), logt);
-          a0s = fma(f0, lg, a0s);
-          a1s = fma(f1, lg, a1s);
-          a2s = fma(f2, lg, a2s);
-        }
+      for (int l = sub; l < L; l += 8) {
+        const double2 r01 = ldg(rows + 4 * l), r23 = ldg(rows + 4 * l + 1), r45 = ldg(rows + 4 * l + 2);
+        double S = (double)ldg(Shi + ob * Lp + l);
+        if (!fb.classify) S += (double)ldg(Slo + ob * Lp + l);
+        const double sp = fma(r23.x, D2, fma(r01.y, D1, fma(r01.x, D0, S)));
+        sens |= fb.classify && sp >= lo_b && sp < hi_b;
+        const double lg = log_tab(fmax(sp, eps), logt);
+        a0s = fma(r23.y, lg, a0s);
+        a1s = fma(r45.x, lg, a1s);
+        a2s = fma(r45.y, lg, a2s);
       }
-      const bool gsens = ((__ballot_sync(0xffffffffu, sens) >> (8 * grp)) & 0xffu) != 0;
-#pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        a0s += __shfl_xor_sync(0xffffffffu, a0s, o);
-        a1s += __shfl_xor_sync(0xffffffffu, a1s, o);
-        a2s += __shfl_xor_sync(0xffffffffu, a2s, o);
-      }
-      if (act && sub == 0) {
-        if (gsens) {  // defer: the exact pass re-estimates its block all-fp64
+      if (__any_sync(gm, sens)) {  // defer: the exact pass re-estimates its block all-fp64
+        if (sub == 0) {
           fb.list[atomicAdd(fb.count, 1u)] = p;
           unsigned* word = reinterpret_cast<unsigned*>(fb.blkflag + (ob & ~int64_t(3)));
           const unsigned bitm = 1u << (8 * (unsigned)(ob & 3));
           if (!(atomicOr(word, bitm) & bitm)) fb.blk_list[atomicAdd(fb.blk_count, 1u)] = (uint32_t)ob;
-        } else {
-          // overwrites the owner lane's fp32 stores (ordered by the __syncwarp above)
-          const float xo = (float)(-a0s * g.cal), xd = (float)(-a1s * g.cal);
-          const float co = fmaxf(xo, 0.f);
-          const float t = co + fmaxf(xd, 0.f);
-          thb[p] = t;
-          so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
-          if constexpr (PLANES) {
-            hbo[p] = xo;
-            hb[p] = xd;
-            off[p] = (float)(-a2s);
-          }
+        }
+        continue;
+      }
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        a0s += __shfl_xor_sync(gm, a0s, o);
+        a1s += __shfl_xor_sync(gm, a1s, o);
+        a2s += __shfl_xor_sync(gm, a2s, o);
+      }
+      if (sub == 0) {  // overwrites the fp32 stores of this pixel (ordered by the __syncwarp above)
+        const float xo = (float)(-a0s * g.cal), xd = (float)(-a1s * g.cal);
+        const float co = fmaxf(xo, 0.f);
+        const float t = co + fmaxf(xd, 0.f);
+        thb[p] = t;
+        so2[p] = t > 0.f ? __fdividef(co, t) : qnan_f();
+        if constexpr (PLANES) {
+          hbo[p] = xo;
+          hb[p] = xd;
+          off[p] = (float)(-a2s);
         }
       }
     }

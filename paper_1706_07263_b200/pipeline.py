@@ -273,6 +273,32 @@ def _sequence_plain(frames, sensitivity, basis, cfg, timings):
         yield cmap
 
 
+_COPY_POOL = None
+
+
+def _copy_pool():
+    global _COPY_POOL
+    if _COPY_POOL is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _COPY_POOL = ThreadPoolExecutor(max_workers=4, thread_name_prefix="oxm-copy")
+    return _COPY_POOL
+
+
+def _par_copy(pairs) -> None:
+    """np.copyto for (dst, src) pairs, each split by rows over a small thread
+    pool (NumPy releases the GIL for large copies): the host-side memcpys of
+    50 MB frames and maps are what bound estimate_sequence."""
+    jobs = []
+    for dst, src in pairs:
+        rows = dst.shape[0]
+        step = max(1, -(-rows // 4))
+        for r in range(0, rows, step):
+            jobs.append(_copy_pool().submit(np.copyto, dst[r : r + step], src[r : r + step]))
+    for j in jobs:
+        j.result()
+
+
 class _SequenceRunner:
     """Two pipeline slots for estimate_sequence: pinned host staging, device
     frame, workspace and fp64 map planes per slot, each on its own stream."""
@@ -311,7 +337,7 @@ class _SequenceRunner:
         self.turn ^= 1
         t_sub = time.perf_counter()
         sl["done"].synchronize()  # the slot's previous frame has been collected
-        np.copyto(sl["h_in"].numpy()[0], frame.data)
+        _par_copy([(sl["h_in"].numpy()[0], frame.data)])
         s = sl["stream"]
         with torch.cuda.stream(s):
             sl["d_in"].copy_(sl["h_in"], non_blocking=True)
@@ -335,4 +361,6 @@ class _SequenceRunner:
         if f & _native.FLAG_NEGATIVE_LL:
             raise ArgumentError("low-pass coefficients must be finite and non-negative")
         xs = sl["h_x"].numpy()[:, 0]
-        return trusted_map(xs[0].copy(), xs[1].copy(), xs[2].copy()), t_sub
+        planes = [np.empty_like(xs[k]) for k in range(3)]
+        _par_copy([(planes[k], xs[k]) for k in range(3)])
+        return trusted_map(planes[0], planes[1], planes[2]), t_sub
