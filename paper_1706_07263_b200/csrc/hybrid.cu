@@ -627,90 +627,91 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
       any_fb |= !(vmin[r][0] >= thr) || (two && !(vmin[r][1] >= thr));
     }
   }
-  // Cancellation guard (rare: ~0.4% of textured pixels, clustered): pixels
-  // with a band below fallback_below are recomputed in fp64 right here by
-  // their warp.  The warp's pending pixels are first packed into a per-warp
-  // list in shared memory (a lane can hold up to 2R of them), then lane group
-  // g (8 lanes) takes list entries g, g + 4, ...: each lane of the group 4 of
-  // the pixel's bands (the block spectrum, the reference's eps clamp, a table
-  // log), the three fit sums reduced with xor shuffles inside the group (all 8
-  // lanes end with the same bits).  The pixel's rgb, ybar and spectrum rows
+  // Cancellation guard: pixels with a band below fallback_below (~0.4% of
+  // textured pixels, but spread so that about half of all warps hold one or
+  // two) are recomputed in fp64 right here by their warp, one pixel per pass:
+  // lane l takes band l (the block spectrum, the reference's eps clamp, a
+  // table log) and the three fit sums are reduced with xor shuffles (every
+  // lane ends with the same bits).  The pixel's rgb, ybar and spectrum rows
   // were just read by this warp, so they come from L1, not DRAM; the
-  // operators' band rows come from a 64-byte-per-band device copy (L1).  With
-  // the EM precision schedule (fb.classify) a pixel with a band in
-  // [eps / 2, exact_below) is "sensitive" to the schedule's ~1e-8 spectrum
-  // deviation (see px_fallback_kernel): it is listed for the deferred pass and
-  // its block for the all-fp64 exact pass instead.  Without the schedule the
-  // spectrum is hi + lo (fp64 to 48 bits) and every pixel is finished here.
+  // operators' band rows come from a 64-byte-per-band device copy, loaded
+  // once per warp.  With the EM precision schedule (fb.classify) a pixel with
+  // a band in [eps / 2, exact_below) is "sensitive" to the schedule's ~1e-8
+  // spectrum deviation (see px_fallback_kernel): it is listed for the
+  // deferred pass and its block for the all-fp64 exact pass instead.  Without
+  // the schedule the spectrum is hi + lo (fp64 to 48 bits) and every pixel is
+  // finished here.  (Band counts above 32 take each lane's extra bands from
+  // the same rows.)
   if (__any_sync(0xffffffffu, any_fb)) {
-    __shared__ uint32_t pend[kPxThreads / 32][32 * 2 * R];  // (row << 24) | column, per warp
     const int lane = threadIdx.x & 31;
-    uint32_t* lst = pend[threadIdx.x >> 5];
     unsigned mask = 0;
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int c = 0; c < 2; ++c)
         if (live && r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr)) mask |= 1u << (2 * r + c);
-    const unsigned cnt = __popc(mask);
-    unsigned incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+    if (fb.queued) {
+      const unsigned nq = __reduce_add_sync(0xffffffffu, __popc(mask));
+      if (lane == 0) atomicAdd(fb.queued, nq);
     }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-    if (lane == 31 && fb.queued) atomicAdd(fb.queued, total);
-    unsigned pos = incl - cnt;
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        if (mask & (1u << (2 * r + c))) lst[pos++] = ((uint32_t)r << 24) | (uint32_t)(col + c);
-    __syncwarp();  // the list, and every lane's fp32 map stores before the fp64 rewrites below
-    const int grp = lane >> 3, sub = lane & 7;
-    const unsigned gm = 0xffu << (8 * grp);
+    __syncwarp();  // every lane's fp32 map stores land before the fp64 rewrites below
     const double2* rows = reinterpret_cast<const double2*>(ops.band_rows);  // 4 double2 per band
+    double2 r01 = make_double2(0.0, 0.0), r23 = r01, r45 = r01;
+    if (lane < L) {
+      r01 = ldg(rows + 4 * lane);
+      r23 = ldg(rows + 4 * lane + 1);
+      r45 = ldg(rows + 4 * lane + 2);
+    }
     const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below, eps = ops.eps;
     const double2* logt = log_table_global();
-    const uint32_t W32 = (uint32_t)g.W, prow = (uint32_t)(f * g.H + row0);
-    for (unsigned k = grp; k < total; k += 4) {  // group-uniform trip count
-      const uint32_t e = lst[k];
-      const uint32_t ocol = e & 0xffffffu;
-      const uint32_t p = (prow + (e >> 24)) * W32 + ocol;
-      const int64_t ob = (f * g.hL + by) * g.wL + (ocol >> g.n);
+    const uint32_t W32 = (uint32_t)g.W, prow = (uint32_t)(f * g.H + row0), col32 = (uint32_t)col;
+    const uint32_t frow = (uint32_t)((f * g.hL + by) * g.wL);
+    for (;;) {
+      const unsigned m = __ballot_sync(0xffffffffu, mask != 0);
+      if (!m) break;
+      const int owner = __ffs(m) - 1;
+      const int bit = __shfl_sync(0xffffffffu, mask ? __ffs(mask) - 1 : 0, owner);
+      if (lane == owner) mask &= mask - 1;
+      const uint32_t ocol = __shfl_sync(0xffffffffu, col32, owner) + (uint32_t)(bit & 1);
+      const uint32_t p = (prow + (uint32_t)(bit >> 1)) * W32 + ocol;
+      const uint32_t ob = frow + (ocol >> g.n);
       const double D0 = frames.at(3 * (int64_t)p) - ybar[ob];
       const double D1 = frames.at(3 * (int64_t)p + 1) - ybar[g.nll + ob];
       const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + ob];
       double a0s = 0.0, a1s = 0.0, a2s = 0.0;
       bool sens = false;
-      for (int l = sub; l < L; l += 8) {
-        const double2 r01 = ldg(rows + 4 * l), r23 = ldg(rows + 4 * l + 1), r45 = ldg(rows + 4 * l + 2);
-        double S = (double)ldg(Shi + ob * Lp + l);
-        if (!fb.classify) S += (double)ldg(Slo + ob * Lp + l);
-        const double sp = fma(r23.x, D2, fma(r01.y, D1, fma(r01.x, D0, S)));
+      for (int l = lane; l < L; l += 32) {
+        double2 q01 = r01, q23 = r23, q45 = r45;
+        if (l >= 32) {
+          q01 = ldg(rows + 4 * l);
+          q23 = ldg(rows + 4 * l + 1);
+          q45 = ldg(rows + 4 * l + 2);
+        }
+        double S = (double)ldg(Shi + (int64_t)ob * Lp + l);
+        if (!fb.classify) S += (double)ldg(Slo + (int64_t)ob * Lp + l);
+        const double sp = fma(q23.x, D2, fma(q01.y, D1, fma(q01.x, D0, S)));
         sens |= fb.classify && sp >= lo_b && sp < hi_b;
         const double lg = log_tab(fmax(sp, eps), logt);
-        a0s = fma(r23.y, lg, a0s);
-        a1s = fma(r45.x, lg, a1s);
-        a2s = fma(r45.y, lg, a2s);
+        a0s = fma(q23.y, lg, a0s);
+        a1s = fma(q45.x, lg, a1s);
+        a2s = fma(q45.y, lg, a2s);
       }
-      if (__any_sync(gm, sens)) {  // defer: the exact pass re-estimates its block all-fp64
-        if (sub == 0) {
+      if (__any_sync(0xffffffffu, sens)) {  // defer: the exact pass re-estimates its block all-fp64
+        if (lane == owner) {
           fb.list[atomicAdd(fb.count, 1u)] = p;
-          unsigned* word = reinterpret_cast<unsigned*>(fb.blkflag + (ob & ~int64_t(3)));
-          const unsigned bitm = 1u << (8 * (unsigned)(ob & 3));
-          if (!(atomicOr(word, bitm) & bitm)) fb.blk_list[atomicAdd(fb.blk_count, 1u)] = (uint32_t)ob;
+          unsigned* word = reinterpret_cast<unsigned*>(fb.blkflag + (ob & ~3u));
+          const unsigned bitm = 1u << (8 * (ob & 3u));
+          if (!(atomicOr(word, bitm) & bitm)) fb.blk_list[atomicAdd(fb.blk_count, 1u)] = ob;
         }
         continue;
       }
 #pragma unroll
-      for (int o = 4; o > 0; o >>= 1) {
-        a0s += __shfl_xor_sync(gm, a0s, o);
-        a1s += __shfl_xor_sync(gm, a1s, o);
-        a2s += __shfl_xor_sync(gm, a2s, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        a0s += __shfl_xor_sync(0xffffffffu, a0s, o);
+        a1s += __shfl_xor_sync(0xffffffffu, a1s, o);
+        a2s += __shfl_xor_sync(0xffffffffu, a2s, o);
       }
-      if (sub == 0) {  // overwrites the fp32 stores of this pixel (ordered by the __syncwarp above)
+      if (lane == owner) {
         const float xo = (float)(-a0s * g.cal), xd = (float)(-a1s * g.cal);
         const float co = fmaxf(xo, 0.f);
         const float t = co + fmaxf(xd, 0.f);
