@@ -411,14 +411,14 @@ bool launch_ll_tma_n(const DevOps& ops, const float* frames, int64_t batch, cons
   return true;
 }
 
-// OXM_LL_TMA=0 in the environment selects the per-thread-load ll_kernel
-// instead (A/B measurements; read once per process)
+// Default: the per-thread-load ll_kernel, which measured faster on the fused
+// path (profiles/r02_ll_tma_ab.txt: 6.12 vs 6.49 us per 1080p frame; the
+// pass is bound jointly by HBM and the fp64 start fit, and the per-thread
+// kernel keeps more independent warps in flight than the tile pipeline).
+// OXM_LL_TMA=1 in the environment selects ll_tma_kernel (read at each launch).
 inline bool ll_tma_enabled() {
-  static const bool on = [] {
-    const char* e = getenv("OXM_LL_TMA");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+  const char* e = getenv("OXM_LL_TMA");
+  return e && e[0] == '1';
 }
 
 bool launch_ll_tma(const DevOps& ops, const float* frames, int64_t batch, const LevelDims& d, double* ybar, int64_t nll,

@@ -145,13 +145,20 @@ def test_engine_small_and_odd(cuda, sensitivity, basis, H, W, n, td):
     _engine_vs_oracle(cuda, sensitivity, basis, frames, n)
 
 
-@pytest.mark.parametrize("H,W,n", [(1082, 1924, 2), (578, 724, 1), (1085, 1928, 3)])
-def test_engine_tma_edge_tiles(cuda, sensitivity, basis, H, W, n):
-    """Frames whose rows are 16-byte multiples take the TMA-staged low-pass
-    kernel (ll_tma_kernel); these sizes leave partial tiles and odd level
-    dimensions (per-level edge replication) at the right and bottom."""
+@pytest.mark.parametrize("H,W,n", [(1082, 1924, 2), (578, 724, 1), (64, 64, 2), (1085, 1928, 3)])
+def test_engine_tma_edge_tiles(cuda, sensitivity, basis, H, W, n, monkeypatch):
+    """OXM_LL_TMA=1 selects the TMA-staged low-pass kernel (ll_tma_kernel, n <= 2;
+    frames whose rows are 16-byte multiples); these sizes leave partial tiles and
+    odd level dimensions (per-level edge replication) at the right and bottom.
+    Its outputs must match the oracle exactly as the default kernel's do."""
+    monkeypatch.setenv("OXM_LL_TMA", "1")
     frames = np.stack([synth.phantom_rgb_f32(H, W, s, sensitivity, basis) for s in (31,)])
     _engine_vs_oracle(cuda, sensitivity, basis, frames, n)
+    bad = torch.ones((1, 64, 64, 3), device=cuda)
+    bad[0, 63, 62, 2] = float("inf")
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2))
+    with pytest.raises(ox.ArgumentError):
+        eng.run(bad)
 
 
 def test_engine_cfg2_stereo_pair(cuda, sensitivity, basis):
