@@ -335,10 +335,24 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   auto load = [&](int sl, int64_t i) {
     int f = 1;
     if constexpr (TAIL) f = io.fits[i];
+    // every load is issued before any is used (the hand-over state is the
+    // fp32 xh or, after a hand-over at fit #1, x_init): one memory round
+    // trip per refill instead of two (fits, then the x it selects)
+    double yv[3], xi[3];
+    float xf[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      ycol(sl, k) = kYSoa ? io.y[k * io.n + i] : io.y[3 * i + k];
-      x[sl][k] = f > 1 ? (double)io.xh[k * io.n + i] : io.xinit[k * io.n + i];
+      yv[k] = kYSoa ? io.y[k * io.n + i] : io.y[3 * i + k];
+      xi[k] = io.xinit[k * io.n + i];
+      if constexpr (TAIL) xf[k] = io.xh[k * io.n + i];
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      ycol(sl, k) = yv[k];
+      if constexpr (TAIL)
+        x[sl][k] = f > 1 ? (double)xf[k] : xi[k];
+      else
+        x[sl][k] = xi[k];
     }
     nfit[sl] = f;
     mode[sl] = f <= 1 ? 0 : 2;
