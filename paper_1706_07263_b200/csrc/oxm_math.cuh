@@ -96,8 +96,11 @@ __device__ __forceinline__ double exp_scaled(const double zs, const MathSmem& t)
   const double p = q * rs;  // exp(rs ln2/256) - 1
   const double T = t.expt[k & 255];
   const double res = fma(T, p, T);
-  const int m = k >> 8;  // floor(k / 256)
-  return __hiloint2double(__double2hiint(res) + (m << 20), __double2loint(res));
+  // hi word += floor(k / 256) << 20, as one arithmetic shift + one IMAD
+  int m, hi;
+  asm("shr.s32 %0, %1, 8;" : "=r"(m) : "r"(k));
+  asm("mad.lo.s32 %0, %1, 1048576, %2;" : "=r"(hi) : "r"(m), "r"(__double2hiint(res)));
+  return __hiloint2double(hi, __double2loint(res));
 }
 
 __device__ __forceinline__ double exp_tab(const double z, const MathSmem& t) { return exp_scaled(z * kExpScale, t); }
