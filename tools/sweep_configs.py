@@ -11,6 +11,7 @@ CONFIGS = [  # (name, H, W, n, frames per launch)
     ("cfg1 256x256 n=1", 256, 256, 1, 256),
     ("cfg2 576x720 n=1 (stereo pairs)", 576, 720, 1, 64),
     ("cfg3 1080x1920 n=2", 1080, 1920, 2, 32),
+    ("cfg3 1080x1920 n=2 (bench batch)", 1080, 1920, 2, 64),
     ("cfg5 2160x3840 n=3", 2160, 3840, 3, 8),
 ]
 
