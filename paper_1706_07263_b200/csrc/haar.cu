@@ -137,11 +137,18 @@ __global__ void __launch_bounds__(256) haar_fwd_kernel(const T* __restrict__ src
 // t = (ly TX + lx) 3 + c owns channel c of block (ly, lx).  Interior blocks
 // read their samples at compile-time offsets, blocks at the right / bottom
 // edge through clamped ones (the reference's replication, inside the tile).
+#ifndef OXM_K1_STAGES
+#define OXM_K1_STAGES 2
+#endif
+#ifndef OXM_K1_TY_DIV
+#define OXM_K1_TY_DIV 2
+#endif
 template <typename T, int NL>
 struct FwdTma {
   static constexpr int S = 1 << NL;
   static constexpr int TX = (sizeof(T) == 4 ? 64 : 32) / S;  // 768-byte input tile rows
-  static constexpr int TY = NL == 3 ? 8 : 128 / TX;
+  static constexpr int TY = NL == 3 ? 8 : 128 / OXM_K1_TY_DIV / TX;
+  static constexpr int kStages = OXM_K1_STAGES;  // input tiles in flight per CTA
   static constexpr int kThreads = 3 * TX * TY;
   static constexpr int kRowE = TX * S * 3;
   static constexpr int kRows = TY * S;
@@ -155,7 +162,7 @@ struct FwdTma {
     return o + q * out_elems(k);
   }
   static constexpr int kOutE = out_offset(NL + 1, 0);
-  static constexpr size_t kSmem = sizeof(T) * (size_t)(kTileE + kOutE);
+  static constexpr size_t kSmem = sizeof(T) * (size_t)(kStages * kTileE + kOutE);
 };
 
 struct FwdMaps {
@@ -170,24 +177,28 @@ __global__ void __launch_bounds__(FwdTma<T, NL>::kThreads) haar_fwd_tma_kernel(c
   using G = FwdTma<T, NL>;
   constexpr int S0 = G::S;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* const tile = reinterpret_cast<T*>(smem_raw);
-  T* const stage = tile + G::kTileE;
-  __shared__ __align__(8) uint64_t bar;
+  T* const tiles = reinterpret_cast<T*>(smem_raw);  // kStages input tiles
+  T* const stage = tiles + G::kStages * G::kTileE;   // output staging
+  __shared__ __align__(8) uint64_t bar[G::kStages];
   const int tid = threadIdx.x;
   const int ntiles = tiles_x * tiles_y;
   const int H0 = (int)g.h[0], W0 = (int)g.w[0];
   if (tid == 0) {
-    mbar_init(&bar, 1);
+#pragma unroll
+    for (int b = 0; b < G::kStages; ++b) mbar_init(&bar[b], 1);
     mbar_fence_init();
   }
   __syncthreads();
-  auto issue = [&](int t) {
+  auto issue = [&](int t, int b) {
     if (t >= ntiles) return;
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
-    mbar_expect_tx(&bar, G::kTileBytes);
-    tma_load_2d(tile, &maps.in, tx * G::kRowE, ty * G::kRows, &bar);
+    mbar_expect_tx(&bar[b], G::kTileBytes);
+    tma_load_2d(tiles + b * G::kTileE, &maps.in, tx * G::kRowE, ty * G::kRows, &bar[b]);
   };
-  if (tid == 0) issue(blockIdx.x);
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < G::kStages; ++b) issue(blockIdx.x + b * gridDim.x, b);
+  }
   const int c = tid % 3, blk = tid / 3;
   const int ly = blk / G::TX, lx = blk - ly * G::TX;
   bool bad = false;
@@ -195,7 +206,9 @@ __global__ void __launch_bounds__(FwdTma<T, NL>::kThreads) haar_fwd_tma_kernel(c
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const int ty = t / tiles_x, tx = t - ty * tiles_x;
     const int I = ty * G::TY + ly, J = tx * G::TX + lx;
-    mbar_wait(&bar, it & 1);
+    const int buf = it % G::kStages;
+    mbar_wait(&bar[buf], (it / G::kStages) & 1);
+    const T* tile = tiles + buf * G::kTileE;
     T p[S0][S0];
     if (I * S0 + S0 <= H0 && J * S0 + S0 <= W0) {
       const T* q = tile + (ly * S0) * G::kRowE + lx * S0 * 3 + c;
@@ -218,7 +231,7 @@ __global__ void __launch_bounds__(FwdTma<T, NL>::kThreads) haar_fwd_tma_kernel(c
     __syncthreads();                        // input buffer consumed, staging buffer free
     if (tid == 0) {
       fence_proxy_async();
-      issue(t + gridDim.x);
+      issue(t + G::kStages * gridDim.x, buf);
     }
     const bool valid = I < (int)g.h[NL] && J < (int)g.w[NL];
 #pragma unroll
