@@ -311,11 +311,10 @@ bool launch_fwd_tma(const T* src, const FwdGeom& g, T* out, uint32_t* flags, cud
                         (uint64_t)(3 * g.w[k] * sizeof(T)), G::kRowE >> k, G::kRows >> k))
         return false;
   auto kern = haar_fwd_tma_kernel<T, NL>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem) != cudaSuccess)
-      return false;
-    attr_set = true;
+  // per launch (the attribute is per function and device; a host call of a few us)
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
   }
   const int tiles_x = (int)ceil_div(g.w[NL], G::TX), tiles_y = (int)ceil_div(g.h[NL], G::TY);
   int per_sm = 0;

@@ -394,11 +394,10 @@ bool launch_ll_tma_n(const DevOps& ops, const float* frames, int64_t batch, cons
                     G::kRows))
     return false;
   auto kern = ll_tma_kernel<NLV>;
-  static bool attr_set = false;  // per template instance; the attribute is per function
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem) != cudaSuccess)
-      return false;
-    attr_set = true;
+  // per launch (the attribute is per function and device; a host call of a few us)
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
   }
   const int tiles_x = (int)ceil_div(d.w[NLV], G::TX), tiles_y = (int)ceil_div(d.h[NLV], G::TY);
   const int64_t ntiles = batch * tiles_x * tiles_y;

@@ -195,8 +195,8 @@ def estimate_frame(
     # hybrid (outputs come straight from the kernels: no host-side re-validation)
     ops = _hybrid_operators(sensitivity, basis, cfg)
     out = hybrid_device(upload(frame.data[None], torch.float64, dev), ops, cfg.n_levels, cal)
-    cube = trusted_cube(grid, download(out["cube"][0]))
-    xs = download(out["x"][:, 0])
+    cube = trusted_cube(grid, _download_large(out["cube"][0]))
+    xs = _download_large(out["x"][:, 0])
     cmap = trusted_map(xs[0], xs[1], xs[2])
     if stats is not None:
         stats.update(bayes_coefficients=n_lp, tikhonov_coefficients=n_dir)
@@ -297,6 +297,29 @@ def _par_copy(pairs) -> None:
             jobs.append(_copy_pool().submit(np.copyto, dst[r : r + step], src[r : r + step]))
     for j in jobs:
         j.result()
+
+
+_STAGING: dict = {}
+
+
+def _download_large(t: torch.Tensor) -> np.ndarray:
+    """Device tensor -> fresh host array for the big drop-in outputs (a 1080p
+    cube is 431 MB): DMA into a cached pinned staging buffer, then a
+    row-parallel copy into the new array, instead of one pageable copy that
+    also faults in every destination page on a single thread."""
+    t = t.contiguous()
+    key = (t.numel(), t.dtype)
+    buf = _STAGING.get(key)
+    if buf is None:
+        _STAGING.clear()  # one staging buffer at a time (the largest recent shape)
+        buf = _STAGING[key] = torch.empty(t.numel(), dtype=t.dtype).pin_memory()
+    host = buf[: t.numel()].view(t.shape)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    src = host.numpy()
+    dst = np.empty(src.shape, dtype=src.dtype)
+    _par_copy([(dst, src)])
+    return dst
 
 
 class _SequenceRunner:
