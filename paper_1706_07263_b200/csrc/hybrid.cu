@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   }
   const float cal = (float)g.cal;
   const float thr = (float)ops.fallback_below;
-  bool any_fb = false;
+  unsigned fbmask = 0;  // bit 2r + c: pixel (row r, column c) takes the fp64 fallback
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int64_t p = (f * g.H + row0 + r) * g.W + col;
@@ -620,10 +620,8 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
       // fminf drops NaN operands, so a NaN band (non-finite input: flagged by the
       // low-pass kernel, and launch() callers must check the flags) is caught
       // through the fit sums it poisons instead
-      const bool nan0 = isnan(a0[r].x + a1[r].x), nan1 = two && isnan(a0[r].y + a1[r].y);
-      vmin[r][0] = nan0 ? -1.f : vmin[r][0];
-      vmin[r][1] = nan1 ? -1.f : vmin[r][1];
-      any_fb |= !(vmin[r][0] >= thr) || (two && !(vmin[r][1] >= thr));
+      if (!(vmin[r][0] >= thr) || isnan(a0[r].x + a1[r].x)) fbmask |= 1u << (2 * r);
+      if (two && (!(vmin[r][1] >= thr) || isnan(a0[r].y + a1[r].y))) fbmask |= 2u << (2 * r);
     }
   }
   // Cancellation guard: pixels with a band below fallback_below (~0.4% of
@@ -641,14 +639,9 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   // the schedule the spectrum is hi + lo (fp64 to 48 bits) and every pixel is
   // finished here.  (Band counts above 32 take each lane's extra bands from
   // the same rows.)
-  if (__any_sync(0xffffffffu, any_fb)) {
+  if (__any_sync(0xffffffffu, fbmask != 0)) {
     const int lane = threadIdx.x & 31;
-    unsigned mask = 0;
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        if (live && r < nrow && (c == 0 || two) && !(vmin[r][c] >= thr)) mask |= 1u << (2 * r + c);
+    unsigned mask = fbmask;
     if (fb.queued) {
       const unsigned nq = __reduce_add_sync(0xffffffffu, __popc(mask));
       if (lane == 0) atomicAdd(fb.queued, nq);

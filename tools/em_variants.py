@@ -16,9 +16,10 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
     "base": (),
-    "g64": ("OXM_FB_CTAS_PER_SM=64",),
-    "g16": ("OXM_FB_CTAS_PER_SM=16",),
-    "r64": ("OXM_LEAD_RESID64=1",),  # lead-in residual in fp64 (tools/lead_noise_study.py)
+    "tail4": ("OXM_TAIL_MIN_BLOCKS=4",),
+    "tail6": ("OXM_TAIL_MIN_BLOCKS=6",),
+    "px12": ("OXM_PX_MIN_BLOCKS=12",),
+    "px16": ("OXM_PX_MIN_BLOCKS=16",),
 }
 
 
