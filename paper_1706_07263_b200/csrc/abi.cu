@@ -22,6 +22,16 @@ namespace {
 // fp64 once rel <= 16 tol; redo in fp64 when a tail step has |rel/tol - 1| < 1%
 constexpr double kDefaultLeadRatio = 16.0;
 constexpr double kDefaultLeadGuard = 0.01;
+// The tail's first step redoes the lead-in's uncommitted fit from the fp32 state
+// itself, so its rel carries the hand-over noise undamped (~2.5e-6 |x| / (tol |x|)
+// = ~2.5% of tol; tools/em_flip_study.py found the K = 4 flips exactly there, at
+// rel/tol = 0.998 with the tail continuing): its guard band is 10x wider.
+constexpr double kDefaultFirstGuard = 0.10;
+
+void set_first_guard(DevOps& d, double g1) {
+  d.guard1_lo = (1.0 - g1) * (1.0 - g1) * d.rel_tol * d.rel_tol;
+  d.guard1_hi = (1.0 + g1) * (1.0 + g1) * d.rel_tol * d.rel_tol;
+}
 
 void set_em_lead(DevOps& d, double ratio, double guard, double exact_below) {
   d.exact_below = exact_below;
@@ -29,6 +39,7 @@ void set_em_lead(DevOps& d, double ratio, double guard, double exact_below) {
   d.lead_thr_f = ratio > 1.0 ? static_cast<float>(kt * kt) : 0.0f;
   d.guard_lo = (1.0 - guard) * (1.0 - guard) * d.rel_tol * d.rel_tol;
   d.guard_hi = (1.0 + guard) * (1.0 + guard) * d.rel_tol * d.rel_tol;
+  set_first_guard(d, kDefaultFirstGuard > guard ? kDefaultFirstGuard : guard);
 }
 }  // namespace
 
@@ -151,6 +162,12 @@ extern "C" int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, dou
   if (!ctx || !(ratio >= 0.0) || !(guard >= 0.0 && guard < 1.0) || !(exact_below >= 0.0)) return OXM_ERR_ARGUMENT;
   if (ratio > 1.0 && (ratio * ctx->ops.rel_tol >= 1.0 || guard <= 0.0)) return OXM_ERR_ARGUMENT;
   set_em_lead(ctx->ops, ratio, guard, exact_below);
+  return OXM_OK;
+}
+
+extern "C" int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1) {
+  if (!ctx || !(guard1 >= 0.0 && guard1 < 1.0)) return OXM_ERR_ARGUMENT;
+  set_first_guard(ctx->ops, guard1);
   return OXM_OK;
 }
 

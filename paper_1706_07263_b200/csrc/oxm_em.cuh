@@ -473,9 +473,12 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
           // first tail step redoes the lead-in's uncommitted fit from the fp32
           // state itself, so its decision sees that perturbation undamped: a
           // stop there is never trusted either (rare: rel must fall from
-          // > K tol to < tol in one fit)
-          restart = mode[sl] != 0 && ((dn2 > ops.guard_lo * xm2 && dn2 < ops.guard_hi * xm2) ||
-                                      nfit[sl] >= ops.max_iters || (mode[sl] == 2 && done));
+          // > K tol to < tol in one fit), and its guard band is wider
+          // (oxm_ctx_set_em_first_guard, default +-10%)
+          const bool first = mode[sl] == 2;
+          const double glo = first ? ops.guard1_lo : ops.guard_lo, ghi = first ? ops.guard1_hi : ops.guard_hi;
+          restart = mode[sl] != 0 && ((dn2 > glo * xm2 && dn2 < ghi * xm2) || nfit[sl] >= ops.max_iters ||
+                                      (first && done));
           mode[sl] = restart ? 0 : min(mode[sl], 1);
           if (restart) {
             done = false;
