@@ -110,10 +110,11 @@ OXM_API int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, double
  * because the lead-in's fp32 error is roughly absolute in x, so its relative
  * weight grows as |x| shrinks.  x_floor = 0 (default): plain relative test. */
 OXM_API int oxm_ctx_set_em_lead_floor(oxm_ctx* ctx, double x_floor);
-/* Guard band of the fp64 tail's FIRST step (the redo of the lead-in's
- * uncommitted fit, whose input carries the fp32 hand-over noise undamped):
- * |rel/rel_tol - 1| < guard1 there, or any stop there, redoes the coefficient
- * in fp64 from fit #1.  Default max(0.10, guard); oxm_ctx_set_em_lead resets it. */
+/* Guard band of the fp64 tail's first steps: tail step j (j = 1 is the redo of
+ * the lead-in's uncommitted fit, whose input carries the fp32 hand-over noise
+ * undamped) with |rel/rel_tol - 1| < max(guard, guard1 * 2^(1-j)), or any stop
+ * at j = 1, redoes the coefficient in fp64 from fit #1.  Default
+ * max(0.10, guard); oxm_ctx_set_em_lead resets it. */
 OXM_API int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1);
 
 /* ---- K1: multi-level Haar forward ---------------------------------------

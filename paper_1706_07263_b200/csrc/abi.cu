@@ -25,20 +25,18 @@ constexpr double kDefaultLeadGuard = 0.01;
 // The tail's first step redoes the lead-in's uncommitted fit from the fp32 state
 // itself, so its rel carries the hand-over noise undamped (~2.5e-6 |x| / (tol |x|)
 // = ~2.5% of tol; tools/em_flip_study.py found the K = 4 flips exactly there, at
-// rel/tol = 0.998 with the tail continuing): its guard band is 10x wider.
+// rel/tol = 0.998 with the tail continuing): its guard band is 10x wider, and the
+// band halves with every further tail step (the iteration contracts by <= 1/2 per
+// fit, so the hand-over noise in rel does too) down to the plain guard.
 constexpr double kDefaultFirstGuard = 0.10;
 
-void set_first_guard(DevOps& d, double g1) {
-  d.guard1_lo = (1.0 - g1) * (1.0 - g1) * d.rel_tol * d.rel_tol;
-  d.guard1_hi = (1.0 + g1) * (1.0 + g1) * d.rel_tol * d.rel_tol;
-}
+void set_first_guard(DevOps& d, double g1) { d.guard1 = g1; }
 
 void set_em_lead(DevOps& d, double ratio, double guard, double exact_below) {
   d.exact_below = exact_below;
   const double kt = ratio * d.rel_tol;
   d.lead_thr_f = ratio > 1.0 ? static_cast<float>(kt * kt) : 0.0f;
-  d.guard_lo = (1.0 - guard) * (1.0 - guard) * d.rel_tol * d.rel_tol;
-  d.guard_hi = (1.0 + guard) * (1.0 + guard) * d.rel_tol * d.rel_tol;
+  d.guard = guard;
   set_first_guard(d, kDefaultFirstGuard > guard ? kDefaultFirstGuard : guard);
 }
 }  // namespace

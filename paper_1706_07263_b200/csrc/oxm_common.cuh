@@ -35,8 +35,9 @@ struct DevOps {
   double rel_tol;
   double fallback_below;
   double exact_below;  // with the lead-in: fallback pixels with a band below this get their block's EM redone all-fp64
-  double guard_lo, guard_hi;  // ((1 -+ m) tol)^2: an fp64 tail step with rel/tol in (1-m, 1+m) redoes the coefficient
-  double guard1_lo, guard1_hi;  // the same for the tail's first step (its input still carries undamped fp32 noise)
+  // fp64 tail guard bands: tail step j (1 = the redo of the lead-in's uncommitted
+  // fit) with |rel/tol - 1| < max(guard, guard1 * 2^(1-j)) redoes its coefficient
+  double guard, guard1;
   double solve[kMaxBands][3];  // Tikhonov ridge inverse, unmix.py:53-65
   double fitm[3][kMaxBands];   // (xi^T xi)^-1 xi^T, bayes.py:102
   double xi[kMaxBands][3];     // chromophore basis, core.py:134-158

@@ -326,8 +326,8 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   int64_t idx[NS];
   int nfit[NS];
   // TAIL state per lane: 0 = exact (runs the coefficient from fit #1, no guard),
-  // 1 = continuing a hand-over (guarded), 2 = the next step is the fp64 redo of the
-  // lead-in's uncommitted fit
+  // j >= 1 = the next step is tail step j of a hand-over (j = 1: the fp64 redo of
+  // the lead-in's uncommitted fit), guarded by max(guard, guard1 2^(1-j))
   int mode[NS];
   unsigned wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats; < 2^32 per warp)
   double x[NS][3];
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
         x[sl][k] = xi[k];
     }
     nfit[sl] = f;
-    mode[sl] = f <= 1 ? 0 : 2;
+    mode[sl] = f <= 1 ? 0 : 1;
   };
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) {
@@ -473,13 +473,16 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
           // first tail step redoes the lead-in's uncommitted fit from the fp32
           // state itself, so its decision sees that perturbation undamped: a
           // stop there is never trusted either (rare: rel must fall from
-          // > K tol to < tol in one fit), and its guard band is wider
-          // (oxm_ctx_set_em_first_guard, default +-10%)
-          const bool first = mode[sl] == 2;
-          const double glo = first ? ops.guard1_lo : ops.guard_lo, ghi = first ? ops.guard1_hi : ops.guard_hi;
-          restart = mode[sl] != 0 && ((dn2 > glo * xm2 && dn2 < ghi * xm2) || nfit[sl] >= ops.max_iters ||
-                                      (first && done));
-          mode[sl] = restart ? 0 : min(mode[sl], 1);
+          // > K tol to < tol in one fit), and the guard band starts wider
+          // (oxm_ctx_set_em_first_guard, default +-10%) and halves per tail step
+          const int j = mode[sl];
+          if (j) {
+            // guard1 * 2^(1-j): the exponent field of 2^(1-j) is 1024 - j (j < 1000)
+            const double gj = fmax(ops.guard, ops.guard1 * __hiloint2double((1024 - min(j, 900)) << 20, 0));
+            const double lo = (1.0 - gj) * (1.0 - gj) * tol2, hi = (1.0 + gj) * (1.0 + gj) * tol2;
+            restart = (dn2 > lo * xm2 && dn2 < hi * xm2) || nfit[sl] >= ops.max_iters || (j == 1 && done);
+          }
+          mode[sl] = restart || !j ? 0 : j + 1;
           if (restart) {
             done = false;
             nfit[sl] = 1;
