@@ -112,10 +112,11 @@ OXM_API int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, double
 OXM_API int oxm_ctx_set_em_lead_floor(oxm_ctx* ctx, double x_floor);
 /* Guard band of the fp64 tail's first steps: tail step j (j = 1 is the redo of
  * the lead-in's uncommitted fit, whose input carries the fp32 hand-over noise
- * undamped) with |rel/rel_tol - 1| < max(guard, guard1 * 2^(1-j)), or any stop
- * at j = 1, redoes the coefficient in fp64 from fit #1.  Default
- * max(0.10, guard); oxm_ctx_set_em_lead resets it. */
-OXM_API int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1);
+ * undamped) with |rel/rel_tol - 1| < max(guard, guard1 * 2^(-(j-1) h)),
+ * h = halvings_per_step (>= 1; 64 = only the first step is widened), or any
+ * stop at j = 1, redoes the coefficient in fp64 from fit #1.  Default
+ * (max(0.10, guard), 2); oxm_ctx_set_em_lead resets it. */
+OXM_API int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1, int halvings_per_step);
 
 /* ---- K1: multi-level Haar forward ---------------------------------------
  * Replaces haar.forward (haar.py:120-142) incl. per-level edge replication

@@ -29,15 +29,19 @@ constexpr double kDefaultLeadGuard = 0.01;
 // band halves with every further tail step (the iteration contracts by <= 1/2 per
 // fit, so the hand-over noise in rel does too) down to the plain guard.
 constexpr double kDefaultFirstGuard = 0.10;
+constexpr int kDefaultGuardShift = 2;  // the band quarters per tail step (the measured contraction)
 
-void set_first_guard(DevOps& d, double g1) { d.guard1 = g1; }
+void set_first_guard(DevOps& d, double g1, int shift) {
+  d.guard1 = g1;
+  d.guard_shift = shift;
+}
 
 void set_em_lead(DevOps& d, double ratio, double guard, double exact_below) {
   d.exact_below = exact_below;
   const double kt = ratio * d.rel_tol;
   d.lead_thr_f = ratio > 1.0 ? static_cast<float>(kt * kt) : 0.0f;
   d.guard = guard;
-  set_first_guard(d, kDefaultFirstGuard > guard ? kDefaultFirstGuard : guard);
+  set_first_guard(d, kDefaultFirstGuard > guard ? kDefaultFirstGuard : guard, kDefaultGuardShift);
 }
 }  // namespace
 
@@ -163,9 +167,9 @@ extern "C" int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, dou
   return OXM_OK;
 }
 
-extern "C" int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1) {
-  if (!ctx || !(guard1 >= 0.0 && guard1 < 1.0)) return OXM_ERR_ARGUMENT;
-  set_first_guard(ctx->ops, guard1);
+extern "C" int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1, int halvings_per_step) {
+  if (!ctx || !(guard1 >= 0.0 && guard1 < 1.0) || halvings_per_step < 1) return OXM_ERR_ARGUMENT;
+  set_first_guard(ctx->ops, guard1, halvings_per_step > 64 ? 64 : halvings_per_step);
   return OXM_OK;
 }
 

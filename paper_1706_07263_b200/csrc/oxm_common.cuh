@@ -36,8 +36,10 @@ struct DevOps {
   double fallback_below;
   double exact_below;  // with the lead-in: fallback pixels with a band below this get their block's EM redone all-fp64
   // fp64 tail guard bands: tail step j (1 = the redo of the lead-in's uncommitted
-  // fit) with |rel/tol - 1| < max(guard, guard1 * 2^(1-j)) redoes its coefficient
+  // fit) with |rel/tol - 1| < max(guard, guard1 * 2^(-(j-1) guard_shift)) redoes
+  // its coefficient
   double guard, guard1;
+  int guard_shift;
   double solve[kMaxBands][3];  // Tikhonov ridge inverse, unmix.py:53-65
   double fitm[3][kMaxBands];   // (xi^T xi)^-1 xi^T, bayes.py:102
   double xi[kMaxBands][3];     // chromophore basis, core.py:134-158

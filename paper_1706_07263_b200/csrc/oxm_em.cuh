@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   int nfit[NS];
   // TAIL state per lane: 0 = exact (runs the coefficient from fit #1, no guard),
   // j >= 1 = the next step is tail step j of a hand-over (j = 1: the fp64 redo of
-  // the lead-in's uncommitted fit), guarded by max(guard, guard1 2^(1-j))
+  // the lead-in's uncommitted fit), guarded by max(guard, guard1 2^(-(j-1) shift))
   int mode[NS];
   unsigned wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats; < 2^32 per warp)
   double x[NS][3];
@@ -474,11 +474,12 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
           // state itself, so its decision sees that perturbation undamped: a
           // stop there is never trusted either (rare: rel must fall from
           // > K tol to < tol in one fit), and the guard band starts wider
-          // (oxm_ctx_set_em_first_guard, default +-10%) and halves per tail step
+          // (oxm_ctx_set_em_first_guard, default +-10%) and shrinks 4x per tail step
           const int j = mode[sl];
           if (j) {
-            // guard1 * 2^(1-j): the exponent field of 2^(1-j) is 1024 - j (j < 1000)
-            const double gj = fmax(ops.guard, ops.guard1 * __hiloint2double((1024 - min(j, 900)) << 20, 0));
+            // guard1 * 2^(-(j-1) shift): exponent field 1023 - (j-1) shift (clamped: 2^-900 ~ 0)
+            const int ex = min((j - 1) * ops.guard_shift, 900);
+            const double gj = fmax(ops.guard, ops.guard1 * __hiloint2double((1023 - ex) << 20, 0));
             const double lo = (1.0 - gj) * (1.0 - gj) * tol2, hi = (1.0 + gj) * (1.0 + gj) * tol2;
             restart = (dn2 > lo * xm2 && dn2 < hi * xm2) || nfit[sl] >= ops.max_iters || (j == 1 && done);
           }

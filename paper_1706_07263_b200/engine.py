@@ -77,7 +77,7 @@ class HybridMapEngine:
         fallback_below: float = DEFAULT_FALLBACK_BELOW,
         em_lead: tuple | None = DEFAULT_EM_LEAD,
     ):
-        """``em_lead``: (ratio, guard[, exact_below[, x_floor[, first_guard]]]) of the EM's fp32
+        """``em_lead``: (ratio, guard[, exact_below[, x_floor[, first_guard[, halvings]]]]) of the EM's fp32
         lead-in (oxm_ctx_set_em_lead: fp32 fits while rel > ratio * rel_tol, then
         fp64; fp64 redo of coefficients whose stop decision lands within
         ``guard`` of rel_tol; all-fp64 re-estimate of blocks holding a fallback
@@ -105,7 +105,9 @@ class HybridMapEngine:
             if len(lead) > 3:
                 _native.check(self._lib.oxm_ctx_set_em_lead_floor(self.ctx.handle, float(lead[3])), "em_lead_floor")
             if len(lead) > 4:
-                _native.check(self._lib.oxm_ctx_set_em_first_guard(self.ctx.handle, float(lead[4])), "em_first_guard")
+                shift = int(lead[5]) if len(lead) > 5 else 2
+                _native.check(self._lib.oxm_ctx_set_em_first_guard(self.ctx.handle, float(lead[4]), shift),
+                              "em_first_guard")
         self.em_lead = em_lead
         self._ws: torch.Tensor | None = None
 

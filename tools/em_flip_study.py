@@ -10,7 +10,7 @@ fp64 on the host with the oracle's operators (bayes.py:185-207) to record its
 decides whether a schedule knob (hand-over ratio K, x_floor) protects it.
 
     python tools/em_flip_study.py SEEDS FIRST_SEED [schedule ...]
-schedule = "K[:x_floor[:first_guard]]" (e.g. 16, 4, 4:60, 6:0:0.1); one JSON line per (seed,
+schedule = "K[:x_floor[:first_guard[:halvings]]]" (e.g. 16, 4, 4:60, 4:0:0.1:64); one JSON line per (seed,
 schedule) with flips, restarts and per-stage us/frame, then one per flip.
 """
 from __future__ import annotations
@@ -61,7 +61,7 @@ def main():
     engines = {"0": ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev, em_lead=None)}
     for sp in specs:
         p = [float(v) for v in sp.split(":")]
-        lead = (p[0], 0.01, 2e-3) + tuple(p[1:3])  # K[:x_floor[:first_guard]]
+        lead = (p[0], 0.01, 2e-3) + tuple(p[1:4])  # K[:x_floor[:first_guard[:halvings]]]
         engines[sp] = ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev, em_lead=lead)
     outs = {k: e.allocate(B, H, W, fits=True) for k, e in engines.items()}
     hL, wL = -(-H // 4), -(-W // 4)
