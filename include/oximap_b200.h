@@ -117,6 +117,12 @@ OXM_API int oxm_ctx_set_em_lead_floor(oxm_ctx* ctx, double x_floor);
  * stop at j = 1, redoes the coefficient in fp64 from fit #1.  Default
  * (max(0.10, guard), 2); oxm_ctx_set_em_lead resets it. */
 OXM_API int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1, int halvings_per_step);
+/* Diagnostics for tools/em_margin_study.py: device buffers of (n_coefficients x 24)
+ * entries; the fp64 EM kernels of later launches on this context record, for fit m
+ * of low-pass coefficient i, rel at rel[i * 24 + m] and the tail step index (0 =
+ * exact fp64 trajectory, j >= 1 = j-th step after the fp32 hand-over) at
+ * step[i * 24 + m].  NULL, NULL (default) turns it off. */
+OXM_API int oxm_ctx_set_em_debug_log(oxm_ctx* ctx, float* rel, uint8_t* step);
 
 /* ---- K1: multi-level Haar forward ---------------------------------------
  * Replaces haar.forward (haar.py:120-142) incl. per-level edge replication

@@ -73,6 +73,7 @@ _SIGNATURES = {
     "oxm_ctx_set_em_lead": (_i32, [_vp, _f64, _f64, _f64]),
     "oxm_ctx_set_em_lead_floor": (_i32, [_vp, _f64]),
     "oxm_ctx_set_em_first_guard": (_i32, [_vp, _f64, _i32]),
+    "oxm_ctx_set_em_debug_log": (_i32, [_vp, _vp, _vp]),
     "oxm_haar_layout": (_i32, [_i64, _i64, _i32, _vp, _vp]),
     "oxm_haar_forward_f32": (_i32, [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
     "oxm_haar_forward_f64": (_i32, [_vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),

@@ -173,6 +173,13 @@ extern "C" int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1, int halvi
   return OXM_OK;
 }
 
+extern "C" int oxm_ctx_set_em_debug_log(oxm_ctx* ctx, float* rel, uint8_t* step) {
+  if (!ctx || (!rel) != (!step)) return OXM_ERR_ARGUMENT;
+  ctx->ops.dbg_rel = rel;
+  ctx->ops.dbg_step = step;
+  return OXM_OK;
+}
+
 extern "C" int oxm_ctx_set_em_lead_floor(oxm_ctx* ctx, double x_floor) {
   if (!ctx || !(x_floor >= 0.0) || !(x_floor < 1e18)) return OXM_ERR_ARGUMENT;
   ctx->ops.lead_floor2_f = static_cast<float>(x_floor * x_floor);

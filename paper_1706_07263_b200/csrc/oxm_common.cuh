@@ -50,6 +50,11 @@ struct DevOps {
   // (L x 8 doubles, 64 B per band): code that indexes bands by lane reads
   // them with coalesced loads instead of serialised indexed constant loads
   const double* band_rows;
+  // diagnostics (oxm_ctx_set_em_debug_log, normally null): the persistent EM
+  // kernels record rel of every fit m of coefficient i at dbg_rel[i * 24 + m]
+  // and the tail step index j (0 = exact fp64 trajectory) at dbg_step[i * 24 + m]
+  float* dbg_rel;
+  uint8_t* dbg_step;
 };
 
 struct oxm_ctx_impl {

@@ -466,6 +466,12 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
                                      __dmul_rn(x[sl][2], x[sl][2]));
         const double xm2 = fmax(xn2, 1e-16);
         done = dn2 < tol2 * xm2 || nfit[sl] >= ops.max_iters;
+        if (ops.dbg_rel && nfit[sl] < 24) {
+          ops.dbg_rel[idx[sl] * 24 + nfit[sl]] = (float)sqrt(dn2 / xm2);
+          int j = 0;
+          if constexpr (TAIL) j = mode[sl];
+          ops.dbg_step[idx[sl] * 24 + nfit[sl]] = (uint8_t)min(j, 255);
+        }
         if constexpr (TAIL) {
           // the state still carries the lead-in's fp32 perturbation: a stop
           // decision near the threshold (or one forced by max_iters) is not
