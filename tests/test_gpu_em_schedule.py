@@ -199,3 +199,40 @@ def test_bench_configuration_vs_oracle(cuda, sensitivity, basis):
         assert np.all(np.abs(thb[b] - ref["thb"]) <= 1e-4 * np.abs(ref["thb"])), b
         ok = ~np.isnan(ref["so2"])
         assert np.max(np.abs(so2[b][ok] - ref["so2"][ok])) <= 1e-5, b
+
+
+def test_schedule_knobs_and_debug_log(cuda, sensitivity, basis):
+    """oxm_ctx_set_em_first_guard / _lead_floor validate their arguments; the
+    per-fit rel log of oxm_ctx_set_em_debug_log reproduces the stopping rule
+    (bayes.py:199-205): for every coefficient of the all-fp64 schedule, rel of
+    its last fit is < tol and every earlier logged rel is >= tol."""
+    from paper_1706_07263_b200.device import ptr
+
+    lib = _native.load()
+    ok, bad = _native.OXM_OK, _native.OXM_ERR_ARGUMENT
+    eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2), em_lead=None)
+    h = eng.ctx.handle
+    assert lib.oxm_ctx_set_em_first_guard(h, 0.1, 2) == ok
+    assert lib.oxm_ctx_set_em_first_guard(h, 1.5, 2) == bad
+    assert lib.oxm_ctx_set_em_first_guard(h, 0.1, 0) == bad
+    assert lib.oxm_ctx_set_em_lead_floor(h, 0.0) == ok
+    assert lib.oxm_ctx_set_em_lead_floor(h, -1.0) == bad
+    rgb = synth.phantom_rgb_f32(96, 128, 17, sensitivity, basis)
+    x = torch.from_numpy(rgb[None].astype(np.float32)).to(cuda)
+    nll = 24 * 32
+    rel = torch.zeros(nll * 24, dtype=torch.float32, device=cuda)
+    step = torch.zeros(nll * 24, dtype=torch.uint8, device=cuda)
+    assert lib.oxm_ctx_set_em_debug_log(h, ptr(rel), None) == bad
+    assert lib.oxm_ctx_set_em_debug_log(h, ptr(rel), ptr(step)) == ok
+    out = eng.run(x, fits=True)
+    torch.cuda.synchronize()
+    assert lib.oxm_ctx_set_em_debug_log(h, None, None) == ok
+    fits = out.fits.reshape(-1).cpu().numpy()
+    r = rel.reshape(nll, 24).cpu().numpy()
+    assert np.all(step.cpu().numpy() == 0)  # all-fp64: every fit is on the exact trajectory
+    for i in range(nll):
+        m = fits[i]
+        assert r[i, m] < 1e-4 * (1 + 1e-5), (i, m, r[i, m])
+        assert np.all(r[i, 2:m] >= 1e-4 * (1 - 1e-5)), (i, r[i, :m + 1])
+    ref = O.estimate_frame(rgb, sensitivity.c, basis.xi, n_levels=2, want_cube=False)
+    assert np.array_equal(out.fits[0].cpu().numpy(), ref["fits"])
