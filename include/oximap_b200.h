@@ -113,14 +113,16 @@ OXM_API int oxm_ctx_set_em_lead_floor(oxm_ctx* ctx, double x_floor);
 /* Guard band of the fp64 tail's first steps: tail step j (j = 1 is the redo of
  * the lead-in's uncommitted fit, whose input carries the fp32 hand-over noise
  * undamped) with |rel/rel_tol - 1| < max(guard, guard1 * 2^(-(j-1) h)),
- * h = halvings_per_step (>= 1; 64 = only the first step is widened), or any
+ * h = halvings_per_step (>= 1; 64 = only the first step is widened; from the
+ * third step on the band is max(guard, guard1 * 2^(-2h))), or any
  * stop at j = 1, redoes the coefficient in fp64 from fit #1.  Default
  * (max(0.10, guard), 2); oxm_ctx_set_em_lead resets it. */
 OXM_API int oxm_ctx_set_em_first_guard(oxm_ctx* ctx, double guard1, int halvings_per_step);
 /* Diagnostics for tools/em_margin_study.py: device buffers of (n_coefficients x 24)
  * entries; the fp64 EM kernels of later launches on this context record, for fit m
  * of low-pass coefficient i, rel at rel[i * 24 + m] and the tail step index (0 =
- * exact fp64 trajectory, j >= 1 = j-th step after the fp32 hand-over) at
+ * exact fp64 trajectory, j = 1, 2 = j-th step after the fp32 hand-over, 3 = a
+ * later one) at
  * step[i * 24 + m].  NULL, NULL (default) turns it off. */
 OXM_API int oxm_ctx_set_em_debug_log(oxm_ctx* ctx, float* rel, uint8_t* step);
 

@@ -34,6 +34,13 @@ constexpr int kDefaultGuardShift = 2;  // the band quarters per tail step (the m
 void set_first_guard(DevOps& d, double g1, int shift) {
   d.guard1 = g1;
   d.guard_shift = shift;
+  for (int k = 0; k < 3; ++k) {
+    // step j = k + 1; the last entry serves every later step, so it uses the
+    // larger of step 3's band and the floor (exact for shift >= 2 or g1 <= 4 guard)
+    const double gj = std::fmax(d.guard, g1 * std::ldexp(1.0, -k * shift));
+    d.band_lo[k] = (1.0 - gj) * (1.0 - gj) * d.rel_tol * d.rel_tol;
+    d.band_hi[k] = (1.0 + gj) * (1.0 + gj) * d.rel_tol * d.rel_tol;
+  }
 }
 
 void set_em_lead(DevOps& d, double ratio, double guard, double exact_below) {

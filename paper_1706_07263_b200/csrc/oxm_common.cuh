@@ -36,10 +36,12 @@ struct DevOps {
   double fallback_below;
   double exact_below;  // with the lead-in: fallback pixels with a band below this get their block's EM redone all-fp64
   // fp64 tail guard bands: tail step j (1 = the redo of the lead-in's uncommitted
-  // fit) with |rel/tol - 1| < max(guard, guard1 * 2^(-(j-1) guard_shift)) redoes
-  // its coefficient
+  // fit) with |rel/tol - 1| < g_j = max(guard, guard1 * 2^(-(j-1) guard_shift))
+  // redoes its coefficient; band_lo/hi[k] = ((1 -+ g_j) tol)^2 for j = 1, 2 and
+  // j >= 3 (g_j has reached guard by step 3 for every shift >= 2)
   double guard, guard1;
   int guard_shift;
+  double band_lo[3], band_hi[3];
   double solve[kMaxBands][3];  // Tikhonov ridge inverse, unmix.py:53-65
   double fitm[3][kMaxBands];   // (xi^T xi)^-1 xi^T, bayes.py:102
   double xi[kMaxBands][3];     // chromophore basis, core.py:134-158

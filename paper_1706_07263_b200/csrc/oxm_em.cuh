@@ -483,13 +483,11 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
           // (oxm_ctx_set_em_first_guard, default +-10%) and shrinks 4x per tail step
           const int j = mode[sl];
           if (j) {
-            // guard1 * 2^(-(j-1) shift): exponent field 1023 - (j-1) shift (clamped: 2^-900 ~ 0)
-            const int ex = min((j - 1) * ops.guard_shift, 900);
-            const double gj = fmax(ops.guard, ops.guard1 * __hiloint2double((1023 - ex) << 20, 0));
-            const double lo = (1.0 - gj) * (1.0 - gj) * tol2, hi = (1.0 + gj) * (1.0 + gj) * tol2;
+            const double lo = j == 1 ? ops.band_lo[0] : (j == 2 ? ops.band_lo[1] : ops.band_lo[2]);
+            const double hi = j == 1 ? ops.band_hi[0] : (j == 2 ? ops.band_hi[1] : ops.band_hi[2]);
             restart = (dn2 > lo * xm2 && dn2 < hi * xm2) || nfit[sl] >= ops.max_iters || (j == 1 && done);
           }
-          mode[sl] = restart || !j ? 0 : j + 1;
+          mode[sl] = restart || !j ? 0 : min(j + 1, 3);
           if (restart) {
             done = false;
             nfit[sl] = 1;

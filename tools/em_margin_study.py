@@ -7,7 +7,7 @@ perturbation directly: the all-fp64 schedule and the schedule under test run
 the same batch with oxm_ctx_set_em_debug_log on, which records rel of every
 fit of every low-pass coefficient (and, for the schedule, which tail step j
 after the hand-over made it; restarted coefficients are re-recorded as exact).
-For each tail step j the script reports the distribution of
+For each tail step j (3 = the third or a later one) the script reports the distribution of
 |rel_tail / rel_exact - 1| over all decisions, next to the guard band the
 schedule applies at that step (max(guard, guard1 2^(-(j-1) h))).
 
