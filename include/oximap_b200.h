@@ -104,12 +104,6 @@ OXM_API int oxm_ctx_destroy(oxm_ctx* ctx);
  * points are always all-fp64.  Not thread-safe against concurrent launches on
  * the same context. */
 OXM_API int oxm_ctx_set_em_lead(oxm_ctx* ctx, double ratio, double guard, double exact_below);
-/* Hand-over floor of the fp32 lead-in: fits stay in fp32 while
- * |dx| > ratio * rel_tol * max(|x|, x_floor) -- i.e. coefficients with
- * |x| < x_floor hand over at the larger relative step ratio * x_floor / |x|,
- * because the lead-in's fp32 error is roughly absolute in x, so its relative
- * weight grows as |x| shrinks.  x_floor = 0 (default): plain relative test. */
-OXM_API int oxm_ctx_set_em_lead_floor(oxm_ctx* ctx, double x_floor);
 /* Guard band of the fp64 tail's first steps: tail step j (j = 1 is the redo of
  * the lead-in's uncommitted fit, whose input carries the fp32 hand-over noise
  * undamped) with |rel/rel_tol - 1| < max(guard, guard1 * 2^(-(j-1) h)),

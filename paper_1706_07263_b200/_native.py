@@ -71,7 +71,6 @@ _SIGNATURES = {
     "oxm_ctx_create": (_i32, [_i32, ctypes.POINTER(Operators), ctypes.POINTER(_vp)]),
     "oxm_ctx_destroy": (_i32, [_vp]),
     "oxm_ctx_set_em_lead": (_i32, [_vp, _f64, _f64, _f64]),
-    "oxm_ctx_set_em_lead_floor": (_i32, [_vp, _f64]),
     "oxm_ctx_set_em_first_guard": (_i32, [_vp, _f64, _i32]),
     "oxm_ctx_set_em_debug_log": (_i32, [_vp, _vp, _vp]),
     "oxm_haar_layout": (_i32, [_i64, _i64, _i32, _vp, _vp]),

@@ -187,12 +187,6 @@ extern "C" int oxm_ctx_set_em_debug_log(oxm_ctx* ctx, float* rel, uint8_t* step)
   return OXM_OK;
 }
 
-extern "C" int oxm_ctx_set_em_lead_floor(oxm_ctx* ctx, double x_floor) {
-  if (!ctx || !(x_floor >= 0.0) || !(x_floor < 1e18)) return OXM_ERR_ARGUMENT;
-  ctx->ops.lead_floor2_f = static_cast<float>(x_floor * x_floor);
-  return OXM_OK;
-}
-
 extern "C" int oxm_ctx_destroy(oxm_ctx* ctx) {
   if (ctx && ctx->ops.band_rows) {
     DeviceGuard dg(ctx->device);

@@ -26,8 +26,7 @@ struct DevOps {
   float xl2_t[2][kMaxBands];  // -xi[:, 0:2]^T * log2(e): e = 2^(xl2 . x - log2(e) x2)
   float sens_f[3][kMaxBands];
   float gain_t[3][kMaxBands];  // gain^T
-  float lead_thr_f;  // (K tol)^2: fp32 steps continue while |dx|^2 > lead_thr max(|x|^2, lead_floor2_f); 0 = no lead-in
-  float lead_floor2_f;  // x_floor^2 of oxm_ctx_set_em_lead_floor (0: relative test)
+  float lead_thr_f;  // (K tol)^2: fp32 steps continue while |dx|^2 > lead_thr |x|^2; 0 = no lead-in
   float eps_f;
   int L;
   int max_iters;

@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
     if (idx >= 0) {
       const float d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
       const float dn2 = d0 * d0 + d1 * d1 + d2 * d2;
-      const float xn2 = fmaxf(x0 * x0 + x1 * x1 + x2 * x2, fmaxf(ops.lead_floor2_f, 1e-16f));
+      const float xn2 = fmaxf(x0 * x0 + x1 * x1 + x2 * x2, 1e-16f);
       // commit fit nfit+1 only when the reference surely continues after it;
       // NaN / inf (fp32 overflow) fail the test and hand over the last finite state
       if (dn2 > thr * xn2 && dn2 <= 3.0e38f && nfit + 1 < ops.max_iters) {

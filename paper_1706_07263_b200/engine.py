@@ -77,13 +77,12 @@ class HybridMapEngine:
         fallback_below: float = DEFAULT_FALLBACK_BELOW,
         em_lead: tuple | None = DEFAULT_EM_LEAD,
     ):
-        """``em_lead``: (ratio, guard[, exact_below[, x_floor[, first_guard[, halvings]]]]) of the EM's fp32
+        """``em_lead``: (ratio, guard[, exact_below[, first_guard[, halvings]]]) of the EM's fp32
         lead-in (oxm_ctx_set_em_lead: fp32 fits while rel > ratio * rel_tol, then
         fp64; fp64 redo of coefficients whose stop decision lands within
         ``guard`` of rel_tol; all-fp64 re-estimate of blocks holding a fallback
         pixel with a band below ``exact_below``, default ``fallback_below``;
-        oxm_ctx_set_em_lead_floor: |x| below ``x_floor`` hands over earlier;
-        oxm_ctx_set_em_first_guard: guard band of the tail's first step), or
+        oxm_ctx_set_em_first_guard: guard bands of the tail's first steps), or
         None for all-fp64 EM fits."""
         check_grids(sensitivity.grid, basis.grid)
         self.cfg = cfg if cfg is not None else PipelineConfig(mode="hybrid", n_levels=2)
@@ -103,10 +102,8 @@ class HybridMapEngine:
             _native.check(self._lib.oxm_ctx_set_em_lead(self.ctx.handle, float(ratio), float(guard), float(exact)),
                           "em_lead")
             if len(lead) > 3:
-                _native.check(self._lib.oxm_ctx_set_em_lead_floor(self.ctx.handle, float(lead[3])), "em_lead_floor")
-            if len(lead) > 4:
-                shift = int(lead[5]) if len(lead) > 5 else 2
-                _native.check(self._lib.oxm_ctx_set_em_first_guard(self.ctx.handle, float(lead[4]), shift),
+                shift = int(lead[4]) if len(lead) > 4 else 2
+                _native.check(self._lib.oxm_ctx_set_em_first_guard(self.ctx.handle, float(lead[3]), shift),
                               "em_first_guard")
         self.em_lead = em_lead
         self._ws: torch.Tensor | None = None

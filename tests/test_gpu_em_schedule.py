@@ -202,7 +202,7 @@ def test_bench_configuration_vs_oracle(cuda, sensitivity, basis):
 
 
 def test_schedule_knobs_and_debug_log(cuda, sensitivity, basis):
-    """oxm_ctx_set_em_first_guard / _lead_floor validate their arguments; the
+    """oxm_ctx_set_em_first_guard validates its arguments; the
     per-fit rel log of oxm_ctx_set_em_debug_log reproduces the stopping rule
     (bayes.py:199-205): for every coefficient of the all-fp64 schedule, rel of
     its last fit is < tol and every earlier logged rel is >= tol."""
@@ -215,8 +215,6 @@ def test_schedule_knobs_and_debug_log(cuda, sensitivity, basis):
     assert lib.oxm_ctx_set_em_first_guard(h, 0.1, 2) == ok
     assert lib.oxm_ctx_set_em_first_guard(h, 1.5, 2) == bad
     assert lib.oxm_ctx_set_em_first_guard(h, 0.1, 0) == bad
-    assert lib.oxm_ctx_set_em_lead_floor(h, 0.0) == ok
-    assert lib.oxm_ctx_set_em_lead_floor(h, -1.0) == bad
     rgb = synth.phantom_rgb_f32(96, 128, 17, sensitivity, basis)
     x = torch.from_numpy(rgb[None].astype(np.float32)).to(cuda)
     nll = 24 * 32

@@ -7,10 +7,11 @@ compared with the all-fp64 schedule's (which equal the oracle's: the GPU
 tests pin that).  For every mismatch ("flip") the coefficient is replayed in
 fp64 on the host with the oracle's operators (bayes.py:185-207) to record its
 |x|, fit count and the rel / tol values of its last decisions -- which is what
-decides whether a schedule knob (hand-over ratio K, x_floor) protects it.
+decides whether a schedule knob (hand-over ratio K, guard bands) protects it.
 
     python tools/em_flip_study.py SEEDS FIRST_SEED [schedule ...]
-schedule = "K[:x_floor[:first_guard[:halvings]]]" (e.g. 16, 4, 4:60, 4:0:0.1:64); one JSON line per (seed,
+schedule = "K[:first_guard[:halvings]]" (e.g. 16, 4, 4:0.1:64; round-2 runs used an
+extra x_floor field, since removed: "4:0:0.1:64"); one JSON line per (seed,
 schedule) with flips, restarts and per-stage us/frame, then one per flip.
 """
 from __future__ import annotations
@@ -61,7 +62,7 @@ def main():
     engines = {"0": ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev, em_lead=None)}
     for sp in specs:
         p = [float(v) for v in sp.split(":")]
-        lead = (p[0], 0.01, 2e-3) + tuple(p[1:4])  # K[:x_floor[:first_guard[:halvings]]]
+        lead = (p[0], 0.01, 2e-3) + tuple(p[1:3])  # K[:first_guard[:halvings]]
         engines[sp] = ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev, em_lead=lead)
     outs = {k: e.allocate(B, H, W, fits=True) for k, e in engines.items()}
     hL, wL = -(-H // 4), -(-W // 4)

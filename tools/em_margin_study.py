@@ -39,7 +39,7 @@ def main():
     sens, basis = bench.operators()
     ref = ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev, em_lead=None)
     sch = ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev,
-                             em_lead=(K, 0.01, 2e-3, 0.0, g1, h))
+                             em_lead=(K, 0.01, 2e-3, g1, h))
     nll = B * (-(-H // 4)) * (-(-W // 4))
     bufs = {}
     for name, eng in (("ref", ref), ("sch", sch)):
