@@ -626,74 +626,55 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
   }
   // Cancellation guard: pixels with a band below fallback_below (~0.4% of
   // textured pixels, but spread so that about half of all warps hold one or
-  // two) are recomputed in fp64 right here by their warp.  The warp's pending
-  // pixels are packed into a per-warp list in shared memory (prefix sum of the
-  // lanes' counts), then each half-warp takes every other entry: lane s of the
-  // half takes bands s and s + 16 (the block spectrum, the reference's eps
-  // clamp, a table log) and the three fit sums are reduced with xor shuffles
-  // inside the half (all 16 lanes end with the same bits).  The pixel's rgb,
-  // ybar and spectrum rows were just read by this warp, so they come from L1,
-  // not DRAM; the operators' band rows come from a 64-byte-per-band device
-  // copy, loaded once per warp.  With the EM precision schedule (fb.classify)
-  // a pixel with a band in [eps / 2, exact_below) is "sensitive" to the
-  // schedule's ~1e-8 spectrum deviation (see px_fallback_kernel): it is listed
-  // for the deferred pass and its block for the all-fp64 exact pass instead.
-  // Without the schedule the spectrum is hi + lo (fp64 to 48 bits) and every
-  // pixel is finished here.
+  // two) are recomputed in fp64 right here by their warp, one pixel per pass:
+  // lane l takes band l (the block spectrum, the reference's eps clamp, a
+  // table log) and the three fit sums are reduced with xor shuffles (every
+  // lane ends with the same bits).  The pixel's rgb, ybar and spectrum rows
+  // were just read by this warp, so they come from L1, not DRAM; the
+  // operators' band rows come from a 64-byte-per-band device copy, loaded
+  // once per warp.  With the EM precision schedule (fb.classify) a pixel with
+  // a band in [eps / 2, exact_below) is "sensitive" to the schedule's ~1e-8
+  // spectrum deviation (see px_fallback_kernel): it is listed for the
+  // deferred pass and its block for the all-fp64 exact pass instead.  Without
+  // the schedule the spectrum is hi + lo (fp64 to 48 bits) and every pixel is
+  // finished here.  (Band counts above 32 take each lane's extra bands from
+  // the same rows.)
   if (__any_sync(0xffffffffu, fbmask != 0)) {
-    __shared__ uint32_t pend[kPxThreads / 32][32 * 2 * R];  // (row << 24) | column, per warp
-    const int lane = threadIdx.x & 31, half = lane >> 4, sub = lane & 15;
-    uint32_t* lst = pend[threadIdx.x >> 5];
-    const unsigned cnt = __popc(fbmask);
-    unsigned incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
+    const int lane = threadIdx.x & 31;
+    unsigned mask = fbmask;
+    if (fb.queued) {
+      const unsigned nq = __reduce_add_sync(0xffffffffu, __popc(mask));
+      if (lane == 0) atomicAdd(fb.queued, nq);
     }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-    if (lane == 31 && fb.queued) atomicAdd(fb.queued, total);
-    unsigned pos = incl - cnt;
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int c = 0; c < 2; ++c)
-        if (fbmask & (1u << (2 * r + c))) lst[pos++] = ((uint32_t)r << 24) | (uint32_t)(col + c);
-    __syncwarp();  // the list, and every lane's fp32 map stores before the fp64 rewrites below
-    const unsigned hm = 0xffffu << (16 * half);
+    __syncwarp();  // every lane's fp32 map stores land before the fp64 rewrites below
     const double2* rows = reinterpret_cast<const double2*>(ops.band_rows);  // 4 double2 per band
-    double2 r01[2], r23[2], r45[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int l = sub + 16 * i;
-      r01[i] = r23[i] = r45[i] = make_double2(0.0, 0.0);
-      if (l < L) {
-        r01[i] = ldg(rows + 4 * l);
-        r23[i] = ldg(rows + 4 * l + 1);
-        r45[i] = ldg(rows + 4 * l + 2);
-      }
+    double2 r01 = make_double2(0.0, 0.0), r23 = r01, r45 = r01;
+    if (lane < L) {
+      r01 = ldg(rows + 4 * lane);
+      r23 = ldg(rows + 4 * lane + 1);
+      r45 = ldg(rows + 4 * lane + 2);
     }
     const double lo_b = 0.5 * ops.eps, hi_b = ops.exact_below, eps = ops.eps;
     const double2* logt = log_table_global();
-    const uint32_t W32 = (uint32_t)g.W, prow = (uint32_t)(f * g.H + row0);
+    const uint32_t W32 = (uint32_t)g.W, prow = (uint32_t)(f * g.H + row0), col32 = (uint32_t)col;
     const uint32_t frow = (uint32_t)((f * g.hL + by) * g.wL);
-    for (unsigned k = half; k < total; k += 2) {  // trip count uniform per half-warp
-      const uint32_t e = lst[k];
-      const uint32_t ocol = e & 0xffffffu;
-      const uint32_t p = (prow + (e >> 24)) * W32 + ocol;
+    for (;;) {
+      const unsigned m = __ballot_sync(0xffffffffu, mask != 0);
+      if (!m) break;
+      const int owner = __ffs(m) - 1;
+      const int bit = __shfl_sync(0xffffffffu, mask ? __ffs(mask) - 1 : 0, owner);
+      if (lane == owner) mask &= mask - 1;
+      const uint32_t ocol = __shfl_sync(0xffffffffu, col32, owner) + (uint32_t)(bit & 1);
+      const uint32_t p = (prow + (uint32_t)(bit >> 1)) * W32 + ocol;
       const uint32_t ob = frow + (ocol >> g.n);
       const double D0 = frames.at(3 * (int64_t)p) - ybar[ob];
       const double D1 = frames.at(3 * (int64_t)p + 1) - ybar[g.nll + ob];
       const double D2 = frames.at(3 * (int64_t)p + 2) - ybar[2 * g.nll + ob];
       double a0s = 0.0, a1s = 0.0, a2s = 0.0;
       bool sens = false;
-      for (int i = 0, l = sub; l < L; ++i, l += 16) {
-        double2 q01, q23, q45;
-        if (i < 2) {
-          q01 = i ? r01[1] : r01[0];
-          q23 = i ? r23[1] : r23[0];
-          q45 = i ? r45[1] : r45[0];
-        } else {  // band counts above 32 (generic-L builds)
+      for (int l = lane; l < L; l += 32) {
+        double2 q01 = r01, q23 = r23, q45 = r45;
+        if (l >= 32) {
           q01 = ldg(rows + 4 * l);
           q23 = ldg(rows + 4 * l + 1);
           q45 = ldg(rows + 4 * l + 2);
@@ -707,8 +688,8 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
         a1s = fma(q45.x, lg, a1s);
         a2s = fma(q45.y, lg, a2s);
       }
-      if (__any_sync(hm, sens)) {  // defer: the exact pass re-estimates its block all-fp64
-        if (sub == 0) {
+      if (__any_sync(0xffffffffu, sens)) {  // defer: the exact pass re-estimates its block all-fp64
+        if (lane == owner) {
           fb.list[atomicAdd(fb.count, 1u)] = p;
           unsigned* word = reinterpret_cast<unsigned*>(fb.blkflag + (ob & ~3u));
           const unsigned bitm = 1u << (8 * (ob & 3u));
@@ -717,12 +698,12 @@ __global__ void __launch_bounds__(kPxThreads, OXM_PX_MIN_BLOCKS) px_f32_kernel(c
         continue;
       }
 #pragma unroll
-      for (int o = 8; o > 0; o >>= 1) {
-        a0s += __shfl_xor_sync(hm, a0s, o);
-        a1s += __shfl_xor_sync(hm, a1s, o);
-        a2s += __shfl_xor_sync(hm, a2s, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        a0s += __shfl_xor_sync(0xffffffffu, a0s, o);
+        a1s += __shfl_xor_sync(0xffffffffu, a1s, o);
+        a2s += __shfl_xor_sync(0xffffffffu, a2s, o);
       }
-      if (sub == 0) {  // overwrites the fp32 stores of this pixel (ordered by the __syncwarp above)
+      if (lane == owner) {
         const float xo = (float)(-a0s * g.cal), xd = (float)(-a1s * g.cal);
         const float co = fmaxf(xo, 0.f);
         const float t = co + fmaxf(xd, 0.f);
