@@ -229,11 +229,13 @@ def test_engine_planes_match_fp64(cuda, golden, sensitivity, basis):
 
 
 # ---------------------------------------------------------------- less-travelled paths
-def test_engine_generic_band_count(cuda):
-    """Fused path with L != 26 (runtime-L kernels) against the oracle."""
+@pytest.mark.parametrize("step,count", [(9.0, 31), (6.5, 40)])
+def test_engine_generic_band_count(cuda, step, count):
+    """Fused path with L != 26 (runtime-L kernels; L = 40 > 32 also exercises the
+    in-warp fp64 fallback's extra bands per lane) against the oracle."""
     from paper_1706_07263_b200 import WavelengthGrid, fixtures
 
-    grid = WavelengthGrid(440.0, 9.0, 31)
+    grid = WavelengthGrid(440.0, step, count)
     sens, bas = fixtures.default_sensitivity(grid), fixtures.default_basis(grid)
     frames = np.stack([synth.phantom_rgb_f32(48, 40, s, sens, bas) for s in (3, 4)])
     _engine_vs_oracle(cuda, sens, bas, frames, 2)
