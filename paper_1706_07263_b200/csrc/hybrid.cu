@@ -135,42 +135,98 @@ __global__ void __launch_bounds__(kLlThreads) ll_kernel(const __grid_constant__ 
   bool neg = false;
   double yv[3];
   double ll[3];
-  // fp32 frames, 2 levels, a block whose 4 x 4 pixels are all inside the frame
-  // (no edge replication at either level) and 16-byte aligned rows: the four
-  // 12-float rows as three float4s each instead of 48 strided scalars; same
-  // fp64 adds in the same order as LowPass<>
+  // fp32 frames, n <= 3 levels, a block whose 2^n x 2^n pixels are all inside
+  // the frame (no edge replication at any level) and 16-byte aligned rows: the
+  // block's rows as float4 (n >= 2) / float2 (n = 1) loads instead of 3 4^n
+  // strided scalars, the same fp64 adds in the same order as LowPass<> (level by
+  // level, window by window; n = 3 streams two level-0 rows at a time).  A
+  // sample is non-finite iff the fp64 low-pass sum over its block is (fp32
+  // inputs cannot overflow fp64): 3 compares instead of one per sample.
   bool fast = false;
-  if constexpr (NLV == 2 && Src::kF32 && std::is_same<Src, PlainSrc<float>>::value) {
-    fast = ((reinterpret_cast<uintptr_t>(frames.p) & 15) == 0) && (d.w[0] & 3) == 0 && 4 * by + 4 <= d.h[0] &&
-           4 * bx + 4 <= d.w[0];
+  if constexpr (Src::kF32 && std::is_same<Src, PlainSrc<float>>::value && NLV <= 3) {
+    constexpr int S = 1 << NLV;
+    fast = ((reinterpret_cast<uintptr_t>(frames.p) & 15) == 0) && (d.w[0] & 3) == 0 && S * by + S <= d.h[0] &&
+           S * bx + S <= d.w[0];
     if (fast) {
-      float px[4][12];
+      const float* blk = frames.p + base + ((S * by) * d.w[0] + S * bx) * 3;
+      const int64_t rowf = d.w[0] * 3;
+      auto win = [](double a, double b2, double cc, double dd) {
+        return 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b2), cc), dd);
+      };
+      if constexpr (NLV == 1) {
+        float px[2][6];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        const float4* rp = reinterpret_cast<const float4*>(frames.p + base + ((4 * by + r) * d.w[0] + 4 * bx) * 3);
+        for (int r = 0; r < 2; ++r)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const float4 v = ldg(rp + q);
-          px[r][4 * q] = v.x;
-          px[r][4 * q + 1] = v.y;
-          px[r][4 * q + 2] = v.z;
-          px[r][4 * q + 3] = v.w;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        double l1[2][2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const double a = px[2 * i][(2 * j) * 3 + c], b2 = px[2 * i][(2 * j + 1) * 3 + c];
-            const double cc = px[2 * i + 1][(2 * j) * 3 + c], dd = px[2 * i + 1][(2 * j + 1) * 3 + c];
-            bad |= !isfinite(a) || !isfinite(b2) || !isfinite(cc) || !isfinite(dd);
-            l1[i][j] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(a, b2), cc), dd);
+          for (int q = 0; q < 3; ++q) {
+            const float2 v = ldg(reinterpret_cast<const float2*>(blk + r * rowf) + q);
+            px[r][2 * q] = v.x;
+            px[r][2 * q + 1] = v.y;
           }
-        ll[c] = 0.5 * __dadd_rn(__dadd_rn(__dadd_rn(l1[0][0], l1[0][1]), l1[1][0]), l1[1][1]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ll[c] = win(px[0][c], px[0][3 + c], px[1][c], px[1][3 + c]);
+      } else if constexpr (NLV == 2) {
+        float px[4][12];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4* rp = reinterpret_cast<const float4*>(blk + r * rowf);
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const float4 v = ldg(rp + q);
+            px[r][4 * q] = v.x;
+            px[r][4 * q + 1] = v.y;
+            px[r][4 * q + 2] = v.z;
+            px[r][4 * q + 3] = v.w;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          double l1[2][2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              l1[i][j] = win(px[2 * i][6 * j + c], px[2 * i][6 * j + 3 + c], px[2 * i + 1][6 * j + c],
+                             px[2 * i + 1][6 * j + 3 + c]);
+          ll[c] = win(l1[0][0], l1[0][1], l1[1][0], l1[1][1]);
+        }
+      } else {
+        double l2[2][2][3];
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+          double l1[2][4][3];
+#pragma unroll
+          for (int i1 = 0; i1 < 2; ++i1) {
+            float px[2][24];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const float4* rp = reinterpret_cast<const float4*>(blk + (4 * i2 + 2 * i1 + r) * rowf);
+#pragma unroll
+              for (int q = 0; q < 6; ++q) {
+                const float4 v = ldg(rp + q);
+                px[r][4 * q] = v.x;
+                px[r][4 * q + 1] = v.y;
+                px[r][4 * q + 2] = v.z;
+                px[r][4 * q + 3] = v.w;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                l1[i1][j][c] = win(px[0][6 * j + c], px[0][6 * j + 3 + c], px[1][6 * j + c], px[1][6 * j + 3 + c]);
+          }
+#pragma unroll
+          for (int j2 = 0; j2 < 2; ++j2)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              l2[i2][j2][c] = win(l1[0][2 * j2][c], l1[0][2 * j2 + 1][c], l1[1][2 * j2][c], l1[1][2 * j2 + 1][c]);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ll[c] = win(l2[0][0][c], l2[0][1][c], l2[1][0][c], l2[1][1][c]);
       }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) bad |= !isfinite(ll[c]);
     }
   }
 #pragma unroll
