@@ -13,6 +13,7 @@ CONFIGS = [  # (name, H, W, n, frames per launch)
     ("cfg3 1080x1920 n=2", 1080, 1920, 2, 32),
     ("cfg3 1080x1920 n=2 (bench batch)", 1080, 1920, 2, 64),
     ("cfg5 2160x3840 n=3", 2160, 3840, 3, 8),
+    ("cfg5 2160x3840 n=3 (batches of 32)", 2160, 3840, 3, 32),
 ]
 
 
