@@ -8,6 +8,7 @@
 // Both are HBM-bound streaming kernels: each CTA moves a contiguous slab of
 // (n, L) rows through shared memory so every global access is coalesced.
 #include "oxm_common.cuh"
+#include "oxm_tma.cuh"
 
 namespace oxm {
 namespace {
@@ -56,22 +57,40 @@ __global__ void __launch_bounds__(kRows) unmix_kernel(const __grid_constant__ Ma
 // KL > 0: band count fixed at compile time (staging index math by constant
 // division, band loop unrolled); KL == 0: generic L.  32-bit index math
 // inside a CTA slab (cnt * L <= kRows * kMaxBands).
-template <typename T, int KL>
+// BULK: the CTA's slab of kRows x L values is contiguous in global memory and
+// arrives by one cp.async.bulk (TMA) copy into shared memory (row stride L);
+// otherwise (partial last slab, unaligned cube) per-thread coalesced loads fill
+// rows of odd stride L | 1.
+template <typename T, int KL, bool BULK>
 __global__ void __launch_bounds__(kRows) fit_kernel(const __grid_constant__ DevOps ops, const T* __restrict__ cube,
                                                     int64_t n, double cal, T* __restrict__ hbo, T* __restrict__ hb,
                                                     T* __restrict__ off) {
-  extern __shared__ unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   T* stage = reinterpret_cast<T*>(smem_raw);
+  __shared__ __align__(8) uint64_t bar;
   const int L = KL > 0 ? KL : ops.L;
-  const int LS = L | 1;  // odd row stride: conflict-free per-thread row walks
   const int64_t base = (int64_t)blockIdx.x * kRows;
   const int cnt = (int)min64(kRows, n - base);
   const T* src = cube + base * L;
-  for (int k = threadIdx.x; k < cnt * L; k += kRows) {
-    const int r = k / L, l = k - r * L;
-    stage[r * LS + l] = ldg(src + k);
+  int LS;
+  if constexpr (BULK) {
+    LS = L;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar, 1);
+      mbar_fence_init();
+      mbar_expect_tx(&bar, (uint32_t)(sizeof(T) * kRows * L));
+      bulk_load_1d(stage, src, (uint32_t)(sizeof(T) * kRows * L), &bar);
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    mbar_wait(&bar, 0);
+  } else {
+    LS = L | 1;  // odd row stride: conflict-free per-thread row walks
+    for (int k = threadIdx.x; k < cnt * L; k += kRows) {
+      const int r = k / L, l = k - r * L;
+      stage[r * LS + l] = ldg(src + k);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   if ((int)threadIdx.x >= cnt) return;
   const T* row = stage + threadIdx.x * LS;
   T x0, x1, x2;
@@ -149,10 +168,31 @@ int fit_impl(const oxm_ctx* ctx, const T* cube, int64_t n, double cal, T* hbo, T
   if (!ctx || n < 0 || (n > 0 && !cube)) return OXM_ERR_ARGUMENT;
   if (n == 0) return OXM_OK;
   DeviceGuard dg(ctx->device);
-  const size_t smem = sizeof(T) * kRows * (ctx->ops.L | 1);
-  auto kern = ctx->ops.L == 26 ? fit_kernel<T, 26> : fit_kernel<T, 0>;
-  if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  kern<<<grid_1d(n, kRows), kRows, smem, s>>>(ctx->ops, cube, n, cal, hbo, hb, off);
+  const int L = ctx->ops.L;
+  const size_t smem = sizeof(T) * kRows * (L | 1);
+  const int64_t full = n / kRows;  // CTAs with a whole slab
+  // whole slabs by bulk copy when every slab start is 16-byte aligned
+  const bool bulk = (reinterpret_cast<uintptr_t>(cube) & 15) == 0 && (sizeof(T) * kRows * L) % 16 == 0 && full > 0;
+  auto launch = [&](auto kern, int64_t first, int64_t cnt) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int64_t off_px = first * kRows;
+    kern<<<(unsigned)cnt, kRows, smem, s>>>(ctx->ops, cube + off_px * L, n - off_px, cal, hbo ? hbo + off_px : nullptr,
+                                            hb ? hb + off_px : nullptr, off ? off + off_px : nullptr);
+  };
+  if (bulk) {
+    if (L == 26)
+      launch(fit_kernel<T, 26, true>, 0, full);
+    else
+      launch(fit_kernel<T, 0, true>, 0, full);
+  }
+  const int64_t first = bulk ? full : 0;
+  const int64_t rest = (int64_t)grid_1d(n - first * kRows, kRows);
+  if (n > first * kRows) {
+    if (L == 26)
+      launch(fit_kernel<T, 26, false>, first, rest);
+    else
+      launch(fit_kernel<T, 0, false>, first, rest);
+  }
   return check_launch("fit");
 }
 
