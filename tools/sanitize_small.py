@@ -20,6 +20,21 @@ def main():
     for shape, n in [((37, 23, 3), 2), ((9, 15), 5), ((64, 48, 26), 4)]:
         img = rng.normal(size=shape)
         assert np.max(np.abs(ox.inverse(ox.forward(img, n)) - img)) < 1e-12
+    # TMA paths: K1 tiles in/out (3-channel planes with 16-byte rows, fp32 and fp64,
+    # partial tiles), K5 bulk-copied slabs (>= 128 pixels), the TMA low-pass kernel
+    from paper_1706_07263_b200.haar import pyramid_device
+
+    for dt in (torch.float32, torch.float64):
+        pyramid_device(torch.from_numpy(rng.uniform(0, 1, (70, 100, 3))).to("cuda", dt), 2)
+        pyramid_device(torch.from_numpy(rng.uniform(0, 1, (37, 36, 3))).to("cuda", dt), 3)
+    ox.fit_concentration(rng.uniform(0.1, 1, (300, 26)), basis)
+    import os
+
+    os.environ["OXM_LL_TMA"] = "1"
+    for n in (1, 2):
+        e = ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n))
+        e.run(torch.from_numpy(synth.phantom_rgb_f32(46, 68, 3, sens, basis)[None].astype(np.float32)).cuda())
+    os.environ["OXM_LL_TMA"] = "0"
     op = ox.TikhonovOperator.from_relative(sens, 1e-3)
     ox.tikhonov_unmix(rng.uniform(0, 1, (100, 3)), op)
     ox.estimate_lowpass(ox.LowPassBlock(rng.uniform(0.1, 1, (5, 7, 3)), 2.0), sens, basis, ox.BayesConfig(), op)
