@@ -33,15 +33,12 @@ __device__ __forceinline__ float dot3<float>(const Mat3& M, int l, float y0, flo
   return fmaf(M.mf[l][2], y2, fmaf(M.mf[l][1], y1, M.mf[l][0] * y0));
 }
 
-// BULK: whole slabs, in and out 16-byte aligned -- the CTA's kRows x L output
-// rows leave shared memory as one cp.async.bulk store (TMA) instead of
-// per-thread stores; otherwise per-thread coalesced stores.
-template <typename T, bool BULK>
+template <typename T>
 __global__ void __launch_bounds__(kRows) unmix_kernel(const __grid_constant__ Mat3 M, const T* __restrict__ rgb,
                                                       int64_t n, T* __restrict__ out) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ unsigned char smem_raw[];
   T* sin = reinterpret_cast<T*>(smem_raw);  // [kRows*3]
-  T* sout = sin + kRows * 3;                // [kRows*L] (16-byte aligned: kRows * 3 * sizeof(T) is)
+  T* sout = sin + kRows * 3;                // [kRows*L]
   const int L = M.L;
   const int64_t base = (int64_t)blockIdx.x * kRows;
   const int64_t cnt = min64(kRows, n - base);
@@ -52,19 +49,9 @@ __global__ void __launch_bounds__(kRows) unmix_kernel(const __grid_constant__ Ma
     T* row = sout + threadIdx.x * L;
     for (int l = 0; l < L; ++l) row[l] = dot3<T>(M, l, y0, y1, y2);
   }
+  __syncthreads();
   T* dst = out + base * L;
-  if constexpr (BULK) {
-    fence_proxy_async();  // this thread's staging writes -> visible to the bulk copy
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      bulk_store_1d(dst, sout, (uint32_t)(sizeof(T) * kRows * L));
-      tma_store_commit();
-      tma_store_wait_read0();  // shared memory must outlive the copy's reads
-    }
-  } else {
-    __syncthreads();
-    for (int64_t k = threadIdx.x; k < cnt * L; k += kRows) dst[k] = sout[k];
-  }
+  for (int64_t k = threadIdx.x; k < cnt * L; k += kRows) dst[k] = sout[k];
 }
 
 // KL > 0: band count fixed at compile time (staging index math by constant
@@ -170,16 +157,9 @@ int unmix_impl(int L, const double* matrix, const T* rgb, int64_t n, T* out, cud
   if (n < 0 || (n > 0 && (!rgb || !out))) return OXM_ERR_ARGUMENT;
   if (n == 0) return OXM_OK;
   const size_t smem = sizeof(T) * kRows * (3 + L);
-  const int64_t full = n / kRows;
-  const bool bulk = (reinterpret_cast<uintptr_t>(out) & 15) == 0 && (sizeof(T) * kRows * L) % 16 == 0 && full > 0;
-  auto launch = [&](auto kern, int64_t first, int64_t ctas) {
-    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int64_t o = first * kRows;
-    kern<<<(unsigned)ctas, kRows, smem, s>>>(M, rgb + 3 * o, n - o, out + o * L);
-  };
-  if (bulk) launch(unmix_kernel<T, true>, 0, full);
-  const int64_t first = bulk ? full : 0;
-  if (n > first * kRows) launch(unmix_kernel<T, false>, first, (int64_t)grid_1d(n - first * kRows, kRows));
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(unmix_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  unmix_kernel<T><<<grid_1d(n, kRows), kRows, smem, s>>>(M, rgb, n, out);
   return check_launch("unmix");
 }
 
