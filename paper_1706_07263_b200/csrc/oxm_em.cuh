@@ -136,7 +136,11 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, unsigned v, 
   if (ctr && lane == 0 && t) atomicAdd(ctr, (unsigned long long)t);
 }
 
-constexpr int kEmThreads = 128;
+constexpr int kEmThreads = 128;  // fp32 lead-in and fit #1 kernels
+#ifndef OXM_PERS_THREADS
+#define OXM_PERS_THREADS 128
+#endif
+constexpr int kPersThreads = OXM_PERS_THREADS;  // persistent fp64 EM kernel (tail / all-fp64 / exact list)
 constexpr int kEmUnroll = OXM_EM_UNROLL;
 constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 #ifndef OXM_EM_CHUNK
@@ -288,7 +292,7 @@ __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol
 // whose rel lands within the guard band around tol, or a tail that runs into
 // max_iters, restarts its coefficient from fit #1 in exact fp64 mode.
 template <int KL, SpecOut OUT, bool TAIL = false>
-__global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_EM_MIN_BLOCKS)
+__global__ void __launch_bounds__(kPersThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_EM_MIN_BLOCKS)
     em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
   constexpr int NS = kEmSlots;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -297,9 +301,9 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   // e of slot s, band l at e[(s * (L + kEmColExtra) + l) * es]: one column per
   // thread and slot, then r (rows L..L+2) and the coefficient index (row L+3)
   double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem) + sizeof(ops.gain)) + threadIdx.x;
-  constexpr int es = kEmThreads + 1;  // band stride of the e columns (see em_smem_bytes)
+  constexpr int es = kPersThreads + 1;  // band stride of the e columns (see em_smem_bytes)
   load_math_tables(mt);
-  for (int i = threadIdx.x; i < kMaxBands * 3; i += kEmThreads) gsm[i / 3][i % 3] = ops.gain[i / 3][i % 3];
+  for (int i = threadIdx.x; i < kMaxBands * 3; i += kPersThreads) gsm[i / 3][i % 3] = ops.gain[i / 3][i % 3];
   __syncthreads();
 
   const int L = BandCount<KL>::get(ops);
@@ -307,10 +311,10 @@ __global__ void __launch_bounds__(kEmThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_E
   const double tol2 = ops.rel_tol * ops.rel_tol;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
-  const int64_t warp = ((int64_t)blockIdx.x * kEmThreads + threadIdx.x) >> 5;
+  const int64_t warp = ((int64_t)blockIdx.x * kPersThreads + threadIdx.x) >> 5;
   // first 32 * NS coefficients statically per warp, then kEmChunk-sized
   // chunks from io.work, numbered from dyn0
-  const int64_t dyn0 = (int64_t)gridDim.x * kEmThreads * NS;
+  const int64_t dyn0 = (int64_t)gridDim.x * kPersThreads * NS;
   // positions 0 .. count are coefficients, or indices into io.sel
   const int64_t count = io.sel ? (int64_t)*io.sel_count : io.n;
   auto coef = [&](int64_t pos) -> int64_t { return io.sel ? (int64_t)io.sel[pos] : pos; };
@@ -680,13 +684,14 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
 }
 
 template <typename K>
-inline int persistent_blocks(K kern, size_t smem, int reserve, int64_t need_ctas, int64_t& blocks) {
+inline int persistent_blocks(K kern, size_t smem, int reserve, int64_t need_ctas, int64_t& blocks,
+                             int threads = kEmThreads) {
   cudaError_t err = cudaSuccess;
   if (smem > 48 * 1024) err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 0, per_sm = 0;
   if (err == cudaSuccess) err = cudaGetDevice(&dev);
   if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kEmThreads, smem);
+  if (err == cudaSuccess) err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (err != cudaSuccess) {
     set_last_error("em launch configuration", err);
     return OXM_ERR_CUDA;
@@ -712,8 +717,9 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s, cudaEvent_t spl
   if (!io.fits || !io.xinit || !io.work) return OXM_ERR_ARGUMENT;
   if ((io.y_soa != 0) != (OUT != SpecOut::kAosF64)) return OXM_ERR_ARGUMENT;  // see em_persistent_kernel
   io.fmt = OUT;
-  const size_t smem = em_smem_bytes(ops.L, kEmThreads);
+  const size_t smem = em_smem_bytes(ops.L, kPersThreads);
   const int64_t need = ceil_div(io.n, kEmThreads);
+  const int64_t need_p = ceil_div(io.n, kPersThreads);
   if (!io.xinit_ready || ops.max_iters <= 1) {
     em_init_kernel<KL><<<(unsigned)need, kEmThreads, 0, s>>>(ops, io);
     int st0 = check_launch("em_init");
@@ -735,14 +741,14 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s, cudaEvent_t spl
   if constexpr (kCanLead) {
     if (lead) {
       auto tk = em_persistent_kernel<KL, OUT, true>;
-      if ((st = persistent_blocks(tk, smem, io.em_reserve, ceil_div(need, kEmSlots), blocks))) return st;
-      tk<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
+      if ((st = persistent_blocks(tk, smem, io.em_reserve, ceil_div(need_p, kEmSlots), blocks, kPersThreads))) return st;
+      tk<<<(unsigned)blocks, kPersThreads, smem, s>>>(ops, io);
       return check_launch("em_tail");
     }
   }
   auto kern = em_persistent_kernel<KL, OUT>;
-  if ((st = persistent_blocks(kern, smem, io.em_reserve, ceil_div(need, kEmSlots), blocks))) return st;
-  kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
+  if ((st = persistent_blocks(kern, smem, io.em_reserve, ceil_div(need_p, kEmSlots), blocks, kPersThreads))) return st;
+  kern<<<(unsigned)blocks, kPersThreads, smem, s>>>(ops, io);
   return check_launch("em_persistent");
 }
 
@@ -902,10 +908,11 @@ inline int launch_em_selected(const DevOps& ops, EmIO io, cudaStream_t s) {
   // 8 frames 10.3 vs 10.6 us/frame, 32 frames 5.6 vs 5.2, 64 frames 5.3 vs 4.7).
   if (io.n >= kExactSeqMinN) {
     io.stats = nullptr;
-    const size_t smem = em_smem_bytes(ops.L, kEmThreads);
+    const size_t smem = em_smem_bytes(ops.L, kPersThreads);
     auto kern = em_persistent_kernel<KL, OUT>;
-    if ((st = persistent_blocks(kern, smem, 0, ceil_div(ceil_div(io.n, kEmThreads), kEmSlots), blocks))) return st;
-    kern<<<(unsigned)blocks, kEmThreads, smem, s>>>(ops, io);
+    if ((st = persistent_blocks(kern, smem, 0, ceil_div(ceil_div(io.n, kPersThreads), kEmSlots), blocks, kPersThreads)))
+      return st;
+    kern<<<(unsigned)blocks, kPersThreads, smem, s>>>(ops, io);
   } else {
     auto kern = em_exact_kernel<KL, OUT>;
     if ((st = persistent_blocks(kern, 0, 0, ceil_div(io.n * kXLanes, kXThreads), blocks))) return st;

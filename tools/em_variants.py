@@ -16,10 +16,8 @@ ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
     "base": (),
-    "tail4": ("OXM_TAIL_MIN_BLOCKS=4",),
-    "tail6": ("OXM_TAIL_MIN_BLOCKS=6",),
-    "px12": ("OXM_PX_MIN_BLOCKS=12",),
-    "px16": ("OXM_PX_MIN_BLOCKS=16",),
+    "p640": ("OXM_PERS_THREADS=640", "OXM_TAIL_MIN_BLOCKS=1", "OXM_EM_MIN_BLOCKS=1"),
+    "p320": ("OXM_PERS_THREADS=320", "OXM_TAIL_MIN_BLOCKS=2", "OXM_EM_MIN_BLOCKS=2"),
 }
 
 
