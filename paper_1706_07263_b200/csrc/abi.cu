@@ -99,6 +99,7 @@ extern "C" int oxm_ctx_create(int device, const oxm_operators* o, oxm_ctx** out)
   d.max_iters = o->max_iters;
   d.eps = o->epsilon;
   d.rel_tol = o->rel_tol;
+  d.rel_tol2 = o->rel_tol * o->rel_tol;
   // the fp32 map path skips the eps clamp, which is only sound when every
   // band below the fallback threshold is recomputed in fp64
   d.fallback_below = o->fallback_below > o->epsilon ? o->fallback_below : o->epsilon;

@@ -32,6 +32,7 @@ struct DevOps {
   int max_iters;
   double eps;
   double rel_tol;
+  double rel_tol2;  // rel_tol^2 (the stopping test compares squared norms)
   double fallback_below;
   double exact_below;  // with the lead-in: fallback pixels with a band below this get their block's EM redone all-fp64
   // fp64 tail guard bands: tail step j (1 = the redo of the lead-in's uncommitted

@@ -37,9 +37,6 @@
 #ifndef OXM_EM_UNROLL_B
 #define OXM_EM_UNROLL_B 26
 #endif
-#ifndef OXM_EM_SLOTS
-#define OXM_EM_SLOTS 1
-#endif
 #ifndef OXM_TAIL_MIN_BLOCKS
 #define OXM_TAIL_MIN_BLOCKS 5
 #endif
@@ -61,18 +58,33 @@ struct BandCount {
   __device__ __forceinline__ static int get(const DevOps& ops) { return KL > 0 ? KL : ops.L; }
 };
 
-// Dynamic shared memory of an EM kernel: tables + G + one e column per thread.
-// The e columns are strided by threads + 1 doubles per band: rows (one band,
+// Dynamic shared memory of the persistent EM kernel: tables + one column per
+// thread.  Columns are strided by threads + 1 doubles per row: rows (one band,
 // consecutive threads) stay contiguous, and a column (one thread, consecutive
 // bands -- write_spectra) walks the banks instead of hitting one bank 26 times.
-// Each column also holds, after its L bands, the lane's residual r (3 rows)
-// and coefficient index (1 row), which write_spectra reads for the owner lane,
-// and its data y (3 rows: kept in shared memory rather than six registers).
-constexpr int kEmColExtra = 7;  // r (3), coefficient index (1), y (3)
+// Rows of a lane's column after its L bands (which hold e during phase A and
+// s = max(e + G r, eps) after phase B):
+constexpr int kColOff = 0;     // element offset of the lane's output row (write_spectra)
+constexpr int kColY = 1;       // 3 rows: y of the current coefficient
+constexpr int kColPre = 4;     // 6 rows: cp.async prefetch of the next coefficient --
+                               // y (3 rows), then x_init (3 rows; all-fp64 kernel) or
+                               // {xh0, xh1}, {xh2, fits} (tail)
+constexpr int kEmColExtra = 10;
 __host__ __device__ constexpr size_t em_smem_bytes(int L, int threads) {
-  return sizeof(MathSmem) + sizeof(double) * 3 * kMaxBands +
-         sizeof(double) * (size_t)(L + kEmColExtra) * (size_t)(threads + 1) * OXM_EM_SLOTS;
+  return sizeof(MathSmem) + sizeof(double) * (size_t)(L + kEmColExtra) * (size_t)(threads + 1);
 }
+
+// cp.async (LDGSTS) of 4 / 8 bytes into shared memory, and its group waits
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
 // Persistent, warp-refilled EM kernel.
@@ -147,7 +159,6 @@ constexpr int kEmUnrollB = OXM_EM_UNROLL_B;
 #define OXM_EM_CHUNK 32
 #endif
 constexpr int kEmChunk = OXM_EM_CHUNK;  // coefficients per dynamically assigned chunk (>= 32)
-constexpr int kEmSlots = OXM_EM_SLOTS;  // coefficients in flight per thread
 #ifndef OXM_LEAD_RESID64
 #define OXM_LEAD_RESID64 0  // 1: the lead-in's residual y - C e in fp64 (tools/lead_noise_study.py)
 #endif
@@ -226,63 +237,53 @@ __global__ void __launch_bounds__(kEmThreads) em_init_kernel(const __grid_consta
   }
 }
 
-// Write the spectra s = max(e + G r, eps) of the lanes in `done_mask` to
-// global memory.  Phase B does not store s (it only needs log s), so it is
-// re-formed here from the lane's e column in shared memory (column j holds
-// lane j's e_l at ecol0[l * es + j]), its residual r and a shared-memory copy
-// of G -- the same FMAs in the same order, so the same bits.  One finished
-// lane at a time (warp-uniform loop, ~2.4 lanes finish per step); lane l
-// handles band l, so every row is stored with coalesced accesses.  The
-// owner's r and index come from rows L..L+3 of its column (broadcast reads).
-// Slo == nullptr: hi parts only (the exact-block pass rewrites every block
-// whose lo parts the fp64 pixel fallback reads).
-template <int KL, SpecOut OUT>
-__device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol0, int es, int L, unsigned done_mask,
-                                              int lane, const double (*gsm)[3], double eps) {
+// Write the spectra s of the lanes in `done_mask` to global memory.  Phase B
+// leaves each lane's s_l in its shared-memory column (column j holds lane j's
+// s_l at c0[l * es + j]) and row kColOff holds the element offset of its
+// output row, so a finished lane costs the warp one broadcast read of the
+// offset, one read of s per band and one coalesced store: one finished lane
+// at a time (warp-uniform loop, ~9 lanes finish per tail step), lane l
+// storing band l.  lterm is the lane's part of the element index (band
+// `lane` of the output row).  Slo == nullptr: hi parts only (the exact-block
+// pass rewrites every block whose lo parts the fp64 pixel fallback reads).
+template <SpecOut OUT>
+__device__ __forceinline__ void store_band(const EmIO& io, int64_t e, double s) {
+  if constexpr (OUT == SpecOut::kAosF32HiLo) {
+    const float h = __double2float_rn(s);
+    io.Shi[e] = h;
+    if (io.Slo) io.Slo[e] = __double2float_rn(s - (double)h);
+  } else {
+    io.S[e] = s;
+  }
+}
+
+template <SpecOut OUT>
+__device__ __forceinline__ int64_t out_row_offset(const EmIO& io, int64_t i, int L) {
+  return OUT == SpecOut::kSoaF64 ? i : (OUT == SpecOut::kAosF64 ? i * L : i * io.Lp);
+}
+
+template <SpecOut OUT>
+__device__ __forceinline__ int64_t out_band_term(const EmIO& io, int l) {
+  return OUT == SpecOut::kSoaF64 ? (int64_t)l * io.n : (int64_t)l;
+}
+
+template <int KL, SpecOut OUT, int es>
+__device__ __forceinline__ void write_spectra(const EmIO& io, const double* c0, int L, unsigned done_mask, int lane,
+                                              int64_t lterm) {
   if constexpr (KL > 0 && KL <= 32) {
-    // one band per lane: its G row is loaded once for all finished lanes
-    if (lane >= KL) {  // lanes without a band only take part in the shuffle-free loop
-      return;
-    }
-    const double g0 = gsm[lane][0], g1 = gsm[lane][1], g2 = gsm[lane][2];
+    if (lane >= KL) return;  // lanes without a band
     while (done_mask) {
       const int owner = __ffs(done_mask) - 1;
       done_mask &= done_mask - 1;
-      const double* oc = ecol0 + owner;
-      const double q0 = oc[KL * es], q1 = oc[(KL + 1) * es], q2 = oc[(KL + 2) * es];
-      const int64_t oidx = __double_as_longlong(oc[(KL + 3) * es]);
-      const double s = clamp_eps(fma(g2, q2, fma(g1, q1, fma(g0, q0, ecol0[lane * es + owner]))), eps);
-      if constexpr (OUT == SpecOut::kSoaF64) {
-        io.S[(int64_t)lane * io.n + oidx] = s;
-      } else if constexpr (OUT == SpecOut::kAosF64) {
-        io.S[oidx * KL + lane] = s;
-      } else {
-        const float h = __double2float_rn(s);
-        io.Shi[oidx * io.Lp + lane] = h;
-        if (io.Slo) io.Slo[oidx * io.Lp + lane] = __double2float_rn(s - (double)h);
-      }
+      const int64_t off = __double_as_longlong(c0[(KL + kColOff) * es + owner]);
+      store_band<OUT>(io, off + lterm, c0[lane * es + owner]);
     }
-    return;
-  }
-  while (done_mask) {
-    const int owner = __ffs(done_mask) - 1;
-    done_mask &= done_mask - 1;
-    const double* oc = ecol0 + owner;
-    const double q0 = oc[L * es], q1 = oc[(L + 1) * es], q2 = oc[(L + 2) * es];
-    const int64_t oidx = __double_as_longlong(oc[(L + 3) * es]);
-#pragma unroll
-    for (int l = lane; l < BandCount<KL>::kMax; l += 32) {
-      if (KL == 0 && l >= L) break;
-      const double s = clamp_eps(fma(gsm[l][2], q2, fma(gsm[l][1], q1, fma(gsm[l][0], q0, ecol0[l * es + owner]))), eps);
-      if constexpr (OUT == SpecOut::kSoaF64) {
-        io.S[(int64_t)l * io.n + oidx] = s;
-      } else if constexpr (OUT == SpecOut::kAosF64) {
-        io.S[oidx * L + l] = s;
-      } else {
-        const float h = __double2float_rn(s);
-        io.Shi[oidx * io.Lp + l] = h;
-        if (io.Slo) io.Slo[oidx * io.Lp + l] = __double2float_rn(s - (double)h);
-      }
+  } else {
+    while (done_mask) {
+      const int owner = __ffs(done_mask) - 1;
+      done_mask &= done_mask - 1;
+      const int64_t off = __double_as_longlong(c0[(L + kColOff) * es + owner]);
+      for (int l = lane; l < L; l += 32) store_band<OUT>(io, off + out_band_term<OUT>(io, l), c0[l * es + owner]);
     }
   }
 }
@@ -291,92 +292,106 @@ __device__ __forceinline__ void write_spectra(const EmIO& io, const double* ecol
 // when the hand-over came at fit #1; fit count from io.fits).  A tail step
 // whose rel lands within the guard band around tol, or a tail that runs into
 // max_iters, restarts its coefficient from fit #1 in exact fp64 mode.
+//
+// Refill: every lane holds its next coefficient's data (y and x_init, or the
+// hand-over state) in the prefetch rows of its column, copied there by
+// cp.async when the lane took its current one; a lane whose coefficient
+// converges takes the prefetched one (its copies landed steps ago) and issues
+// the next prefetch.  Invariant: a lane without a current coefficient
+// (idx < 0) has none prefetched either (pidx < 0).
 template <int KL, SpecOut OUT, bool TAIL = false>
 __global__ void __launch_bounds__(kPersThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM_EM_MIN_BLOCKS)
     em_persistent_kernel(const __grid_constant__ DevOps ops, EmIO io) {
-  constexpr int NS = kEmSlots;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MathSmem& mt = *reinterpret_cast<MathSmem*>(smem_raw);
-  double(*gsm)[3] = reinterpret_cast<double(*)[3]>(smem_raw + sizeof(MathSmem));  // G, for write_spectra
-  // e of slot s, band l at e[(s * (L + kEmColExtra) + l) * es]: one column per
-  // thread and slot, then r (rows L..L+2) and the coefficient index (row L+3)
-  double* e = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem) + sizeof(ops.gain)) + threadIdx.x;
-  constexpr int es = kPersThreads + 1;  // band stride of the e columns (see em_smem_bytes)
+  constexpr int es = kPersThreads + 1;  // row stride of the columns (see em_smem_bytes)
+  double* const col = reinterpret_cast<double*>(smem_raw + sizeof(MathSmem)) + threadIdx.x;  // this lane's column
   load_math_tables(mt);
-  for (int i = threadIdx.x; i < kMaxBands * 3; i += kPersThreads) gsm[i / 3][i % 3] = ops.gain[i / 3][i % 3];
   __syncthreads();
 
   const int L = BandCount<KL>::get(ops);
+  double* const xrow = col + L * es;  // the rows after the bands
+  auto row = [&](int r) -> double& { return xrow[r * es]; };
   const double eps = ops.eps;
-  const double tol2 = ops.rel_tol * ops.rel_tol;
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t warp = ((int64_t)blockIdx.x * kPersThreads + threadIdx.x) >> 5;
-  // first 32 * NS coefficients statically per warp, then kEmChunk-sized
-  // chunks from io.work, numbered from dyn0
-  const int64_t dyn0 = (int64_t)gridDim.x * kPersThreads * NS;
+  // first 32 coefficients statically per warp, then kEmChunk-sized chunks
+  // from io.work, numbered from dyn0
+  const int64_t dyn0 = (int64_t)gridDim.x * kPersThreads;
   // positions 0 .. count are coefficients, or indices into io.sel
   const int64_t count = io.sel ? (int64_t)*io.sel_count : io.n;
   auto coef = [&](int64_t pos) -> int64_t { return io.sel ? (int64_t)io.sel[pos] : pos; };
-  int64_t next = warp * 32 * NS;                // next unassigned position of the current chunk
-  int64_t stop = min64(next + 32 * NS, count);  // end of the current chunk
+  int64_t next = warp * 32;               // next unassigned position of the current chunk
+  int64_t stop = min64(next + 32, count);  // end of the current chunk
   bool exhausted = false;
 
   if (ops.max_iters <= 1) return;  // fit #1 is the answer: written by em_init_kernel
 
   // y layout is fixed per output format (hybrid path: SoA; estimate_lowpass
-  // API: AoS), so the refill has no runtime branch for it
+  // API: AoS), so the prefetch has no runtime branch for it
   constexpr bool kYSoa = OUT != SpecOut::kAosF64;
-  int64_t idx[NS];
-  int nfit[NS];
-  // TAIL state per lane: 0 = exact (runs the coefficient from fit #1, no guard),
-  // j >= 1 = the next step is tail step j of a hand-over (j = 1: the fp64 redo of
-  // the lead-in's uncommitted fit), guarded by max(guard, guard1 2^(-(j-1) shift))
-  int mode[NS];
+  const int64_t lterm = out_band_term<OUT>(io, lane);
+  int64_t idx = -1, pidx = -1;
+  int nfit = 1;
+  // TAIL state: 0 = exact (runs the coefficient from fit #1, no guard), j >= 1 =
+  // the next step is tail step j of a hand-over (j = 1: the fp64 redo of the
+  // lead-in's uncommitted fit), guarded by max(guard, guard1 2^(-(j-1) shift))
+  int mode = 0;
   unsigned wsteps = 0, wrestarts = 0;  // TAIL work counters of this warp (io.stats; < 2^32 per warp)
-  double x[NS][3];
-  auto ycol = [&](int sl, int k) -> double& { return e[(sl * (L + kEmColExtra) + L + 4 + k) * es]; };
-  auto load = [&](int sl, int64_t i) {
-    int f = 1;
-    if constexpr (TAIL) f = io.fits[i];
-    // every load is issued before any is used (the hand-over state is the
-    // fp32 xh or, after a hand-over at fit #1, x_init): one memory round
-    // trip per refill instead of two (fits, then the x it selects)
-    double yv[3], xi[3];
-    float xf[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      yv[k] = kYSoa ? io.y[k * io.n + i] : io.y[3 * i + k];
-      xi[k] = io.xinit[k * io.n + i];
-      if constexpr (TAIL) xf[k] = io.xh[k * io.n + i];
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      ycol(sl, k) = yv[k];
-      if constexpr (TAIL)
-        x[sl][k] = f > 1 ? (double)xf[k] : xi[k];
-      else
-        x[sl][k] = xi[k];
-    }
-    nfit[sl] = f;
-    mode[sl] = f <= 1 ? 0 : 1;
-  };
-#pragma unroll
-  for (int sl = 0; sl < NS; ++sl) {
-    const int64_t i = next + 32 * sl + lane;
-    idx[sl] = i < stop ? coef(i) : -1;
-    nfit[sl] = 1;
-    mode[sl] = 0;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) ycol(sl, k) = x[sl][k] = 0.0;
-    if (idx[sl] >= 0) load(sl, idx[sl]);
-    e[(sl * (L + kEmColExtra) + L + 3) * es] = __longlong_as_double(idx[sl]);  // for write_spectra
-  }
-  next = stop;
+  double x0 = 0.0, x1 = 0.0, x2 = 0.0;
 
-  // refill the finished lanes (mask m) of slot sl: rest of the current chunk,
-  // then a new one
-  auto refill = [&](int sl, unsigned m, bool done) {
+  auto prefetch = [&](int64_t i) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cp_async8(&row(kColPre + k), kYSoa ? io.y + k * io.n + i : io.y + 3 * i + k);
+    if constexpr (TAIL) {
+      float* a = reinterpret_cast<float*>(&row(kColPre + 3));
+      float* b = reinterpret_cast<float*>(&row(kColPre + 4));
+      cp_async4(a, io.xh + i);
+      cp_async4(a + 1, io.xh + io.n + i);
+      cp_async4(b, io.xh + 2 * io.n + i);
+      cp_async4(b + 1, io.fits + i);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) cp_async8(&row(kColPre + 3 + k), io.xinit + k * io.n + i);
+    }
+    cp_async_commit();
+  };
+  // make the prefetched coefficient (pidx >= 0) the current one
+  auto take = [&]() {
+    cp_async_wait_all();
+    idx = pidx;
+    double yv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) yv[k] = row(kColPre + k);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) row(kColY + k) = yv[k];
+    if constexpr (TAIL) {
+      const float2 a = *reinterpret_cast<const float2*>(&row(kColPre + 3));
+      const float2 b = *reinterpret_cast<const float2*>(&row(kColPre + 4));
+      const int f = __float_as_int(b.y);
+      nfit = f;
+      mode = f <= 1 ? 0 : 1;
+      if (f > 1) {
+        x0 = a.x;
+        x1 = a.y;
+        x2 = b.x;
+      } else {  // hand-over at fit #1 (rare): exact fp64 from x_init
+        x0 = io.xinit[idx];
+        x1 = io.xinit[io.n + idx];
+        x2 = io.xinit[2 * io.n + idx];
+      }
+    } else {
+      x0 = row(kColPre + 3);
+      x1 = row(kColPre + 4);
+      x2 = row(kColPre + 5);
+      nfit = 1;
+      mode = 0;
+    }
+  };
+  // hand out the next positions to the lanes of mask m (warp-uniform call;
+  // `want`: this lane is in m): rest of the current chunk, then a new one
+  auto assign = [&](unsigned m, bool want) -> int64_t {
     const int need = __popc(m);
     const int64_t avail = stop - next;  // warp-uniform
     int64_t fresh = count, fresh_end = count;
@@ -387,13 +402,11 @@ __global__ void __launch_bounds__(kPersThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM
       fresh_end = min64(fresh + kEmChunk, count);
       exhausted = fresh >= count;
     }
-    if (done) {
+    int64_t got = -1;
+    if (want) {
       const int r = __popc(m & lt_mask);
-      const int64_t mine = r < avail ? next + r : fresh + (r - avail);
-      idx[sl] = mine < (r < avail ? stop : fresh_end) ? coef(mine) : -1;
-      nfit[sl] = 1;
-      mode[sl] = 0;
-      if (idx[sl] >= 0) load(sl, idx[sl]);
+      const int64_t pos = r < avail ? next + r : fresh + (r - avail);
+      got = pos < (r < avail ? stop : fresh_end) ? coef(pos) : -1;
     }
     if (avail < need) {
       next = fresh_end > fresh ? min64(fresh + (need - avail), fresh_end) : fresh_end;
@@ -401,131 +414,128 @@ __global__ void __launch_bounds__(kPersThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM
     } else {
       next += need;
     }
+    return got;
   };
 
-  auto any_active = [&]() {
-    bool a = false;
-#pragma unroll
-    for (int sl = 0; sl < NS; ++sl) a |= idx[sl] >= 0;
-    return __any_sync(0xffffffffu, a);
-  };
-
-  while (any_active()) {
-    if constexpr (TAIL) {
-#pragma unroll
-      for (int sl = 0; sl < NS; ++sl) wsteps += __popc(__ballot_sync(0xffffffffu, idx[sl] >= 0));
+  // start: the static chunk's coefficient is fetched and taken at once, then
+  // every lane that got one prefetches its next
+  pidx = assign(0xffffffffu, true);
+  if (pidx >= 0) {
+    prefetch(pidx);
+    take();
+    row(kColOff) = __longlong_as_double(out_row_offset<OUT>(io, idx, L));
+  }
+  pidx = -1;
+  {
+    const unsigned m = __ballot_sync(0xffffffffu, idx >= 0);
+    if (m) {
+      pidx = assign(m, idx >= 0);
+      if (pidx >= 0) prefetch(pidx);
     }
+  }
+
+  while (__any_sync(0xffffffffu, idx >= 0)) {
+    if constexpr (TAIL) wsteps += __popc(__ballot_sync(0xffffffffu, idx >= 0));
     // ---- phase A: expected spectrum e = exp(-xi x) and residual r = y - C e
-    double c[NS][3], x2s[NS];
-#pragma unroll
-    for (int sl = 0; sl < NS; ++sl) {
-      c[sl][0] = c[sl][1] = c[sl][2] = 0.0;
-      x2s[sl] = x[sl][2] * kExpScale;  // xi[:, 2] == 1 (core.py:152-153); xis = xi[:, 0:2] * kExpScale
-    }
+    double c0 = 0.0, c1 = 0.0, c2 = 0.0;
+    const double x2s = x2 * kExpScale;  // xi[:, 2] == 1 (core.py:152-153); xis = xi[:, 0:2] * kExpScale
 #pragma unroll(KL > 0 ? kEmUnroll : 2)
     for (int l = 0; l < L; ++l) {
-#pragma unroll
-      for (int sl = 0; sl < NS; ++sl) {
-        const double el = exp_scaled(-fma(ops.xis[l][0], x[sl][0], fma(ops.xis[l][1], x[sl][1], x2s[sl])), mt);
-        e[(sl * (L + kEmColExtra) + l) * es] = el;
-        c[sl][0] = fma(ops.sens[0][l], el, c[sl][0]);
-        c[sl][1] = fma(ops.sens[1][l], el, c[sl][1]);
-        c[sl][2] = fma(ops.sens[2][l], el, c[sl][2]);
-      }
+      const double el = exp_scaled(-fma(ops.xis[l][0], x0, fma(ops.xis[l][1], x1, x2s)), mt);
+      col[l * es] = el;
+      c0 = fma(ops.sens[0][l], el, c0);
+      c1 = fma(ops.sens[1][l], el, c1);
+      c2 = fma(ops.sens[2][l], el, c2);
     }
-    double r[NS][3], nn[NS][3];
-#pragma unroll
-    for (int sl = 0; sl < NS; ++sl)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        r[sl][k] = ycol(sl, k) - c[sl][k];
-        nn[sl][k] = 0.0;
-        e[(sl * (L + kEmColExtra) + L + k) * es] = r[sl][k];  // for write_spectra
-      }
-    // ---- phase B: s = max(e + G r, eps), Beer-Lambert fit of log s
-    // (s itself is not stored: write_spectra re-forms it for finished lanes)
+    const double r0 = row(kColY) - c0, r1 = row(kColY + 1) - c1, r2 = row(kColY + 2) - c2;
+    // ---- phase B: s = max(e + G r, eps) (kept in the column for
+    // write_spectra), Beer-Lambert fit of log s
+    double m0 = 0.0, m1 = 0.0, m2 = 0.0;
 #pragma unroll(KL > 0 ? kEmUnrollB : 2)
     for (int l = 0; l < L; ++l) {
-#pragma unroll
-      for (int sl = 0; sl < NS; ++sl) {
-        const double sv = clamp_eps(
-            fma(ops.gain[l][2], r[sl][2], fma(ops.gain[l][1], r[sl][1], fma(ops.gain[l][0], r[sl][0], e[(sl * (L + kEmColExtra) + l) * es]))),
-            eps);
-        const double lg = log_tab(sv, mt.logt);
-        nn[sl][0] = fma(ops.fitm[0][l], lg, nn[sl][0]);
-        nn[sl][1] = fma(ops.fitm[1][l], lg, nn[sl][1]);
-        nn[sl][2] = fma(ops.fitm[2][l], lg, nn[sl][2]);
-      }
+      const double sv = clamp_eps(fma(ops.gain[l][2], r2, fma(ops.gain[l][1], r1, fma(ops.gain[l][0], r0, col[l * es]))), eps);
+      col[l * es] = sv;
+      const double lg = log_tab(sv, mt.logt);
+      m0 = fma(ops.fitm[0][l], lg, m0);
+      m1 = fma(ops.fitm[1][l], lg, m1);
+      m2 = fma(ops.fitm[2][l], lg, m2);
     }
     // ---- bookkeeping: stopping rule of bayes.py:195-205, then write-out and refill
-#pragma unroll
-    for (int sl = 0; sl < NS; ++sl) {
-      const double n0 = -nn[sl][0], n1 = -nn[sl][1], n2 = -nn[sl][2];
-      bool done = false, restart = false;
-      if (idx[sl] >= 0) {
-        ++nfit[sl];
-        const double d0 = n0 - x[sl][0], d1 = n1 - x[sl][1], d2 = n2 - x[sl][2];
-        const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
-        const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x[sl][0], x[sl][0]), __dmul_rn(x[sl][1], x[sl][1])),
-                                     __dmul_rn(x[sl][2], x[sl][2]));
-        const double xm2 = fmax(xn2, 1e-16);
-        done = dn2 < tol2 * xm2 || nfit[sl] >= ops.max_iters;
-        if (ops.dbg_rel && nfit[sl] < 24) {
-          ops.dbg_rel[idx[sl] * 24 + nfit[sl]] = (float)sqrt(dn2 / xm2);
-          int j = 0;
-          if constexpr (TAIL) j = mode[sl];
-          ops.dbg_step[idx[sl] * 24 + nfit[sl]] = (uint8_t)min(j, 255);
+    const double n0 = -m0, n1 = -m1, n2 = -m2;
+    bool done = false, restart = false;
+    if (idx >= 0) {
+      ++nfit;
+      const double d0 = n0 - x0, d1 = n1 - x1, d2 = n2 - x2;
+      const double dn2 = __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
+      const double xn2 = __dadd_rn(__dadd_rn(__dmul_rn(x0, x0), __dmul_rn(x1, x1)), __dmul_rn(x2, x2));
+      const double xm2 = fmax(xn2, 1e-16);
+      done = dn2 < ops.rel_tol2 * xm2 || nfit >= ops.max_iters;
+      if (ops.dbg_rel && nfit < 24) {
+        ops.dbg_rel[idx * 24 + nfit] = (float)sqrt(dn2 / xm2);
+        ops.dbg_step[idx * 24 + nfit] = (uint8_t)min(TAIL ? mode : 0, 255);
+      }
+      if constexpr (TAIL) {
+        // the state still carries the lead-in's fp32 perturbation: a stop
+        // decision near the threshold (or one forced by max_iters) is not
+        // trusted -- redo the coefficient in exact fp64 from fit #1.  The
+        // first tail step redoes the lead-in's uncommitted fit from the fp32
+        // state itself, so its decision sees that perturbation undamped: a
+        // stop there is never trusted either (rare: rel must fall from
+        // > K tol to < tol in one fit), and the guard band starts wider
+        // (oxm_ctx_set_em_first_guard, default +-10%) and shrinks 4x per tail step
+        const int j = mode;
+        if (j) {
+          const double lo = j == 1 ? ops.band_lo[0] : (j == 2 ? ops.band_lo[1] : ops.band_lo[2]);
+          const double hi = j == 1 ? ops.band_hi[0] : (j == 2 ? ops.band_hi[1] : ops.band_hi[2]);
+          restart = (dn2 > lo * xm2 && dn2 < hi * xm2) || nfit >= ops.max_iters || (j == 1 && done);
         }
-        if constexpr (TAIL) {
-          // the state still carries the lead-in's fp32 perturbation: a stop
-          // decision near the threshold (or one forced by max_iters) is not
-          // trusted -- redo the coefficient in exact fp64 from fit #1.  The
-          // first tail step redoes the lead-in's uncommitted fit from the fp32
-          // state itself, so its decision sees that perturbation undamped: a
-          // stop there is never trusted either (rare: rel must fall from
-          // > K tol to < tol in one fit), and the guard band starts wider
-          // (oxm_ctx_set_em_first_guard, default +-10%) and shrinks 4x per tail step
-          const int j = mode[sl];
-          if (j) {
-            const double lo = j == 1 ? ops.band_lo[0] : (j == 2 ? ops.band_lo[1] : ops.band_lo[2]);
-            const double hi = j == 1 ? ops.band_hi[0] : (j == 2 ? ops.band_hi[1] : ops.band_hi[2]);
-            restart = (dn2 > lo * xm2 && dn2 < hi * xm2) || nfit[sl] >= ops.max_iters || (j == 1 && done);
-          }
-          mode[sl] = restart || !j ? 0 : min(j + 1, 3);
-          if (restart) {
-            done = false;
-            nfit[sl] = 1;
-          }
-        }
-        if (done) {
-          io.fits[idx[sl]] = nfit[sl];
-          if (io.x) {
-            io.x[3 * idx[sl]] = n0;
-            io.x[3 * idx[sl] + 1] = n1;
-            io.x[3 * idx[sl] + 2] = n2;
-          }
+        mode = restart || !j ? 0 : min(j + 1, 3);
+        if (restart) {
+          done = false;
+          nfit = 1;
         }
       }
-      if (TAIL && restart) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) x[sl][k] = io.xinit[k * io.n + idx[sl]];
-      } else {
-        x[sl][0] = n0;
-        x[sl][1] = n1;
-        x[sl][2] = n2;
+      if (done) {
+        io.fits[idx] = nfit;
+        if (io.x) {
+          io.x[3 * idx] = n0;
+          io.x[3 * idx + 1] = n1;
+          io.x[3 * idx + 2] = n2;
+        }
       }
-      if constexpr (TAIL) wrestarts += __popc(__ballot_sync(0xffffffffu, restart));
-      const unsigned m = __ballot_sync(0xffffffffu, done);
-      if (m) {
-        // the whole warp streams the finished lanes' spectra out, then refills them
-        // refill first: the new coefficients' global loads are in flight while
-        // the warp streams the finished spectra out (which reads the old
-        // index rows, so the new ones are stored afterwards)
-        refill(sl, m, done);
-        write_spectra<KL, OUT>(io, e - lane + sl * (L + kEmColExtra) * es, es, L, m, lane, gsm, eps);
-        __syncwarp();
-        if (done) e[(sl * (L + kEmColExtra) + L + 3) * es] = __longlong_as_double(idx[sl]);
+    }
+    if (TAIL && restart) {
+      x0 = io.xinit[idx];
+      x1 = io.xinit[io.n + idx];
+      x2 = io.xinit[2 * io.n + idx];
+    } else {
+      x0 = n0;
+      x1 = n1;
+      x2 = n2;
+    }
+    if constexpr (TAIL) wrestarts += __popc(__ballot_sync(0xffffffffu, restart));
+    const unsigned m = __ballot_sync(0xffffffffu, done);
+    if (m) {
+      // finished lanes take their prefetched coefficient and prefetch the
+      // next; then the whole warp streams the finished spectra out (their s
+      // rows and output offsets are still in the columns), and only then are
+      // the new offsets stored
+      const bool more = done && pidx >= 0;
+      const unsigned mm = __ballot_sync(0xffffffffu, more);
+      int64_t np = -1;
+      if (mm) np = assign(mm, more);
+      if (done) {
+        if (more) {
+          take();
+          pidx = np;
+          if (np >= 0) prefetch(np);
+        } else {
+          idx = -1;
+        }
       }
+      write_spectra<KL, OUT, es>(io, col - lane, L, m, lane, lterm);
+      __syncwarp();
+      if (done && idx >= 0) row(kColOff) = __longlong_as_double(out_row_offset<OUT>(io, idx, L));
     }
   }
   if (TAIL && io.stats && lane == 0) {
@@ -741,13 +751,13 @@ inline int launch_em(const DevOps& ops, EmIO io, cudaStream_t s, cudaEvent_t spl
   if constexpr (kCanLead) {
     if (lead) {
       auto tk = em_persistent_kernel<KL, OUT, true>;
-      if ((st = persistent_blocks(tk, smem, io.em_reserve, ceil_div(need_p, kEmSlots), blocks, kPersThreads))) return st;
+      if ((st = persistent_blocks(tk, smem, io.em_reserve, need_p, blocks, kPersThreads))) return st;
       tk<<<(unsigned)blocks, kPersThreads, smem, s>>>(ops, io);
       return check_launch("em_tail");
     }
   }
   auto kern = em_persistent_kernel<KL, OUT>;
-  if ((st = persistent_blocks(kern, smem, io.em_reserve, ceil_div(need_p, kEmSlots), blocks, kPersThreads))) return st;
+  if ((st = persistent_blocks(kern, smem, io.em_reserve, need_p, blocks, kPersThreads))) return st;
   kern<<<(unsigned)blocks, kPersThreads, smem, s>>>(ops, io);
   return check_launch("em_persistent");
 }
@@ -785,7 +795,7 @@ __global__ void __launch_bounds__(kXThreads, OXM_X_MIN_BLOCKS) em_exact_kernel(c
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, sub = lane & (kXLanes - 1), lead = lane & ~(kXLanes - 1);
-  const double eps = ops.eps, tol2 = ops.rel_tol * ops.rel_tol;
+  const double eps = ops.eps, tol2 = ops.rel_tol2;
   const int64_t count = io.sel ? (int64_t)*io.sel_count : io.n;
   int64_t idx = -1;
   int nfit = 1;
@@ -910,7 +920,7 @@ inline int launch_em_selected(const DevOps& ops, EmIO io, cudaStream_t s) {
     io.stats = nullptr;
     const size_t smem = em_smem_bytes(ops.L, kPersThreads);
     auto kern = em_persistent_kernel<KL, OUT>;
-    if ((st = persistent_blocks(kern, smem, 0, ceil_div(ceil_div(io.n, kPersThreads), kEmSlots), blocks, kPersThreads)))
+    if ((st = persistent_blocks(kern, smem, 0, ceil_div(io.n, kPersThreads), blocks, kPersThreads)))
       return st;
     kern<<<(unsigned)blocks, kPersThreads, smem, s>>>(ops, io);
   } else {

@@ -14,10 +14,9 @@ import sys
 
 ROOT = pathlib.Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
-VARIANTS = {  # name -> extra -D defines (occupancy knobs of the EM kernels)
+VARIANTS = {  # name -> extra -D defines (EM kernel knobs)
     "base": (),
-    "p640": ("OXM_PERS_THREADS=640", "OXM_TAIL_MIN_BLOCKS=1", "OXM_EM_MIN_BLOCKS=1"),
-    "p320": ("OXM_PERS_THREADS=320", "OXM_TAIL_MIN_BLOCKS=2", "OXM_EM_MIN_BLOCKS=2"),
+    "c64": ("OXM_EM_CHUNK=64",),
 }
 
 
