@@ -15,6 +15,8 @@
 // evaluation of `0.5 * (a + b - c - d)` so fp64 results are bit-identical.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 
 #include "oxm_common.cuh"
 #include "oxm_tma.cuh"
@@ -295,12 +297,33 @@ inline bool haar_tma_enabled() {
 
 // launches the TMA pass when the planes allow it (3 channels, 16-byte aligned
 // rows and plane bases, 32-bit in-plane indices); false = not launched
-template <typename T, int NL>
-bool launch_fwd_tma(const T* src, const FwdGeom& g, T* out, uint32_t* flags, cudaStream_t stream) {
-  using G = FwdTma<T, NL>;
-  if (!haar_tma_enabled() || g.C != 3) return false;
-  if (g.h[0] * g.w[0] * 3 >= ((int64_t)1 << 31)) return false;
+// Host cost of a launch: encoding the 4 NL + 1 tensor maps and the launch
+// configuration queries take longer than the 1080p kernel itself, so
+// back-to-back calls would leave the GPU idle between frames.  Both are
+// cached: the maps for the last kFwdMapCache (source, output, geometry) sets
+// (a video loop reuses its buffers), the shared-memory attribute and the
+// occupancy once per kernel instantiation and device.
+constexpr int kFwdMapCache = 16;
+struct FwdMapEntry {
+  const void* src = nullptr;
+  const void* out = nullptr;
+  FwdGeom g{};
+  int nl = 0, esz = 0;
   FwdMaps maps;
+};
+
+template <typename T, int NL>
+bool fwd_maps(const T* src, const FwdGeom& g, T* out, FwdMaps& maps) {
+  using G = FwdTma<T, NL>;
+  static std::mutex mu;
+  static FwdMapEntry cache[kFwdMapCache];
+  static int victim = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (const FwdMapEntry& e : cache)
+    if (e.src == src && e.out == out && e.nl == NL && e.esz == (int)sizeof(T) && !std::memcmp(&e.g, &g, sizeof(g))) {
+      maps = e.maps;
+      return true;
+    }
   const bool f64 = sizeof(T) == 8;
   if (!make_tmap_2d(&maps.in, src, f64, (uint64_t)(3 * g.w[0]), (uint64_t)g.h[0], (uint64_t)(3 * g.w[0] * sizeof(T)),
                     G::kRowE, G::kRows))
@@ -310,16 +333,61 @@ bool launch_fwd_tma(const T* src, const FwdGeom& g, T* out, uint32_t* flags, cud
       if (!make_tmap_2d(&maps.out[k - 1][q], out + g.off[k][q], f64, (uint64_t)(3 * g.w[k]), (uint64_t)g.h[k],
                         (uint64_t)(3 * g.w[k] * sizeof(T)), G::kRowE >> k, G::kRows >> k))
         return false;
+  FwdMapEntry& e = cache[victim];
+  victim = (victim + 1) % kFwdMapCache;
+  e.src = src;
+  e.out = out;
+  e.g = g;
+  e.nl = NL;
+  e.esz = (int)sizeof(T);
+  e.maps = maps;
+  return true;
+}
+
+// resident CTAs per SM of haar_fwd_tma_kernel<T, NL>, setting its
+// shared-memory attribute on first use per device; 0 = unusable.  (Templated
+// on the instantiation, not on the kernel's pointer type, which every
+// instantiation shares.)
+template <typename T, int NL>
+int fwd_tma_ctas_per_sm() {
+  using G = FwdTma<T, NL>;
   auto kern = haar_fwd_tma_kernel<T, NL>;
-  // per launch (the attribute is per function and device; a host call of a few us)
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::kSmem) != cudaSuccess) {
+  const int threads = G::kThreads;
+  const size_t smem = G::kSmem;
+  constexpr int kDevs = 64;
+  static std::mutex mu;
+  static int per_sm[kDevs] = {};  // 0 = not configured yet, -1 = failed
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kDevs) {
     cudaGetLastError();
-    return false;
+    return 0;
   }
+  std::lock_guard<std::mutex> lock(mu);
+  if (per_sm[dev] == 0) {
+    int n = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, threads, smem) != cudaSuccess || n < 1) {
+      cudaGetLastError();
+      n = -1;
+    }
+    per_sm[dev] = n;
+  }
+  return per_sm[dev] > 0 ? per_sm[dev] : 0;
+}
+
+// launches the TMA pass when the planes allow it (3 channels, 16-byte aligned
+// rows and plane bases, 32-bit in-plane indices); false = not launched
+template <typename T, int NL>
+bool launch_fwd_tma(const T* src, const FwdGeom& g, T* out, uint32_t* flags, cudaStream_t stream) {
+  using G = FwdTma<T, NL>;
+  if (!haar_tma_enabled() || g.C != 3) return false;
+  if (g.h[0] * g.w[0] * 3 >= ((int64_t)1 << 31)) return false;
+  auto kern = haar_fwd_tma_kernel<T, NL>;
+  const int per_sm = fwd_tma_ctas_per_sm<T, NL>();
+  if (per_sm < 1) return false;
+  FwdMaps maps;
+  if (!fwd_maps<T, NL>(src, g, out, maps)) return false;
   const int tiles_x = (int)ceil_div(g.w[NL], G::TX), tiles_y = (int)ceil_div(g.h[NL], G::TY);
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, G::kThreads, G::kSmem) != cudaSuccess || per_sm < 1)
-    return false;
   const int64_t grid = std::min<int64_t>((int64_t)tiles_x * tiles_y, (int64_t)device_sms() * per_sm);
   kern<<<(unsigned)grid, G::kThreads, G::kSmem, stream>>>(maps, g, flags, tiles_x, tiles_y);
   return true;
