@@ -86,21 +86,28 @@ def operators():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md): the
+    sampler runs every 20 ms and is up (first sample written) before the timed
+    region starts; `mark()` brackets the region in wall-clock time and the
+    summary keeps the samples whose nvidia-smi timestamps fall inside it (or,
+    for a region shorter than the sampling period, the first one after its
+    start)."""
 
     FIELD_SETS = [
         ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"),
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,timestamp"),
         ("index,clocks.sm,clocks.max.sm,power.draw,clocks_throttle_reasons.active,"
          "clocks_throttle_reasons.hw_slowdown,clocks_throttle_reasons.hw_thermal_slowdown,"
-         "clocks_throttle_reasons.sw_thermal_slowdown,clocks_throttle_reasons.sw_power_cap"),
+         "clocks_throttle_reasons.sw_thermal_slowdown,clocks_throttle_reasons.sw_power_cap,timestamp"),
     ]
+    PERIOD_MS = 20
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.t0 = self.t1 = None
 
     def _fields(self):
         for f in self.FIELD_SETS:
@@ -122,26 +129,44 @@ class ClockSampler:
             try:
                 self.proc = subprocess.Popen(
                     ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={fields}", "--format=csv,noheader,nounits",
-                     "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-                time.sleep(0.3)
+                     "-lms", str(self.PERIOD_MS)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                deadline = time.time() + 5.0  # wait for the sampler's first line (NVML start-up)
+                while time.time() < deadline and os.path.getsize(self.path) == 0:
+                    time.sleep(0.02)
             except OSError:
                 self.proc = None
         return self
 
+    def mark(self, start: bool) -> None:
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+
     def __exit__(self, *a):
         if self.proc is not None:
+            time.sleep(2 * self.PERIOD_MS / 1000)  # let the sample covering the region's end land
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    @staticmethod
+    def _ts(text: str):
+        import datetime
+
+        try:
+            return datetime.datetime.strptime(text.strip(), "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return None
+
     def summary(self) -> dict:
         rows = []
         try:
             for line in open(self.path):
                 parts = [x.strip() for x in line.split(",")]
-                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                if len(parts) >= 10 and parts[1].replace(".", "").isdigit():
                     rows.append(parts)
         except OSError:
             pass
@@ -152,11 +177,21 @@ class ClockSampler:
                 pass
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[1]) for r in rows]
+        window = rows
+        if self.t0 is not None and self.t1 is not None:
+            stamped = [(self._ts(r[9]), r) for r in rows]
+            window = [r for t, r in stamped if t is not None and self.t0 <= t <= self.t1]
+            if not window:  # region shorter than the sampling period: the first sample after its start
+                after = [r for t, r in stamped if t is not None and t >= self.t0]
+                window = after[:1] or rows[-1:]
+        sm = [float(r[1]) for r in window]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
-                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+        reasons = sorted({n for r in window for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        pw = [float(r[3]) for r in window if r[3].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(window[0][2]), "reasons": reasons,
+                "samples": len(window), "sample_period_ms": self.PERIOD_MS,
+                "window_s": round(self.t1 - self.t0, 4) if self.t0 is not None and self.t1 is not None else None,
+                "power_w_max": max(pw) if pw else None}
 
 
 # ---------------------------------------------------------------- inputs
@@ -535,11 +570,13 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev.index) as clk:
+        clk.mark(True)
         start.record(stream)
         for k in range(args.steps):
             eng.launch(frames, out, stage_events=ev[k])
         stop.record(stream)
         torch.cuda.synchronize()
+        clk.mark(False)
     if world > 1:
         dist.barrier()
     elapsed = start.elapsed_time(stop) * 1e-3
