@@ -250,6 +250,24 @@ def test_em_generic_band_count(cuda, rng):
         assert np.max(np.abs(cmap.stacked() - ref_x)) <= 1e-7, L
 
 
+def test_em_ragged_counts(cuda, sensitivity, basis, rng):
+    """Coefficient counts around the persistent kernel's warp / chunk / grid
+    boundaries (static first chunk per warp, 32-coefficient dynamic chunks,
+    per-lane prefetch of the next coefficient): every coefficient is processed
+    exactly once and matches the oracle."""
+    op = ox.TikhonovOperator.from_relative(sensitivity, 1e-3)
+    for n in (1, 31, 32, 33, 95, 129, 1000, 4099, 20000):
+        x0 = np.column_stack([rng.uniform(5, 60, n), rng.uniform(5, 60, n), rng.uniform(-0.2, 0.2, n)])
+        y = np.exp(-(x0 @ basis.xi.T)) @ sensitivity.c.T * rng.uniform(0.8, 1.2, (n, 1))
+        blk = y.reshape(1, n, 3)
+        spectra, cmap, fits = ox.estimate_lowpass_fits(ox.LowPassBlock(blk, 1.0), sensitivity, basis,
+                                                       ox.BayesConfig(), op)
+        ref_s, ref_x, ref_f = O.estimate_lowpass(blk, 1.0, sensitivity.c, basis.xi, op.solve)
+        assert np.array_equal(fits, ref_f), n
+        assert np.max(np.abs(spectra - ref_s) / np.maximum(np.abs(ref_s), 1e-3)) <= 1e-9, n
+        assert np.max(np.abs(cmap.stacked() - ref_x)) <= 1e-8, n
+
+
 def test_expectation_step_dense_oracle(cuda, rng, sensitivity):
     from paper_1706_07263_b200 import CameraSensitivity, WavelengthGrid
 
