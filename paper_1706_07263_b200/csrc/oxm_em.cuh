@@ -533,6 +533,7 @@ __global__ void __launch_bounds__(kPersThreads, TAIL ? OXM_TAIL_MIN_BLOCKS : OXM
           idx = -1;
         }
       }
+      __syncwarp();  // every lane's phase-B stores of s are visible to the warp
       write_spectra<KL, OUT, es>(io, col - lane, L, m, lane, lterm);
       __syncwarp();
       if (done && idx >= 0) row(kColOff) = __longlong_as_double(out_row_offset<OUT>(io, idx, L));
