@@ -106,9 +106,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // per-thread indexed LDCs feeding every DFMA.
 //
 // The final spectrum is not written by its own lane (a 26-store divergent
-// branch in almost every step): e stays in the lane's shared-memory column,
-// and when lanes finish the whole warp re-forms their s = max(e + G r, eps)
-// rows and writes them out together (write_spectra: coalesced).
+// branch in almost every step): phase B leaves s = max(e + G r, eps) in the
+// lane's shared-memory column, and when lanes finish the whole warp writes
+// their rows out together (write_spectra: coalesced).  The next coefficient's
+// inputs are already in the lane's column (cp.async prefetch), so a refill
+// does not wait on global memory.
 enum class SpecOut { kSoaF64, kAosF32HiLo, kAosF64 };
 
 struct EmIO {
