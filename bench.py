@@ -297,23 +297,13 @@ def parity_record(out, ref_outs: list, frames_idx: list) -> dict:
             "pass": flips == 0 and nan_eq and thb_rel <= 1e-4 and so2_abs <= 1e-5}
 
 
-def schedule_check(eng_all64, frames, out) -> dict:
+def schedule_check(eng, frames, out) -> dict:
     """Runtime flip detector for the EM precision schedule: the whole timed
-    batch through the all-fp64 EM schedule (em_lead=None), every low-pass
-    coefficient's fit count compared, maps compared (outside the timed region)."""
-    import torch
-
-    ref = eng_all64.run(frames, fits=True)
-    torch.cuda.synchronize()
-    flips = int((ref.fits != out.fits).sum().item())
-    rt = ref.thb.double()
-    nz = rt != 0
-    thb_rel = float(((out.thb.double() - rt).abs()[nz] / rt.abs()[nz]).max().item()) if bool(nz.any()) else 0.0
-    ok = ~torch.isnan(ref.so2)
-    so2_abs = float((out.so2[ok] - ref.so2[ok]).abs().max().item()) if bool(ok.any()) else 0.0
-    nan_eq = bool(torch.equal(torch.isnan(out.so2), torch.isnan(ref.so2)))
-    return {"vs": "all-fp64 EM schedule (em_lead=None) on the whole timed batch", "coefficients": int(out.fits.numel()),
-            "fit_count_flips": flips, "max_thb_rel": thb_rel, "max_so2_abs": so2_abs, "so2_nan_pattern_equal": nan_eq}
+    batch through the all-fp64 EM schedule (HybridMapEngine.audit), every
+    low-pass coefficient's fit count compared, maps compared (outside the
+    timed region)."""
+    return {"vs": "all-fp64 EM schedule (em_lead=None) on the whole timed batch (HybridMapEngine.audit)",
+            **eng.audit(frames, out)}
 
 
 def dropin_record(frames_host: np.ndarray, levels: int, n_seq: int) -> dict:
@@ -643,8 +633,7 @@ def run_ours(args):
         return
 
     # ---- correctness of what was timed (outside every timed region)
-    sched = schedule_check(ox.HybridMapEngine(sens, basis, ox.PipelineConfig(n_levels=n), device=dev, em_lead=None),
-                           frames, out)
+    sched = schedule_check(eng, frames, out)
     cpu = None
     sample = frames[:CPU_SAMPLE_FRAMES if world == 1 and not args.no_cpu else 1].cpu().numpy()
     if world == 1 and not args.no_cpu:

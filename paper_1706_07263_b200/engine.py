@@ -107,6 +107,8 @@ class HybridMapEngine:
                               "em_first_guard")
         self.em_lead = em_lead
         self._ws: torch.Tensor | None = None
+        self._audit_args = (sensitivity, basis, float(fallback_below))
+        self._audit_engine: HybridMapEngine | None = None
 
     # ---- workspace ---------------------------------------------------------
     def workspace_bytes(self, batch: int, height: int, width: int) -> int:
@@ -146,6 +148,33 @@ class HybridMapEngine:
         _native.check(st, "em_counters")
         return {"lead_fits": int(out[0]), "tail_fits": int(out[1]), "restarts": int(out[2]),
                 "exact_blocks": int(out[3]), "queued_px": int(out[4]), "deferred_px": int(out[5])}
+
+    def audit(self, frames: torch.Tensor, out: MapBatch) -> dict:
+        """Runtime check of the EM precision schedule on a batch this engine
+        has mapped: ``frames`` again through an all-fp64 EM engine (em_lead=None,
+        same operators and configuration; created on first use and kept), then
+        every low-pass coefficient's fit count (``out`` must come from
+        ``launch`` / ``run`` with ``fits=True``) and the maps compared.  Fit
+        counts equal the reference's exactly when this reports 0 flips (the
+        all-fp64 schedule is pinned to the oracle by the GPU tests).  Costs one
+        all-fp64 run of the batch; synchronises."""
+        if out.fits is None:
+            raise ArgumentError("audit needs the fit counts: allocate / run with fits=True")
+        if self._audit_engine is None:
+            sens, basis, fb = self._audit_args
+            self._audit_engine = HybridMapEngine(sens, basis, self.cfg, device=self.device, fallback_below=fb,
+                                                 em_lead=None)
+        ref = self._audit_engine.run(frames, fits=True)
+        torch.cuda.synchronize(self.device)
+        flips = int((ref.fits != out.fits).sum().item())
+        rt = ref.thb.double()
+        nz = rt != 0
+        thb_rel = float(((out.thb.double() - rt).abs()[nz] / rt.abs()[nz]).max().item()) if bool(nz.any()) else 0.0
+        ok = ~torch.isnan(ref.so2)
+        so2_abs = float((out.so2[ok] - ref.so2[ok]).abs().max().item()) if bool(ok.any()) else 0.0
+        return {"coefficients": int(out.fits.numel()), "fit_count_flips": flips, "max_thb_rel": thb_rel,
+                "max_so2_abs": so2_abs,
+                "so2_nan_pattern_equal": bool(torch.equal(torch.isnan(out.so2), torch.isnan(ref.so2)))}
 
     # ---- device-resident path ---------------------------------------------
     def launch(self, frames: torch.Tensor, out: MapBatch, *, stream: torch.cuda.Stream | None = None,

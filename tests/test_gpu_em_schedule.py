@@ -234,3 +234,20 @@ def test_schedule_knobs_and_debug_log(cuda, sensitivity, basis):
         assert np.all(r[i, 2:m] >= 1e-4 * (1 - 1e-5)), (i, r[i, :m + 1])
     ref = O.estimate_frame(rgb, sensitivity.c, basis.xi, n_levels=2, want_cube=False)
     assert np.array_equal(out.fits[0].cpu().numpy(), ref["fits"])
+
+
+def test_engine_audit(cuda, sensitivity, basis, textured):
+    """HybridMapEngine.audit: the runtime flip detector the bench line reports
+    (parity.schedule) as a product API."""
+    eng, out, _ = _run(cuda, sensitivity, basis, textured, 2, ox.engine.DEFAULT_EM_LEAD)
+    x = torch.from_numpy(textured.astype(np.float32)).to(cuda)
+    rep = eng.audit(x, out)
+    assert rep["coefficients"] == out.fits.numel()
+    assert rep["fit_count_flips"] == 0
+    assert rep["so2_nan_pattern_equal"]
+    assert rep["max_thb_rel"] < 1e-5 and rep["max_so2_abs"] < 5e-6
+    # a flip is reported as one
+    out.fits.view(-1)[7] += 1
+    assert eng.audit(x, out)["fit_count_flips"] == 1
+    with pytest.raises(ox.ArgumentError):
+        eng.audit(x, eng.allocate(*textured.shape[:3]))
