@@ -23,7 +23,8 @@ import sys
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 
 
-def main():
+def run(cases: int, seed: int, emit=print) -> dict:
+    """Run the sweep; emit(json line) per case; returns the summary."""
     import numpy as np
     import torch
 
@@ -31,8 +32,7 @@ def main():
     from oracle import oximap_oracle as O
     from paper_1706_07263_b200 import fixtures, synth
 
-    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
-    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2024)
+    rng = np.random.default_rng(seed)
     dev = torch.device("cuda", 0)
     sens, basis = fixtures.default_sensitivity(), fixtures.default_basis()
     engines = {}
@@ -80,8 +80,16 @@ def main():
         ok &= flips == 0
         rec.update({"fit_count_flips": flips, "max_thb_rel": trel, "max_so2_abs": sabs, "pass": bool(ok)})
         fails += not ok
-        print(json.dumps(rec), flush=True)
-    print(json.dumps({"summary": True, "cases": cases, "failed": fails, "worst": worst}), flush=True)
+        emit(json.dumps(rec))
+    summary = {"summary": True, "cases": cases, "failed": fails, "worst": worst}
+    emit(json.dumps(summary))
+    return summary
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 2024
+    run(cases, seed, emit=lambda line: print(line, flush=True))
 
 
 if __name__ == "__main__":
