@@ -276,12 +276,25 @@ def _sequence_plain(frames, sensitivity, basis, cfg, timings):
 _COPY_POOL = None
 
 
+def _copy_threads() -> int:
+    """Host copy threads: OXM_COPY_THREADS, default min(8, cores / 2) (on a
+    16-core B200 host: 2 / 4 / 8 / 16 threads gave 144 / 223 / 263 / 233
+    estimate_sequence frames/s, tools/seq_probe.py)."""
+    import os
+
+    default = max(2, min(8, (os.cpu_count() or 4) // 2))
+    try:
+        return max(1, int(os.environ.get("OXM_COPY_THREADS", default)))
+    except ValueError:
+        return default
+
+
 def _copy_pool():
     global _COPY_POOL
     if _COPY_POOL is None:
         from concurrent.futures import ThreadPoolExecutor
 
-        _COPY_POOL = ThreadPoolExecutor(max_workers=4, thread_name_prefix="oxm-copy")
+        _COPY_POOL = ThreadPoolExecutor(max_workers=_copy_threads(), thread_name_prefix="oxm-copy")
     return _COPY_POOL
 
 
@@ -292,7 +305,7 @@ def _par_copy(pairs) -> None:
     jobs = []
     for dst, src in pairs:
         rows = dst.shape[0]
-        step = max(1, -(-rows // 4))
+        step = max(1, -(-rows // _copy_threads()))
         for r in range(0, rows, step):
             jobs.append(_copy_pool().submit(np.copyto, dst[r : r + step], src[r : r + step]))
     for j in jobs:
