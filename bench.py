@@ -743,7 +743,7 @@ FP64_INST_PER_FIT = 726.0
 FLOPS_PER_FIT = 1260.0
 MUFU_PER_LEAD_FIT = 2 * 26  # fp32 lead-in: one ex2 and one lg2 per band
 CPU_OTHER_FRAMES = 3   # frames for the slower reference thread setting (threads=1, BLAS=nproc)
-DROPIN_SEQ_FRAMES = 8
+DROPIN_SEQ_FRAMES = 16
 # kernels launched per step: zero_counters, ll_tma (+ fit #1), em_lead, em_persistent (tail),
 # px_f32 (+ in-warp fp64 fallback), exact pass, px_fallback (deferred)
 HybridMapLaunches = 7
