@@ -12,7 +12,7 @@ drop-in estimate_frame, and compares every frame with the oracle
     largest magnitude (values reach several hundred g/l in textured frames).
 One JSON line per case, then a summary line.
 
-    python tools/parity_fuzz.py [CASES] [SEED]
+    python tools/parity_fuzz.py [CASES] [SEED] [MAX_SIDE]
 """
 from __future__ import annotations
 
@@ -23,7 +23,7 @@ import sys
 sys.path.insert(0, str(pathlib.Path(__file__).resolve().parents[1]))
 
 
-def run(cases: int, seed: int, emit=print) -> dict:
+def run(cases: int, seed: int, emit=print, max_side: int = 320) -> dict:
     """Run the sweep; emit(json line) per case; returns the summary."""
     import numpy as np
     import torch
@@ -39,7 +39,7 @@ def run(cases: int, seed: int, emit=print) -> dict:
     worst = {"thb_rel": 0.0, "so2_abs": 0.0, "cube_abs": 0.0, "x_abs": 0.0}
     fails = 0
     for case in range(cases):
-        H, W = int(rng.integers(8, 321)), int(rng.integers(8, 321))
+        H, W = int(rng.integers(8, max_side + 1)), int(rng.integers(8, max_side + 1))
         nmax = max(1, min(4, int(np.floor(np.log2(min(H, W))))))
         n = int(rng.integers(1, nmax + 1))
         B = int(rng.integers(1, 5))
@@ -89,7 +89,8 @@ def run(cases: int, seed: int, emit=print) -> dict:
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 2024
-    run(cases, seed, emit=lambda line: print(line, flush=True))
+    max_side = int(sys.argv[3]) if len(sys.argv) > 3 else 320
+    run(cases, seed, emit=lambda line: print(line, flush=True), max_side=max_side)
 
 
 if __name__ == "__main__":
