@@ -52,7 +52,7 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--batch", type=int, default=64, help="frames per step per GPU")
+    p.add_argument("--batch", type=int, default=DEFAULT_BATCH, help="frames per step per GPU")
     p.add_argument("--height", type=int, default=1080)
     p.add_argument("--width", type=int, default=1920)
     p.add_argument("--levels", type=int, default=2)
@@ -731,7 +731,7 @@ def run_ours(args):
 
 # EM tail work per fp64 fit, measured rather than assumed: ncu's
 # SASS-level thread-instruction counts of the tail launch of this exact bench
-# batch (64 frames; tools/ncu_thread_counts.py -> profiles/r02_em_tail_sass_counts.txt)
+# batch (tools/ncu_thread_counts.py -> profiles/r02_em_tail_sass_counts.txt)
 # divided by its 30,300,894 fits -- DFMA + DADD + DMUL + DSETP = 726.0
 # fp64-pipe instructions per fit, 1260.0 flops (FMA = 2).  Per band that is the
 # exp (DADD + 3 DFMA + DMUL + DFMA), its argument (2 DFMA), C e (3 DFMA),
@@ -744,6 +744,10 @@ FLOPS_PER_FIT = 1260.0
 MUFU_PER_LEAD_FIT = 2 * 26  # fp32 lead-in: one ex2 and one lg2 per band
 CPU_OTHER_FRAMES = 3   # frames for the slower reference thread setting (threads=1, BLAS=nproc)
 DROPIN_SEQ_FRAMES = 16
+DEFAULT_BATCH = 128
+# frames per step per GPU: 64 / 128 / 256 frames per launch measured 12.86 / 13.04 /
+# 13.14 k fps (fewer kernel ramp-ups and drains per frame); 128 keeps the
+# N = 8 gather to rank 0 at 17 GB per step
 # kernels launched per step: zero_counters, ll_tma (+ fit #1), em_lead, em_persistent (tail),
 # px_f32 (+ in-warp fp64 fallback), exact pass, px_fallback (deferred)
 HybridMapLaunches = 7

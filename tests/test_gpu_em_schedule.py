@@ -168,8 +168,8 @@ def test_schedule_extreme_exposure(cuda, sensitivity, basis, gain):
 
 
 def test_bench_configuration_vs_oracle(cuda, sensitivity, basis):
-    """The bench's own workload (bench.py: 64 device-synthesised textured 1080p
-    frames, n = 2) through the engine exactly as timed: 8.3 M low-pass
+    """The bench's own workload (bench.py: DEFAULT_BATCH = 128 device-synthesised
+    textured 1080p frames, n = 2) through the engine exactly as timed: 16.6 M low-pass
     coefficients, so the exact-block pass runs the one-lane persistent kernel
     over the selection list (kExactSeqMinN = 2^21).  One frame of each of the
     four truth maps, plus the last frame, against the pinned oracle: fit counts
@@ -178,7 +178,7 @@ def test_bench_configuration_vs_oracle(cuda, sensitivity, basis):
     schedule (em_lead=None): 0 fit-count differences."""
     import bench
 
-    B, H, W = 64, 1080, 1920
+    B, H, W = bench.DEFAULT_BATCH, 1080, 1920
     frames = bench.make_frames(B, H, W, 0.3, 0, cuda)
     eng = ox.HybridMapEngine(sensitivity, basis, ox.PipelineConfig(n_levels=2))
     out = eng.run(frames, fits=True)
@@ -191,7 +191,7 @@ def test_bench_configuration_vs_oracle(cuda, sensitivity, basis):
     assert flips == 0, f"{flips} fit-count differences vs the all-fp64 schedule over {nll} coefficients"
     thb, so2, fits = out.thb.cpu().numpy(), out.so2.cpu().numpy(), out.fits.cpu().numpy()
     host = frames.cpu().numpy().astype(np.float64)
-    for b in (0, 16, 32, 48, 63):
+    for b in (0, 16, 32, 48, B - 1):
         ref = O.estimate_frame(host[b], sensitivity.c, basis.xi, n_levels=2, want_cube=False,
                                threads=O.default_threads())
         assert np.array_equal(fits[b], ref["fits"]), f"frame {b}: {np.sum(fits[b] != ref['fits'])} fit-count flips"

@@ -30,7 +30,7 @@ def launches(path: str) -> str:
             agg[name].append(t)
     tot = sum(sum(v) for v in agg.values())
     out = ["ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --steps 2 --warmup 1 --no-cpu --no-dropin",
-           "(cold-cache, serialised launches: compare SHARES; the two timed steps of 64 frames 1080p n=2, cut at",
+           "(cold-cache, serialised launches: compare SHARES; the two timed steps of the bench batch (1080p n=2), cut at",
            " zero_counters; warm-up, input staging, gathered leg, e2e and the schedule check excluded)",
            f"{'kernel':70s} {'n':>3} {'mean ns':>12} {'share':>7}"]
     for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
