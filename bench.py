@@ -732,15 +732,15 @@ def run_ours(args):
 # EM tail work per fp64 fit, measured rather than assumed: ncu's
 # SASS-level thread-instruction counts of the tail launch of this exact bench
 # batch (tools/ncu_thread_counts.py -> profiles/r02_em_tail_sass_counts.txt)
-# divided by its 30,300,894 fits -- DFMA + DADD + DMUL + DSETP = 726.0
-# fp64-pipe instructions per fit, 1260.0 flops (FMA = 2).  Per band that is the
+# divided by its 60,605,987 fits -- DFMA + DADD + DMUL + DSETP = 714.3
+# fp64-pipe instructions per fit, 1239.4 flops (FMA = 2).  Per band that is the
 # exp (DADD + 3 DFMA + DMUL + DFMA), its argument (2 DFMA), C e (3 DFMA),
 # e + G r (3 DFMA), the eps clamp (DSETP), the table log (DFMA + 3 DFMA + DMUL
 # + 2 DFMA + DADD) and the fit (3 DFMA), plus the per-step norms.  `frac` =
 # fp64-pipe instructions issued / the DFMA probe's rate, the quantity ncu
 # reports as sm__inst_executed_pipe_fp64.
-FP64_INST_PER_FIT = 726.0
-FLOPS_PER_FIT = 1260.0
+FP64_INST_PER_FIT = 714.3
+FLOPS_PER_FIT = 1239.4
 MUFU_PER_LEAD_FIT = 2 * 26  # fp32 lead-in: one ex2 and one lg2 per band
 CPU_OTHER_FRAMES = 3   # frames for the slower reference thread setting (threads=1, BLAS=nproc)
 DROPIN_SEQ_FRAMES = 16
