@@ -43,6 +43,9 @@
 #ifndef OXM_X_MIN_BLOCKS
 #define OXM_X_MIN_BLOCKS 1
 #endif
+#ifndef OXM_LEAD_REVERSE
+#define OXM_LEAD_REVERSE 1  // lead-in takes coefficients last-first (L2 reuse of the low-pass outputs)
+#endif
 #ifndef OXM_EM_MIN_BLOCKS
 #define OXM_EM_MIN_BLOCKS 5
 #endif
@@ -595,7 +598,13 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
     x2 = (float)io.xinit[2 * io.n + i];
     nfit = 1;
   };
-  if (idx >= 0) load(idx);
+  // positions map to coefficients last-first (OXM_LEAD_REVERSE): the low-pass
+  // kernel wrote the last frames' ybar / x_init last, so those are the ones
+  // still in L2 when this kernel starts (128 frames: 18.75 -> 18.11 us/frame);
+  // the fp64 tail then walks forward and starts on the hand-over states this
+  // kernel wrote last
+  auto cof = [&](int64_t p) -> int64_t { return OXM_LEAD_REVERSE ? io.n - 1 - p : p; };
+  if (idx >= 0) load(cof(idx));
   next = stop;
 
   // bands l, l+1 share one packed FFMA2 (two partial sums per accumulator,
@@ -658,12 +667,13 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
         ++nfit;
       } else {
         done = true;
+        const int64_t c = cof(idx);
         if (nfit > 1) {
-          io.xh[idx] = x0;
-          io.xh[io.n + idx] = x1;
-          io.xh[2 * io.n + idx] = x2;
+          io.xh[c] = x0;
+          io.xh[io.n + c] = x1;
+          io.xh[2 * io.n + c] = x2;
         }
-        io.fits[idx] = nfit;
+        io.fits[c] = nfit;
       }
     }
     const unsigned m = __ballot_sync(0xffffffffu, done);
@@ -684,7 +694,7 @@ __global__ void __launch_bounds__(kEmThreads) em_lead_kernel(const __grid_consta
         const int r = __popc(m & lt_mask);
         const int64_t mine = r < avail ? next + r : fresh + (r - avail);
         idx = mine < (r < avail ? stop : fresh_end) ? mine : -1;
-        if (idx >= 0) load(idx);
+        if (idx >= 0) load(cof(idx));
       }
       if (avail < need) {
         next = fresh_end > fresh ? min64(fresh + (need - avail), fresh_end) : fresh_end;
