@@ -403,25 +403,41 @@ def probe_peaks(lib, torch, dev):
 
 
 def copy_bandwidth(torch, dev) -> dict:
-    """Pinned H2D / D2H GB/s with both directions running at once (the e2e
-    roofline: the engine's pipeline overlaps them), 512 MiB per copy, best of
-    3 rounds (tools/pcie_probe.py measures each direction alone too)."""
+    """Pinned H2D / D2H GB/s, each direction alone and both running at once
+    (512 MiB per copy, best of 3 rounds; tools/pcie_probe.py has the full
+    probe).  The e2e bound is the best schedule of a step's copies: both
+    directions at the concurrent rate while both have bytes left, the
+    remainder of the larger one at its alone rate."""
     n = 512 * 2**20
     h_in, h_out = torch.empty(n, dtype=torch.uint8).pin_memory(), torch.empty(n, dtype=torch.uint8).pin_memory()
     d_a, d_b = torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.uint8, device=dev)
     s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    best = 0.0
-    for rep in range(3):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(4):
-            with torch.cuda.stream(s1):
-                d_a.copy_(h_in, non_blocking=True)
-            with torch.cuda.stream(s2):
-                h_out.copy_(d_b, non_blocking=True)
-        torch.cuda.synchronize()
-        best = max(best, 4 * n / (time.perf_counter() - t0) / 1e9)
-    return {"h2d_gbs": best, "d2h_gbs": best}
+
+    def rate(h2d: bool, d2h: bool) -> float:
+        best = 0.0
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(4):
+                if h2d:
+                    with torch.cuda.stream(s1):
+                        d_a.copy_(h_in, non_blocking=True)
+                if d2h:
+                    with torch.cuda.stream(s2):
+                        h_out.copy_(d_b, non_blocking=True)
+            torch.cuda.synchronize()
+            best = max(best, 4 * n / (time.perf_counter() - t0) / 1e9)
+        return best
+
+    return {"h2d_alone_gbs": rate(True, False), "d2h_alone_gbs": rate(False, True), "concurrent_gbs": rate(True, True)}
+
+
+def pcie_bound(frames: float, h2d_bytes: float, d2h_bytes: float, bw: dict) -> float:
+    """Frames/s if a step's copies ran at the measured rates (compute hidden)."""
+    both = min(h2d_bytes, d2h_bytes)
+    rest_rate = bw["h2d_alone_gbs"] if h2d_bytes >= d2h_bytes else bw["d2h_alone_gbs"]
+    t = both / (bw["concurrent_gbs"] * 1e9) + abs(h2d_bytes - d2h_bytes) / (rest_rate * 1e9)
+    return frames / t
 
 
 def init_dist(args):
@@ -621,11 +637,10 @@ def run_ours(args):
                           "api": "maps_from_host(uint16 PPM counts) -> oxm_hybrid_maps_u16"}
         bw = copy_bandwidth(torch, dev)
         for rec in (e2e, e2e["ppm_u16"]):
-            bound = world * B / max(rec["h2d_bytes_per_step"] / (bw["h2d_gbs"] * 1e9),
-                                    rec["d2h_bytes_per_step"] / (bw["d2h_gbs"] * 1e9))
+            bound = world * pcie_bound(B, rec["h2d_bytes_per_step"], rec["d2h_bytes_per_step"], bw)
             rec["pcie_bound"] = bound
             rec["frac_of_pcie_bound"] = rec["value"] / bound
-        e2e["copy_bandwidth_concurrent"] = bw
+        e2e["copy_bandwidth"] = bw
 
     if rank != 0:
         if world > 1:
